@@ -1,0 +1,171 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations.
+
+No public dataset is involved: every array comes from
+``numpy.random.default_rng(seed)`` (seed = config number unless stated) so
+the oracle and the GPU see identical inputs.  Choices the BASELINE leaves
+open are fixed here and recorded in DESIGN.md §6:
+
+* distortion weight kappa = 1e-3, eps = 1e-8;
+* config 1: strip [0,1] x [0,1/64], 64 x 1 cells (128 triangles), steady
+  Burgers (u^2/2)_x = mu u with u(0)=1, u(1)=-0.5 (laws.burgers_strip);
+* configs 3-5: annular sector r in [0.5, 1.5] around a half cylinder;
+* mesh displacement modes: integer wave numbers in [1, 4], random phase and
+  direction, amplitude 0.05 h (h = smallest edge spacing of the grid).
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import laws as L
+from .mesh import Geometry, build_box_mesh, build_sector_mesh
+
+KAPPA = 1e-3
+EPS = 1e-8
+
+
+@dataclass
+class DistortionConfig:
+    """Mirror of strom.distortion.DistortionConfig (distortion.py:19-26)."""
+
+    kappa: float
+    eps: float = 1e-8
+
+    def __post_init__(self):
+        if self.kappa <= 0.0 or self.eps <= 0.0:
+            raise ValueError("kappa and eps must be positive")
+
+
+@dataclass
+class Case:
+    name: str
+    law: object
+    mesh: object
+    maps: object
+    quad_order: int
+    phi: np.ndarray
+    psi: np.ndarray
+    ref_coords: np.ndarray
+    mus: np.ndarray                 # (P, n_mu)
+    W: np.ndarray                   # (P, k_u)
+    Tau: np.ndarray                 # (P, k_x)
+    rho: np.ndarray = None          # (ne,) or None (all ones, reduced.py:134-141)
+    state_offset: np.ndarray = None
+    kappa: float = KAPPA
+    eps: float = EPS
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def geom(self):
+        return Geometry(self.mesh, self.maps, self.quad_order)
+
+    @property
+    def dist(self):
+        return DistortionConfig(self.kappa, self.eps)
+
+
+def orthonormal(rng, n, k, first=None):
+    A = rng.standard_normal((n, k))
+    if first is not None:
+        A[:, 0] = first
+    Q, R = np.linalg.qr(A)
+    return Q * np.sign(np.diag(R))[None, :]
+
+
+def eqp_weights(rng, ne, n_active, scale):
+    act = np.sort(rng.choice(ne, n_active, replace=False))
+    rho = np.zeros(ne)
+    rho[act] = rng.uniform(0.5, 2.0, n_active) * scale
+    return rho
+
+
+def displacement(rng, nodes, h, n_modes=4, amp=0.05):
+    d = np.zeros_like(nodes)
+    for _ in range(n_modes):
+        kx, ky = rng.integers(1, 5, size=2)
+        ph = rng.uniform(0, 2 * np.pi)
+        th = rng.uniform(0, 2 * np.pi)
+        s = np.sin(2 * np.pi * (kx * nodes[:, 0] + ky * nodes[:, 1]) + ph)
+        d[:, 0] += amp * h * np.cos(th) * s
+        d[:, 1] += amp * h * np.sin(th) * s
+    return d
+
+
+def freestream_field(rng, ne, nb, mach, gamma=1.4, jitter=0.05):
+    """Freestream times (1 + U(-jitter, jitter)), one factor per DG node."""
+    ff = L.euler_freestream(mach, gamma)
+    fac = 1.0 + rng.uniform(-jitter, jitter, size=(ne, nb, 1))
+    return (fac * ff[None, None, :]).reshape(-1)
+
+
+# -- config 1 -----------------------------------------------------------------------
+def strip_case(ncell=64, ku=4, kx=2, n_active=10, P=8, seed=1, quad_order=None):
+    mesh, maps = build_box_mesh(((0.0, 0.0), (1.0, 1.0 / ncell)), ncell, 1, degree_sol=2, n_comp=1)
+    rng = np.random.default_rng(seed)
+    phi = orthonormal(rng, maps.n_global_state, ku)
+    psi = orthonormal(rng, maps.n_global_coord, kx)
+    rho = eqp_weights(rng, mesh.num_elements, n_active, mesh.num_elements / n_active)
+    mus = rng.uniform(1.0, 3.0, size=(P, 1))
+    return Case("cfg1-strip", L.burgers_strip(), mesh, maps, quad_order, phi, psi, mesh.nodes.ravel().copy(),
+                mus, np.zeros((P, ku)), np.zeros((P, kx)), rho)
+
+
+# -- config 2 -----------------------------------------------------------------------
+def euler_square_case(n=256, ku=16, kx=8, seed=2, mach=2.0, quad_order=6):
+    """Element microbench: unit square, 2 n^2 triangles, explicit (U, x) fields.
+
+    The state and deformed coordinates enter as the affine offsets of the
+    reduced parametrisation (U = U0 + Phi w, x = x_field + Psi tau) at
+    w = 0, tau = 0, so the reduced Jacobian is evaluated at the given fields
+    with tangents seeded by Phi and Psi (SURVEY §8c iv).
+    """
+    mesh, maps = build_box_mesh(((0.0, 0.0), (1.0, 1.0)), n, n, degree_sol=2, n_comp=4)
+    rng = np.random.default_rng(seed)
+    nb = 6
+    U0 = freestream_field(rng, mesh.num_elements, nb, mach)
+    x = (mesh.nodes + displacement(rng, mesh.nodes, 1.0 / n)).ravel()
+    phi = orthonormal(rng, maps.n_global_state, ku)
+    psi = orthonormal(rng, maps.n_global_coord, kx)
+    law = L.euler(tags={t: "freestream" for t in ("left", "right", "bottom", "top")})
+    return Case("cfg2-euler-square", law, mesh, maps, quad_order, phi, psi, x, np.array([[mach]]),
+                np.zeros((1, ku)), np.zeros((1, kx)), None, U0)
+
+
+# -- configs 3-5 (half cylinder) -----------------------------------------------------------
+SECTOR_BCS = {"inflow": "freestream", "outflow": "extrapolate", "wall": "extrapolate"}
+
+
+def sector_rom_case(n_radial=100, n_circ=200, ku=20, kx=10, frac_active=0.02, rho_scale=50.0, P=64, seed=3,
+                    quad_order=6, name="cfg3-half-cylinder"):
+    mesh, maps = build_sector_mesh(n_radial, n_circ, degree_sol=2, n_comp=4)
+    rng = np.random.default_rng(seed)
+    ne = mesh.num_elements
+    ff = np.tile(L.euler_freestream(3.0), ne * 6)
+    phi = orthonormal(rng, maps.n_global_state, ku, first=ff / np.linalg.norm(ff))
+    psi = orthonormal(rng, maps.n_global_coord, kx)
+    n_act = max(1, int(round(frac_active * ne)))
+    rho = eqp_weights(rng, ne, n_act, rho_scale)
+    mus = rng.uniform(2.0, 4.0, size=(P, 1))
+    w0 = phi.T @ ff
+    law = L.euler(tags=SECTOR_BCS)
+    return Case(name, law, mesh, maps, quad_order, phi, psi, mesh.nodes.ravel().copy(), mus,
+                np.tile(w0, (P, 1)), np.zeros((P, kx)), rho)
+
+
+def cfg3():
+    return sector_rom_case()
+
+
+def cfg5_rom(P=1024):
+    return sector_rom_case(200, 400, 24, 12, 0.03, 100.0 / 3.0, P, seed=5, name="cfg5-greedy")
+
+
+def snapshot_fields(case, S, seed, mach_range=(2.0, 4.0)):
+    """Training snapshots for config 4: perturbed freestream states and meshes."""
+    rng = np.random.default_rng(seed)
+    mesh = case.mesh
+    h = (1.5 - 0.5) / max(1, int(round(np.sqrt(mesh.num_elements / 2))))
+    mus = rng.uniform(*mach_range, size=(S, 1))
+    U = np.stack([freestream_field(rng, mesh.num_elements, 6, m[0]) for m in mus])
+    X = np.stack([(mesh.nodes + displacement(rng, mesh.nodes, h)).ravel() for _ in range(S)])
+    return mus, U, X

@@ -1,0 +1,75 @@
+// Shared definitions for the B200 element kernels (see element_kernels.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "laws.cuh"
+
+namespace strom {
+
+constexpr int KMAX = 40;      // max k_u + k_x (padded Gram dimension <= 40)
+constexpr int KXMAX = 16;     // max k_x
+constexpr int NMU = 4;        // max parameters per mu vector
+constexpr int DERIV_THREADS = 128;
+
+enum Mode {
+  MODE_OBJECTIVE = 0, MODE_DERIVS = 1, MODE_CONTRIB = 2, MODE_CONTRIB_SPLIT = 3,
+  MODE_RESIDUAL = 4, MODE_RESNORM2 = 5, MODE_CONTRIB_LPROWS = 6
+};
+
+// reference-element constants; lives in the kernel parameter (constant) bank
+template <int NB, int NQ, int NS, int NF>
+struct Tabs {
+  double phi[NQ][NB];
+  double dphi[NQ][NB][2];
+  double wq[NQ];
+  double bary[NQ][3];
+  double trace[3][NS][NF];
+  double ws[NS];
+  double wsum;
+  int fnode[3][NF];
+};
+
+struct Run {
+  // mesh
+  int ne;
+  const int* __restrict__ elem_nodes;
+  const double* __restrict__ nodes;
+  const int* __restrict__ nbr;
+  const uint8_t* __restrict__ finfo;
+  const double* __restrict__ eta_ref;
+  // bases
+  const double* __restrict__ phi;
+  const double* __restrict__ psi;
+  const double* __restrict__ xref;
+  const double* __restrict__ u0;
+  int ku, kx, K, KP, LDJ;
+  // call
+  const double* __restrict__ w;
+  const double* __restrict__ tau;
+  const double* __restrict__ mu;
+  int nmu, P;
+  const int* __restrict__ active;
+  const double* __restrict__ rho;
+  int A;
+  double* __restrict__ out;
+  double* __restrict__ part;
+  int* __restrict__ degen;
+  int* __restrict__ degen_list;
+  int degen_cap;
+  int* __restrict__ degen_fill;
+  int mode;
+  int U;          // units per tile (derivs kernel)
+  int ntiles;     // tiles per parameter
+  int gx;         // blocks per parameter
+  int unit_stride;  // doubles per unit in shared memory
+  double kappa, eps;
+  double lawp[8];
+};
+
+template <int NB, int NQ, int NS, int NF>
+struct Params {
+  Tabs<NB, NQ, NS, NF> t;
+  Run r;
+};
+
+}  // namespace strom

@@ -1,0 +1,198 @@
+// Compiled conservation laws for the B200 element kernels.
+//
+// Each law is the device restatement of one reference plugin
+// (ConservationLawSpec, strom/conslaw.py:32-57): pointwise flux f(u) (m x 2),
+// source s(pos, u), LLF wavespeed ws(u, nhat) and the prescribed ghost states.
+// Functions are templated on the scalar so the same code yields values
+// (T = double) and exact pointwise Jacobians (T = Dn<N>, forward mode with N
+// seeded directions) — the pointwise analogue of strom/dual.py, used only on
+// per-point quantities; the per-tangent work in the kernels is explicit
+// linear algebra on those Jacobians.
+#pragma once
+#include <cstdint>
+
+namespace strom {
+
+template <int N>
+struct Dn {
+  double v;
+  double d[N];
+};
+
+// ---- scalar helpers overloaded for double and Dn<N> -------------------------
+__device__ __forceinline__ double val(double x) { return x; }
+template <int N> __device__ __forceinline__ double val(const Dn<N>& x) { return x.v; }
+
+template <int N> __device__ __forceinline__ Dn<N> cst(double c) {
+  Dn<N> r; r.v = c;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = 0.0;
+  return r;
+}
+template <int N> __device__ __forceinline__ Dn<N> seed(double v, int k) {
+  Dn<N> r = cst<N>(v); r.d[k] = 1.0; return r;
+}
+template <int N> __device__ __forceinline__ Dn<N> operator+(const Dn<N>& a, const Dn<N>& b) {
+  Dn<N> r; r.v = a.v + b.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] + b.d[i];
+  return r;
+}
+template <int N> __device__ __forceinline__ Dn<N> operator-(const Dn<N>& a, const Dn<N>& b) {
+  Dn<N> r; r.v = a.v - b.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] - b.d[i];
+  return r;
+}
+template <int N> __device__ __forceinline__ Dn<N> operator-(const Dn<N>& a) {
+  Dn<N> r; r.v = -a.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = -a.d[i];
+  return r;
+}
+template <int N> __device__ __forceinline__ Dn<N> operator*(const Dn<N>& a, const Dn<N>& b) {
+  Dn<N> r; r.v = a.v * b.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] * b.v + a.v * b.d[i];
+  return r;
+}
+template <int N> __device__ __forceinline__ Dn<N> operator/(const Dn<N>& a, const Dn<N>& b) {
+  Dn<N> r; const double inv = 1.0 / b.v; r.v = a.v * inv;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = (a.d[i] - r.v * b.d[i]) * inv;
+  return r;
+}
+template <int N> __device__ __forceinline__ Dn<N> operator+(const Dn<N>& a, double c) { Dn<N> r = a; r.v += c; return r; }
+template <int N> __device__ __forceinline__ Dn<N> operator+(double c, const Dn<N>& a) { return a + c; }
+template <int N> __device__ __forceinline__ Dn<N> operator-(const Dn<N>& a, double c) { Dn<N> r = a; r.v -= c; return r; }
+template <int N> __device__ __forceinline__ Dn<N> operator-(double c, const Dn<N>& a) { Dn<N> r = -a; r.v += c; return r; }
+template <int N> __device__ __forceinline__ Dn<N> operator*(const Dn<N>& a, double c) {
+  Dn<N> r; r.v = a.v * c;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] * c;
+  return r;
+}
+template <int N> __device__ __forceinline__ Dn<N> operator*(double c, const Dn<N>& a) { return a * c; }
+template <int N> __device__ __forceinline__ Dn<N> operator/(const Dn<N>& a, double c) {
+  Dn<N> r; r.v = a.v / c;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = a.d[i] / c;
+  return r;
+}
+
+__device__ __forceinline__ double dsqrt(double x) { return sqrt(x); }
+template <int N> __device__ __forceinline__ Dn<N> dsqrt(const Dn<N>& a) {
+  Dn<N> r; r.v = sqrt(a.v); const double h = 0.5 / r.v;
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = h * a.d[i];
+  return r;
+}
+__device__ __forceinline__ double dexp(double x) { return exp(x); }
+template <int N> __device__ __forceinline__ Dn<N> dexp(const Dn<N>& a) {
+  Dn<N> r; r.v = exp(a.v);
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = r.v * a.d[i];
+  return r;
+}
+// |x| with sign(0) = 0 for the tangent (strom/dual.py:161-163)
+__device__ __forceinline__ double dabs(double x) { return fabs(x); }
+template <int N> __device__ __forceinline__ Dn<N> dabs(const Dn<N>& a) {
+  Dn<N> r; r.v = fabs(a.v); const double sg = a.v > 0.0 ? 1.0 : (a.v < 0.0 ? -1.0 : 0.0);
+#pragma unroll
+  for (int i = 0; i < N; ++i) r.d[i] = sg * a.d[i];
+  return r;
+}
+
+enum SrcKind { SRC_NONE = 0, SRC_POS = 1, SRC_U = 2 };
+
+struct LawArgs {
+  double p[8];   // law constants
+  double mu[4];  // parameter vector of the current unit
+};
+
+// ---------------------------------------------------------------------------
+// linear advection, conslaw.py:174-253 (no manufactured solution)
+struct LinAdv {
+  static constexpr int M = 1;
+  static constexpr int SRC = SRC_NONE;
+  template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
+    f[0][0] = a.p[0] * u[0];
+    f[0][1] = a.p[1] * u[0];
+  }
+  template <class T> __device__ static void source(const T* pos, const T* u, T* s, const LawArgs& a) {
+    s[0] = 0.0 * u[0];
+  }
+  template <class T> __device__ static T wavespeed(const T* u, const T* n, const LawArgs& a) {
+    return dabs(a.p[0] * n[0] + a.p[1] * n[1]) + 0.0 * u[0];
+  }
+  __device__ static void ghost(int id, const LawArgs& a, double* out) { out[0] = 1.0; }
+};
+
+// space-time Burgers, conslaw.py:94-163
+struct BurgersST {
+  static constexpr int M = 1;
+  static constexpr int SRC = SRC_POS;
+  template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
+    f[0][0] = 0.5 * u[0] * u[0];
+    f[0][1] = u[0];
+  }
+  template <class T> __device__ static void source(const T* pos, const T* u, T* s, const LawArgs& a) {
+    s[0] = 0.02 * dexp(a.mu[1] * pos[0]);
+  }
+  template <class T> __device__ static T wavespeed(const T* u, const T* n, const LawArgs& a) {
+    T v = u[0] * n[0] + n[1];
+    return dsqrt(v * v + 1e-6);
+  }
+  __device__ static void ghost(int id, const LawArgs& a, double* out) { out[0] = id == 0 ? a.mu[0] : 1.0; }
+};
+
+// steady Burgers strip (config 1): (u^2/2)_x = mu u
+struct BurgersStrip {
+  static constexpr int M = 1;
+  static constexpr int SRC = SRC_U;
+  template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
+    f[0][0] = 0.5 * u[0] * u[0];
+    f[0][1] = 0.0 * u[0];
+  }
+  template <class T> __device__ static void source(const T* pos, const T* u, T* s, const LawArgs& a) {
+    s[0] = a.mu[0] * u[0];
+  }
+  template <class T> __device__ static T wavespeed(const T* u, const T* n, const LawArgs& a) {
+    T v = u[0] * n[0];
+    return dsqrt(v * v + 1e-6);
+  }
+  __device__ static void ghost(int id, const LawArgs& a, double* out) { out[0] = id == 0 ? a.p[0] : a.p[1]; }
+};
+
+// compressible Euler, conservative (rho, rho u, rho v, E); LLF speed |v.n| + c
+struct Euler {
+  static constexpr int M = 4;
+  static constexpr int SRC = SRC_NONE;
+  template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
+    const double g = a.p[0];
+    T vx = u[1] / u[0], vy = u[2] / u[0];
+    T p = (g - 1.0) * (u[3] - 0.5 * (u[1] * vx + u[2] * vy));
+    f[0][0] = u[1];              f[0][1] = u[2];
+    f[1][0] = u[1] * vx + p;     f[1][1] = u[1] * vy;
+    f[2][0] = u[2] * vx;         f[2][1] = u[2] * vy + p;
+    T Ep = u[3] + p;
+    f[3][0] = Ep * vx;           f[3][1] = Ep * vy;
+  }
+  template <class T> __device__ static void source(const T* pos, const T* u, T* s, const LawArgs& a) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) s[c] = 0.0 * u[c];
+  }
+  template <class T> __device__ static T wavespeed(const T* u, const T* n, const LawArgs& a) {
+    const double g = a.p[0];
+    T vx = u[1] / u[0], vy = u[2] / u[0];
+    T p = (g - 1.0) * (u[3] - 0.5 * (u[1] * vx + u[2] * vy));
+    T vn = vx * n[0] + vy * n[1];
+    return dabs(vn) + dsqrt(g * p / u[0]);
+  }
+  __device__ static void ghost(int id, const LawArgs& a, double* out) {
+    const double g = a.p[0], mach = a.mu[0], p = 1.0 / g;
+    out[0] = 1.0; out[1] = mach; out[2] = 0.0; out[3] = p / (g - 1.0) + 0.5 * mach * mach;
+  }
+};
+
+}  // namespace strom
