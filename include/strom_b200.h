@@ -118,6 +118,13 @@ int strom_lm_solve(strom_handle* h, double* w, double* tau, const double* mu, in
                    const int32_t* active, const double* rho, int32_t A, const double* cfg,
                    double* status, double* history, void* stream);
 
+/* Benchmark probe: while enabled, the dominant kernel of every strom_eval is
+ * bracketed by CUDA events recorded on the call's stream (capacity 4096
+ * launches).  strom_profile_ms synchronizes on the recorded events and
+ * returns the summed kernel time in ms and the launch count. */
+int strom_profile(strom_handle* h, int32_t enable);
+double strom_profile_ms(strom_handle* h, int32_t* launches);
+
 const char* strom_last_error(void);
 void strom_destroy(strom_handle* h);
 

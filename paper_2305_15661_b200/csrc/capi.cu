@@ -8,6 +8,7 @@
 #include <vector>
 #include "../../include/strom_b200.h"
 #include "element_kernels.cuh"
+#include "derivs_warp.cuh"
 #include "lm_kernels.cuh"
 
 using namespace strom;
@@ -50,7 +51,44 @@ struct strom_handle {
   std::vector<std::vector<int>> last_degen;
   int num_sms = 148;
   LmWork lm;
+  // benchmark probe
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  int nprof = 0;
 };
+
+static void prof_mark(strom_handle* h, cudaStream_t st, int which) {
+  if (!h->prof) return;
+  const int i = 2 * h->nprof + which;
+  if (i >= (int)h->ev.size()) return;
+  cudaEventRecord(h->ev[i], st);
+  if (which == 1) ++h->nprof;
+}
+
+extern "C" int strom_profile(strom_handle* h, int32_t enable) {
+  if (!h) return fail(-1, "null handle");
+  if (enable && h->ev.empty()) {
+    h->ev.resize(2 * 4096);
+    for (auto& e : h->ev) CK(cudaEventCreate(&e));
+  }
+  h->prof = enable != 0;
+  h->nprof = 0;
+  return 0;
+}
+
+extern "C" double strom_profile_ms(strom_handle* h, int32_t* launches) {
+  if (!h) return -1.0;
+  double ms = 0.0;
+  int n = std::min(h->nprof, (int)h->ev.size() / 2);
+  for (int i = 0; i < n; ++i) {
+    float t = 0.f;
+    cudaEventSynchronize(h->ev[2 * i + 1]);
+    cudaEventElapsedTime(&t, h->ev[2 * i], h->ev[2 * i + 1]);
+    ms += t;
+  }
+  if (launches) *launches = n;
+  return ms;
+}
 
 extern "C" const char* strom_last_error(void) { return g_err.c_str(); }
 
@@ -159,6 +197,48 @@ struct EvalArgs {
   cudaStream_t stream;
 };
 
+template <class LAW, int NB, int NQ, int NS, int TPU>
+static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WShape<LAW, NB, NQ, NS>::NF>& prm,
+                       int nunits) {
+  using SH = WShape<LAW, NB, NQ, NS>;
+  Run& r = prm.r;
+  constexpr int UPW = 32 / TPU;
+  r.U = UPW;
+  r.unit_stride = SH::unit_stride(r.LDJ);
+  r.gx_warp_stride = SH::warp_stride(r.LDJ, r.KP, UPW);
+  const int smem_cap = 227 * 1024;
+  const size_t warp_bytes = (size_t)r.gx_warp_stride * sizeof(double);
+  int nwarps = std::min<int>(WTHREADS / 32, (int)(smem_cap / warp_bytes));
+  if (nwarps < 1) return fail(-1, "element group does not fit in shared memory");
+  const size_t smem = nwarps * warp_bytes;
+  auto kern = derivs_warp_kernel<LAW, NB, NQ, NS, TPU>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nwarps * 32, smem));
+  per_sm = std::max(per_sm, 1);
+  const int ngroups = (nunits + UPW - 1) / UPW;
+  const int target = h->num_sms * per_sm;
+  const int maxb = std::max(1, (ngroups + nwarps - 1) / nwarps);
+  int gx = std::max(1, std::min(maxb, (target + a.P - 1) / a.P));
+  r.gx = gx;
+  r.ntiles = ngroups;
+  const int PSZ = 1 + r.K + r.KP * r.KP;
+  if (a.mode == MODE_DERIVS) {
+    if (ensure_part(h, (size_t)a.P * gx * PSZ)) return -2;
+    r.part = h->part;
+  }
+  prof_mark(h, a.stream, 0);
+  kern<<<dim3(gx, a.P), nwarps * 32, smem, a.stream>>>(prm);
+  prof_mark(h, a.stream, 1);
+  CK(cudaGetLastError());
+  if (a.mode == MODE_DERIVS) {
+    const int OSZ = 1 + r.K + r.K * r.K;
+    finalize_derivs_kernel<<<dim3((OSZ + 127) / 128, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out);
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
 template <class LAW, int NB, int NQ, int NS>
 static int eval_impl(strom_handle* h, const EvalArgs& a) {
   using SH = Shape<LAW, NB, NQ, NS>;
@@ -189,7 +269,9 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
       if (ensure_part(h, (size_t)a.P * gx)) return -2;
       r.part = h->part;
     }
+    prof_mark(h, a.stream, 0);
     value_kernel<LAW, NB, NQ, NS><<<dim3(gx, a.P), 128, 0, a.stream>>>(prm);
+    prof_mark(h, a.stream, 1);
     CK(cudaGetLastError());
     if (a.mode != MODE_RESIDUAL) {
       sum_partials_kernel<<<(a.P + 127) / 128, 128, 0, a.stream>>>(h->part, gx, a.P, a.out);
@@ -198,36 +280,9 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
     return 0;
   }
   if (h->ku < 1) return fail(-1, "derivative modes need k_u >= 1");
-  int U = std::max(1, DERIV_THREADS / h->ku);
-  int stride = SH::stride(r.LDJ);
-  const int PSZ = 1 + r.K + r.KP * r.KP;
-  const int smem_cap = 227 * 1024;
-  while (U > 1 && (size_t)U * stride * 8 > (size_t)smem_cap) --U;
-  size_t smem = std::max((size_t)U * stride, (size_t)PSZ) * sizeof(double);
-  if (smem > (size_t)smem_cap) return fail(-1, "element tile does not fit in shared memory");
-  r.U = U;
-  r.unit_stride = stride;
-  r.ntiles = (nunits + U - 1) / U;
-  auto kern = derivs_kernel<LAW, NB, NQ, NS>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DERIV_THREADS, smem));
-  per_sm = std::max(per_sm, 1);
-  const int target = h->num_sms * per_sm;
-  int gx = (a.mode == MODE_DERIVS) ? std::max(1, std::min(r.ntiles, (target + a.P - 1) / a.P)) : std::max(1, std::min(r.ntiles, std::max(1, target * 4 / a.P)));
-  r.gx = gx;
-  if (a.mode == MODE_DERIVS) {
-    if (ensure_part(h, (size_t)a.P * gx * PSZ)) return -2;
-    r.part = h->part;
-  }
-  kern<<<dim3(gx, a.P), DERIV_THREADS, smem, a.stream>>>(prm);
-  CK(cudaGetLastError());
-  if (a.mode == MODE_DERIVS) {
-    const int OSZ = 1 + r.K + r.K * r.K;
-    finalize_derivs_kernel<<<dim3((OSZ + 127) / 128, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out);
-    CK(cudaGetLastError());
-  }
-  return 0;
+  if (h->ku > 32) return fail(-1, "derivative modes need k_u <= 32");
+  if (h->ku <= 16) return launch_warp<LAW, NB, NQ, NS, 16>(h, a, prm, nunits);
+  return launch_warp<LAW, NB, NQ, NS, 32>(h, a, prm, nunits);
 }
 
 template <class LAW>
@@ -323,6 +378,7 @@ extern "C" void strom_destroy(strom_handle* h) {
   if (h->degen_fill) cudaFree(h->degen_fill);
   if (h->degen_scratch) cudaFree(h->degen_scratch);
   lm_free(h->lm);
+  for (auto& e : h->ev) cudaEventDestroy(e);
   delete h;
 }
 

@@ -62,6 +62,7 @@ struct Run {
   int ntiles;     // tiles per parameter
   int gx;         // blocks per parameter
   int unit_stride;  // doubles per unit in shared memory
+  int gx_warp_stride;  // doubles per warp in shared memory (warp kernel)
   double kappa, eps;
   double lawp[8];
 };

@@ -113,6 +113,7 @@ struct LawArgs {
 // ---------------------------------------------------------------------------
 // linear advection, conslaw.py:174-253 (no manufactured solution)
 struct LinAdv {
+  static constexpr bool ANALYTIC = false;
   static constexpr int M = 1;
   static constexpr int SRC = SRC_NONE;
   template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
@@ -130,6 +131,7 @@ struct LinAdv {
 
 // space-time Burgers, conslaw.py:94-163
 struct BurgersST {
+  static constexpr bool ANALYTIC = false;
   static constexpr int M = 1;
   static constexpr int SRC = SRC_POS;
   template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
@@ -148,6 +150,7 @@ struct BurgersST {
 
 // steady Burgers strip (config 1): (u^2/2)_x = mu u
 struct BurgersStrip {
+  static constexpr bool ANALYTIC = false;
   static constexpr int M = 1;
   static constexpr int SRC = SRC_U;
   template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
@@ -166,8 +169,45 @@ struct BurgersStrip {
 
 // compressible Euler, conservative (rho, rho u, rho v, E); LLF speed |v.n| + c
 struct Euler {
+  static constexpr bool ANALYTIC = true;
   static constexpr int M = 4;
   static constexpr int SRC = SRC_NONE;
+  // fn = f(u).n and A = d(f.n)/du for a (not necessarily unit) direction n
+  __device__ static void flux_dir(const double* u, const double* n, double* fn, double (*A)[4], const LawArgs& a) {
+    const double g = a.p[0], gm = g - 1.0;
+    const double r = u[0], ir = 1.0 / r, vx = u[1] * ir, vy = u[2] * ir;
+    const double p = gm * (u[3] - 0.5 * (u[1] * vx + u[2] * vy));
+    const double ke = 0.5 * (vx * vx + vy * vy);
+    const double qn = vx * n[0] + vy * n[1];
+    const double H = (u[3] + p) * ir;
+    fn[0] = r * qn;
+    fn[1] = u[1] * qn + p * n[0];
+    fn[2] = u[2] * qn + p * n[1];
+    fn[3] = (u[3] + p) * qn;
+    const double gk = gm * ke;
+    A[0][0] = 0.0;                     A[0][1] = n[0];                             A[0][2] = n[1];                             A[0][3] = 0.0;
+    A[1][0] = gk * n[0] - vx * qn;     A[1][1] = qn + vx * n[0] - gm * vx * n[0];  A[1][2] = vx * n[1] - gm * vy * n[0];       A[1][3] = gm * n[0];
+    A[2][0] = gk * n[1] - vy * qn;     A[2][1] = vy * n[0] - gm * vx * n[1];       A[2][2] = qn + vy * n[1] - gm * vy * n[1];  A[2][3] = gm * n[1];
+    A[3][0] = qn * (gk - H);           A[3][1] = H * n[0] - gm * vx * qn;          A[3][2] = H * n[1] - gm * vy * qn;          A[3][3] = g * qn;
+  }
+  // ws = |v.nh| + c and its gradients wrt u and nh (sign(0) = 0)
+  __device__ static double wavespeed_grad(const double* u, const double* nh, double* dwdu, double* dwdn, const LawArgs& a) {
+    const double g = a.p[0], gm = g - 1.0;
+    const double r = u[0], ir = 1.0 / r, vx = u[1] * ir, vy = u[2] * ir;
+    const double p = gm * (u[3] - 0.5 * (u[1] * vx + u[2] * vy));
+    const double ke = 0.5 * (vx * vx + vy * vy);
+    const double qn = vx * nh[0] + vy * nh[1];
+    const double c = sqrt(g * p / r);
+    const double sg = qn > 0.0 ? 1.0 : (qn < 0.0 ? -1.0 : 0.0);
+    const double cf = g / (2.0 * c * r);
+    dwdu[0] = sg * (-qn * ir) + cf * (gm * ke - p * ir);
+    dwdu[1] = sg * nh[0] * ir - cf * gm * vx;
+    dwdu[2] = sg * nh[1] * ir - cf * gm * vy;
+    dwdu[3] = cf * gm;
+    dwdn[0] = sg * vx;
+    dwdn[1] = sg * vy;
+    return fabs(qn) + c;
+  }
   template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
     const double g = a.p[0];
     T vx = u[1] / u[0], vy = u[2] / u[0];
@@ -192,6 +232,51 @@ struct Euler {
   __device__ static void ghost(int id, const LawArgs& a, double* out) {
     const double g = a.p[0], mach = a.mu[0], p = 1.0 / g;
     out[0] = 1.0; out[1] = mach; out[2] = 0.0; out[3] = p / (g - 1.0) + 0.5 * mach * mach;
+  }
+};
+
+// ---- point Jacobians: analytic when the law provides them, else forward mode ----
+template <class LAW, bool A = LAW::ANALYTIC>
+struct PointOps;
+
+template <class LAW>
+struct PointOps<LAW, true> {
+  __device__ static void flux_dir(const double* u, const double* n, double* fn, double (*Am)[LAW::M], const LawArgs& a) {
+    LAW::flux_dir(u, n, fn, Am, a);
+  }
+  __device__ static double wavespeed_grad(const double* u, const double* nh, double* dwdu, double* dwdn, const LawArgs& a) {
+    return LAW::wavespeed_grad(u, nh, dwdu, dwdn, a);
+  }
+};
+
+template <class LAW>
+struct PointOps<LAW, false> {
+  static constexpr int M = LAW::M;
+  __device__ static void flux_dir(const double* u, const double* n, double* fn, double (*Am)[M], const LawArgs& a) {
+    Dn<M> ud[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) ud[c] = seed<M>(u[c], c);
+    Dn<M> f[M][2];
+    LAW::flux(ud, f, a);
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      fn[c] = f[c][0].v * n[0] + f[c][1].v * n[1];
+#pragma unroll
+      for (int cp = 0; cp < M; ++cp) Am[c][cp] = f[c][0].d[cp] * n[0] + f[c][1].d[cp] * n[1];
+    }
+  }
+  __device__ static double wavespeed_grad(const double* u, const double* nh, double* dwdu, double* dwdn, const LawArgs& a) {
+    Dn<M + 2> ud[M], nd[2];
+#pragma unroll
+    for (int c = 0; c < M; ++c) ud[c] = seed<M + 2>(u[c], c);
+    nd[0] = seed<M + 2>(nh[0], M);
+    nd[1] = seed<M + 2>(nh[1], M + 1);
+    Dn<M + 2> w = LAW::wavespeed(ud, nd, a);
+#pragma unroll
+    for (int c = 0; c < M; ++c) dwdu[c] = w.d[c];
+    dwdn[0] = w.d[M];
+    dwdn[1] = w.d[M + 1];
+    return w.v;
   }
 };
 

@@ -1,0 +1,92 @@
+"""CUDA path vs the oracle/reference golden vectors (parity tests proper)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from cases import EVAL_CASES, build, rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def gpu_op(case):
+    from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases
+
+    bases = ReducedBases(case.phi, case.psi, case.ref_coords)
+    return GpuReducedOperator(case.law, case.geom, bases, case.dist, state_offset=case.state_offset)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("name", EVAL_CASES)
+def test_gpu_matches_reference(name):
+    from paper_2305_15661_b200.reduced import ReducedCoords
+    from paper_2305_15661_b200.eqp import WeightVector
+
+    case, g = build(name)
+    op = gpu_op(case)
+    c = ReducedCoords(g["w"], g["tau"])
+    mu = case.mus[0]
+    assert rel_err(op.objective(c, mu), g["obj_all"]) < TOL
+    J, S, T, Hww, Hwt, Htt = op.derivatives(c, mu)
+    for k, v in dict(J=J, S=S, T=T, Hww=Hww, Hwt=Hwt, Htt=Htt).items():
+        assert rel_err(v, g[f"der_all_{k}"]) < TOL, k
+    if case.rho is not None:
+        rho = WeightVector(case.rho)
+        assert rel_err(op.objective(c, mu, rho), g["obj_rho"]) < TOL
+        J, S, T, Hww, Hwt, Htt = op.derivatives(c, mu, rho)
+        for k, v in dict(J=J, S=S, T=T, Hww=Hww, Hwt=Hwt, Htt=Htt).items():
+            assert rel_err(v, g[f"der_rho_{k}"]) < TOL, k
+        S2, T2 = op.residuals(c, mu, rho)
+        assert rel_err(S2, g["der_rho_S"]) < TOL and rel_err(T2, g["der_rho_T"]) < TOL
+    for k, v in zip(("Se", "Te"), op.elemental_contributions(c, mu)):
+        assert rel_err(v, g[f"contrib_{k}"]) < TOL, k
+    for k, v in zip(("Sv", "Sf", "Tv", "Tf"), op.elemental_contributions(c, mu, split=True)):
+        assert rel_err(v, g[f"split_{k}"]) < TOL, k
+    assert rel_err(op.global_residual(c, mu), g["resid"]) < TOL
+    assert abs(op.residual_norm(c, mu) - np.linalg.norm(g["resid"])) <= TOL * np.linalg.norm(g["resid"])
+    assert op.stats["kernel_calls"] > 0
+
+
+def test_gpu_degenerate_elements():
+    from paper_2305_15661_b200.reduced import DegenerateMappingError, ReducedCoords
+
+    case, g = build("degenerate")
+    op = gpu_op(case)
+    with pytest.raises(DegenerateMappingError) as ei:
+        op.objective(ReducedCoords(np.zeros(4), np.zeros(2)), case.mus[0])
+    assert np.array_equal(np.asarray(ei.value.elements), g["degenerate_elements"])
+    with pytest.raises(DegenerateMappingError):
+        op.derivatives(ReducedCoords(np.zeros(4), np.zeros(2)), case.mus[0])
+
+
+def test_gpu_deterministic():
+    from paper_2305_15661_b200.reduced import ReducedCoords
+
+    case, g = build("euler_square_q6")
+    op = gpu_op(case)
+    c = ReducedCoords(g["w"], g["tau"])
+    a = op.derivatives(c, case.mus[0])
+    b = op.derivatives(c, case.mus[0])
+    for x, y in zip(a, b):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+def test_gpu_empty_active_set():
+    from paper_2305_15661_b200.reduced import ReducedCoords
+    from paper_2305_15661_b200.eqp import WeightVector
+
+    case, g = build("strip")
+    op = gpu_op(case)
+    c = ReducedCoords(g["w"], g["tau"])
+    rho = WeightVector(np.zeros(case.mesh.num_elements))
+    assert op.objective(c, case.mus[0], rho) == 0.0
+    J, S, T, Hww, Hwt, Htt = op.derivatives(c, case.mus[0], rho)
+    assert J == 0.0 and not np.any(S) and not np.any(Htt)
