@@ -11,7 +11,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "_strom_b200.so")
-SRC = os.path.join(HERE, "csrc", "capi.cu")
+CSRC = os.path.join(HERE, "csrc")
+UNITS = ["capi.cu", "law_euler.cu", "law_strip.cu", "law_burgers_st.cu", "law_linadv.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -30,17 +31,35 @@ def up_to_date():
 
 
 def build(force=False, verbose=False):
+    """Compile the translation units in parallel (one per law + the C ABI) and link."""
     if not force and up_to_date():
         return SO
+    import concurrent.futures as cf
+    import tempfile
+
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3", "-o", SO + ".tmp", SRC]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building _strom_b200.so")
+    tmp = tempfile.mkdtemp(prefix="strom_build_")
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
     if verbose:
-        sys.stderr.write(r.stderr)
+        flags += ["-Xptxas", "-v"]
+
+    def compile_unit(u):
+        obj = os.path.join(tmp, u + ".o")
+        r = subprocess.run([nvcc, *flags, "-c", os.path.join(CSRC, u), "-o", obj], capture_output=True, text=True)
+        return u, obj, r
+
+    with cf.ThreadPoolExecutor(max_workers=len(UNITS)) as ex:
+        results = list(ex.map(compile_unit, UNITS))
+    for u, obj, r in results:
+        if verbose or r.returncode:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode:
+            raise RuntimeError(f"nvcc failed on {u}")
+    r = subprocess.run([nvcc, *ARCH, "--shared", "-o", SO + ".tmp", *[o for _, o, _ in results]],
+                       capture_output=True, text=True)
+    if r.returncode:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc link failed")
     os.replace(SO + ".tmp", SO)
     return SO
 

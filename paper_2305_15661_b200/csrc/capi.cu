@@ -1,68 +1,46 @@
-// C ABI of strom_b200 (include/strom_b200.h): handle management, template
-// dispatch over (law, p, volume rule, face rule), launch configuration.
-#include <cuda_runtime.h>
-#include <algorithm>
+// C ABI of strom_b200 (include/strom_b200.h): handle management, dispatch,
+// benchmark probe and the batched LM host loop.
 #include <cstdio>
-#include <cstring>
-#include <string>
-#include <vector>
-#include "../../include/strom_b200.h"
-#include "element_kernels.cuh"
-#include "derivs_warp.cuh"
+#include "handle.h"
 #include "lm_kernels.cuh"
 
 using namespace strom;
+using namespace strom_host;
 
 static thread_local std::string g_err;
 
-static int fail(int code, const std::string& msg) {
+namespace strom_host {
+int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+int ensure_part(strom_handle* h, size_t n) {
+  if (n <= h->part_cap) return 0;
+  if (h->part) cudaFree(h->part);
+  h->part = nullptr;
+  CK(cudaMalloc(&h->part, n * sizeof(double)));
+  h->part_cap = n;
+  return 0;
+}
 
-#define CK(x)                                                                      \
-  do {                                                                             \
-    cudaError_t _e = (x);                                                          \
-    if (_e != cudaSuccess) return fail(-2, std::string(#x ": ") + cudaGetErrorString(_e)); \
-  } while (0)
-
-struct strom_handle {
-  int device = 0;
-  int ne = 0, nv = 0;
-  const int* elem_nodes = nullptr;
-  const double* nodes = nullptr;
-  const int* nbr = nullptr;
-  const uint8_t* finfo = nullptr;
-  strom_law_desc law{};
-  int p = 0, nb = 0, nq = 0, ns = 0, nf = 0;
-  std::vector<double> phi, dphi, wq, bary, trace, ws;
-  double wsum = 0.0;
-  double kappa = 1.0, eps = 1e-8;
-  double* eta_ref = nullptr;
-  const double *Phi = nullptr, *Psi = nullptr, *xref = nullptr, *u0 = nullptr;
-  int ku = 0, kx = 0;
-  double* part = nullptr;
-  size_t part_cap = 0;
-  int* degen_fill = nullptr;
-  int* degen_list = nullptr;
-  int degen_cap = 0;
-  int* degen_scratch = nullptr;
-  int degen_scratch_cap = 0;
-  std::vector<std::vector<int>> last_degen;
-  int num_sms = 148;
-  LmWork lm;
-  // benchmark probe
-  bool prof = false;
-  std::vector<cudaEvent_t> ev;
-  int nprof = 0;
-};
-
-static void prof_mark(strom_handle* h, cudaStream_t st, int which) {
+void prof_mark(strom_handle* h, cudaStream_t st, int which) {
   if (!h->prof) return;
   const int i = 2 * h->nprof + which;
   if (i >= (int)h->ev.size()) return;
   cudaEventRecord(h->ev[i], st);
   if (which == 1) ++h->nprof;
+}
+
+}  // namespace strom_host
+
+static int dispatch(strom_handle* h, const EvalArgs& a) {
+  switch (h->law.law_id) {
+    case 0: return eval_linadv(h, a);
+    case 1: return eval_burgers_st(h, a);
+    case 2: return eval_strip(h, a);
+    case 3: return eval_euler(h, a);
+    default: return fail(-1, "unknown law id");
+  }
 }
 
 extern "C" int strom_profile(strom_handle* h, int32_t enable) {
@@ -92,14 +70,6 @@ extern "C" double strom_profile_ms(strom_handle* h, int32_t* launches) {
 
 extern "C" const char* strom_last_error(void) { return g_err.c_str(); }
 
-static int ensure_part(strom_handle* h, size_t n) {
-  if (n <= h->part_cap) return 0;
-  if (h->part) cudaFree(h->part);
-  h->part = nullptr;
-  CK(cudaMalloc(&h->part, n * sizeof(double)));
-  h->part_cap = n;
-  return 0;
-}
 
 static int ensure_degen(strom_handle* h, int P) {
   if (P > h->degen_scratch_cap) {
@@ -165,145 +135,6 @@ extern "C" int strom_set_bases(strom_handle* h, const double* phi, int32_t ku, c
   return 0;
 }
 
-template <int NB, int NQ, int NS, int NF>
-static void fill_tabs(const strom_handle* h, Tabs<NB, NQ, NS, NF>& t) {
-  for (int q = 0; q < NQ; ++q) {
-    for (int n = 0; n < NB; ++n) {
-      t.phi[q][n] = h->phi[q * NB + n];
-      t.dphi[q][n][0] = h->dphi[(q * NB + n) * 2 + 0];
-      t.dphi[q][n][1] = h->dphi[(q * NB + n) * 2 + 1];
-    }
-    t.wq[q] = h->wq[q];
-    for (int g = 0; g < 3; ++g) t.bary[q][g] = h->bary[q * 3 + g];
-  }
-  for (int f = 0; f < 3; ++f)
-    for (int s = 0; s < NS; ++s)
-      for (int j = 0; j < NF; ++j) t.trace[f][s][j] = h->trace[(f * NS + s) * NF + j];
-  for (int s = 0; s < NS; ++s) t.ws[s] = h->ws[s];
-  t.wsum = h->wsum;
-  for (int f = 0; f < 3; ++f)
-    for (int j = 0; j < NF; ++j) t.fnode[f][j] = fnode_of(NB == 3 ? 1 : 2, f, j);
-}
-
-struct EvalArgs {
-  int mode;
-  const double *w, *tau, *mu;
-  int P;
-  const int* active;
-  const double* rho;
-  int A;
-  double* out;
-  int* degen;
-  cudaStream_t stream;
-};
-
-template <class LAW, int NB, int NQ, int NS, int TPU>
-static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WShape<LAW, NB, NQ, NS>::NF>& prm,
-                       int nunits) {
-  using SH = WShape<LAW, NB, NQ, NS>;
-  Run& r = prm.r;
-  constexpr int UPW = 32 / TPU;
-  r.U = UPW;
-  r.unit_stride = SH::unit_stride(r.LDJ);
-  r.gx_warp_stride = SH::warp_stride(r.LDJ, r.KP, UPW);
-  const int smem_cap = 227 * 1024;
-  const size_t warp_bytes = (size_t)r.gx_warp_stride * sizeof(double);
-  int nwarps = std::min<int>(WTHREADS / 32, (int)(smem_cap / warp_bytes));
-  if (nwarps < 1) return fail(-1, "element group does not fit in shared memory");
-  const size_t smem = nwarps * warp_bytes;
-  auto kern = derivs_warp_kernel<LAW, NB, NQ, NS, TPU>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nwarps * 32, smem));
-  per_sm = std::max(per_sm, 1);
-  const int ngroups = (nunits + UPW - 1) / UPW;
-  const int target = h->num_sms * per_sm;
-  const int maxb = std::max(1, (ngroups + nwarps - 1) / nwarps);
-  int gx = std::max(1, std::min(maxb, (target + a.P - 1) / a.P));
-  r.gx = gx;
-  r.ntiles = ngroups;
-  const int PSZ = 1 + r.K + r.KP * r.KP;
-  if (a.mode == MODE_DERIVS) {
-    if (ensure_part(h, (size_t)a.P * gx * PSZ)) return -2;
-    r.part = h->part;
-  }
-  prof_mark(h, a.stream, 0);
-  kern<<<dim3(gx, a.P), nwarps * 32, smem, a.stream>>>(prm);
-  prof_mark(h, a.stream, 1);
-  CK(cudaGetLastError());
-  if (a.mode == MODE_DERIVS) {
-    const int OSZ = 1 + r.K + r.K * r.K;
-    finalize_derivs_kernel<<<dim3((OSZ + 127) / 128, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out);
-    CK(cudaGetLastError());
-  }
-  return 0;
-}
-
-template <class LAW, int NB, int NQ, int NS>
-static int eval_impl(strom_handle* h, const EvalArgs& a) {
-  using SH = Shape<LAW, NB, NQ, NS>;
-  constexpr int NF = SH::NF;
-  Params<NB, NQ, NS, NF> prm;
-  fill_tabs<NB, NQ, NS, NF>(h, prm.t);
-  Run& r = prm.r;
-  memset(&r, 0, sizeof(r));
-  r.ne = h->ne; r.elem_nodes = h->elem_nodes; r.nodes = h->nodes; r.nbr = h->nbr; r.finfo = h->finfo;
-  r.eta_ref = h->eta_ref;
-  r.phi = h->Phi; r.psi = h->Psi; r.xref = h->xref; r.u0 = h->u0; r.ku = h->ku; r.kx = h->kx;
-  r.K = h->ku + h->kx;
-  r.KP = (r.K + 7) / 8 * 8;
-  if (r.KP < 8) r.KP = 8;
-  r.LDJ = (r.KP % 16 == 0) ? r.KP + 8 : r.KP;
-  r.w = a.w; r.tau = a.tau; r.mu = a.mu; r.nmu = h->law.n_mu; r.P = a.P;
-  r.active = a.active; r.rho = a.rho; r.A = a.A;
-  r.out = a.out;
-  r.degen = a.degen; r.degen_list = h->degen_list; r.degen_cap = h->degen_cap; r.degen_fill = h->degen_fill;
-  r.mode = a.mode;
-  r.kappa = h->kappa; r.eps = h->eps;
-  for (int i = 0; i < 8; ++i) r.lawp[i] = h->law.params[i];
-  const int nunits = a.active ? a.A : h->ne;
-  if (nunits == 0) return 0;
-  if (a.mode == MODE_OBJECTIVE || a.mode == MODE_RESNORM2 || a.mode == MODE_RESIDUAL) {
-    const int gx = (nunits + 127) / 128;
-    if (a.mode != MODE_RESIDUAL) {
-      if (ensure_part(h, (size_t)a.P * gx)) return -2;
-      r.part = h->part;
-    }
-    prof_mark(h, a.stream, 0);
-    value_kernel<LAW, NB, NQ, NS><<<dim3(gx, a.P), 128, 0, a.stream>>>(prm);
-    prof_mark(h, a.stream, 1);
-    CK(cudaGetLastError());
-    if (a.mode != MODE_RESIDUAL) {
-      sum_partials_kernel<<<(a.P + 127) / 128, 128, 0, a.stream>>>(h->part, gx, a.P, a.out);
-      CK(cudaGetLastError());
-    }
-    return 0;
-  }
-  if (h->ku < 1) return fail(-1, "derivative modes need k_u >= 1");
-  if (h->ku > 32) return fail(-1, "derivative modes need k_u <= 32");
-  if (h->ku <= 16) return launch_warp<LAW, NB, NQ, NS, 16>(h, a, prm, nunits);
-  return launch_warp<LAW, NB, NQ, NS, 32>(h, a, prm, nunits);
-}
-
-template <class LAW>
-static int dispatch_shape(strom_handle* h, const EvalArgs& a) {
-  if (h->nb == 6 && h->nq == 12 && h->ns == 4) return eval_impl<LAW, 6, 12, 4>(h, a);
-  if (h->nb == 6 && h->nq == 25 && h->ns == 4) return eval_impl<LAW, 6, 25, 4>(h, a);
-  if (h->nb == 3 && h->nq == 7 && h->ns == 3) return eval_impl<LAW, 3, 7, 3>(h, a);
-  return fail(-1, "no compiled kernel for (p, n_q, n_s) = (" + std::to_string(h->p) + ", " + std::to_string(h->nq) +
-                      ", " + std::to_string(h->ns) + ")");
-}
-
-static int dispatch(strom_handle* h, const EvalArgs& a) {
-  switch (h->law.law_id) {
-    case 0: return dispatch_shape<LinAdv>(h, a);
-    case 1: return dispatch_shape<BurgersST>(h, a);
-    case 2: return dispatch_shape<BurgersStrip>(h, a);
-    case 3: return dispatch_shape<Euler>(h, a);
-    default: return fail(-1, "unknown law id");
-  }
-}
-
 extern "C" int strom_reserve(strom_handle* h, int32_t max_P, int32_t max_active) {
   if (!h) return fail(-1, "null handle");
   const int K = h->ku + h->kx, KP = std::max(8, (K + 7) / 8 * 8);
@@ -354,7 +185,7 @@ extern "C" int strom_eval(strom_handle* h, int32_t mode, const double* w, const 
   }
   CK(cudaMemsetAsync(degen, 0, sizeof(int) * P, st));
   CK(cudaMemsetAsync(h->degen_fill, 0, sizeof(int), st));
-  EvalArgs a{mode, w, tau, mu, P, active, rho, A, out, degen, st};
+  EvalArgs a{mode, nullptr, w, tau, mu, P, active, rho, A, out, degen, st};
   int rc = dispatch(h, a);
   if (rc) return rc;
   if (sync) return collect_degen(h, P, degen, st);

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(WTHREADS) derivs_warp_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int h = lane / TPU, k = lane % TPU;
   const int p = blockIdx.y;
+  if (r.mask && !r.mask[p]) return;
   const int ku = r.ku, kx = r.kx, K = r.K, KP = r.KP, LDJ = r.LDJ, STR = r.unit_stride;
   double* const Wb = smem + (size_t)warp * r.gx_warp_stride;
   double* const S = Wb + h * STR;

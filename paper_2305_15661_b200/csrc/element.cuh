@@ -58,6 +58,7 @@ struct Run {
   int degen_cap;
   int* __restrict__ degen_fill;
   int mode;
+  const int* __restrict__ mask;  // per-row enable (batched LM), or null
   int U;          // units per tile (derivs kernel)
   int ntiles;     // tiles per parameter
   int gx;         // blocks per parameter

@@ -1,0 +1,133 @@
+// Template launchers for one conservation law (included by the per-law units).
+#pragma once
+#include "handle.h"
+#include "derivs_warp.cuh"
+
+namespace strom_host {
+template <int NB, int NQ, int NS, int NF>
+static void fill_tabs(const strom_handle* h, Tabs<NB, NQ, NS, NF>& t) {
+  for (int q = 0; q < NQ; ++q) {
+    for (int n = 0; n < NB; ++n) {
+      t.phi[q][n] = h->phi[q * NB + n];
+      t.dphi[q][n][0] = h->dphi[(q * NB + n) * 2 + 0];
+      t.dphi[q][n][1] = h->dphi[(q * NB + n) * 2 + 1];
+    }
+    t.wq[q] = h->wq[q];
+    for (int g = 0; g < 3; ++g) t.bary[q][g] = h->bary[q * 3 + g];
+  }
+  for (int f = 0; f < 3; ++f)
+    for (int s = 0; s < NS; ++s)
+      for (int j = 0; j < NF; ++j) t.trace[f][s][j] = h->trace[(f * NS + s) * NF + j];
+  for (int s = 0; s < NS; ++s) t.ws[s] = h->ws[s];
+  t.wsum = h->wsum;
+  for (int f = 0; f < 3; ++f)
+    for (int j = 0; j < NF; ++j) t.fnode[f][j] = fnode_of(NB == 3 ? 1 : 2, f, j);
+}
+
+
+template <class LAW, int NB, int NQ, int NS, int TPU>
+static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WShape<LAW, NB, NQ, NS>::NF>& prm,
+                       int nunits) {
+  using SH = WShape<LAW, NB, NQ, NS>;
+  Run& r = prm.r;
+  constexpr int UPW = 32 / TPU;
+  r.U = UPW;
+  r.unit_stride = SH::unit_stride(r.LDJ);
+  r.gx_warp_stride = SH::warp_stride(r.LDJ, r.KP, UPW);
+  const int smem_cap = 227 * 1024;
+  const size_t warp_bytes = (size_t)r.gx_warp_stride * sizeof(double);
+  int nwarps = std::min<int>(WTHREADS / 32, (int)(smem_cap / warp_bytes));
+  if (nwarps < 1) return fail(-1, "element group does not fit in shared memory");
+  const size_t smem = nwarps * warp_bytes;
+  auto kern = derivs_warp_kernel<LAW, NB, NQ, NS, TPU>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nwarps * 32, smem));
+  per_sm = std::max(per_sm, 1);
+  const int ngroups = (nunits + UPW - 1) / UPW;
+  const int target = h->num_sms * per_sm;
+  const int maxb = std::max(1, (ngroups + nwarps - 1) / nwarps);
+  int gx = std::max(1, std::min(maxb, (target + a.P - 1) / a.P));
+  r.gx = gx;
+  r.ntiles = ngroups;
+  const int PSZ = 1 + r.K + r.KP * r.KP;
+  if (a.mode == MODE_DERIVS) {
+    if (ensure_part(h, (size_t)a.P * gx * PSZ)) return -2;
+    r.part = h->part;
+  }
+  prof_mark(h, a.stream, 0);
+  kern<<<dim3(gx, a.P), nwarps * 32, smem, a.stream>>>(prm);
+  prof_mark(h, a.stream, 1);
+  CK(cudaGetLastError());
+  if (a.mode == MODE_DERIVS) {
+    const int OSZ = 1 + r.K + r.K * r.K;
+    finalize_derivs_kernel<<<dim3((OSZ + 127) / 128, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
+template <class LAW, int NB, int NQ, int NS>
+static int eval_impl(strom_handle* h, const EvalArgs& a) {
+  using SH = Shape<LAW, NB, NQ, NS>;
+  constexpr int NF = SH::NF;
+  Params<NB, NQ, NS, NF> prm;
+  fill_tabs<NB, NQ, NS, NF>(h, prm.t);
+  Run& r = prm.r;
+  memset(&r, 0, sizeof(r));
+  r.ne = h->ne; r.elem_nodes = h->elem_nodes; r.nodes = h->nodes; r.nbr = h->nbr; r.finfo = h->finfo;
+  r.eta_ref = h->eta_ref;
+  r.phi = h->Phi; r.psi = h->Psi; r.xref = h->xref; r.u0 = h->u0; r.ku = h->ku; r.kx = h->kx;
+  r.K = h->ku + h->kx;
+  r.KP = (r.K + 7) / 8 * 8;
+  if (r.KP < 8) r.KP = 8;
+  r.LDJ = (r.KP % 16 == 0) ? r.KP + 8 : r.KP;
+  r.w = a.w; r.tau = a.tau; r.mu = a.mu; r.nmu = h->law.n_mu; r.P = a.P;
+  r.active = a.active; r.rho = a.rho; r.A = a.A;
+  r.out = a.out;
+  r.degen = a.degen; r.degen_list = h->degen_list; r.degen_cap = h->degen_cap; r.degen_fill = h->degen_fill;
+  r.mode = a.mode;
+  r.mask = a.mask;
+  r.kappa = h->kappa; r.eps = h->eps;
+  for (int i = 0; i < 8; ++i) r.lawp[i] = h->law.params[i];
+  const int nunits = a.active ? a.A : h->ne;
+  if (nunits == 0) {
+    size_t n = 0;
+    if (a.mode == MODE_OBJECTIVE || a.mode == MODE_RESNORM2) n = a.P;
+    if (a.mode == MODE_DERIVS) n = (size_t)a.P * (1 + r.K + r.K * r.K);
+    if (n) CK(cudaMemsetAsync(a.out, 0, n * sizeof(double), a.stream));
+    return 0;
+  }
+  if (a.mode == MODE_OBJECTIVE || a.mode == MODE_RESNORM2 || a.mode == MODE_RESIDUAL) {
+    const int gx = (nunits + 127) / 128;
+    if (a.mode != MODE_RESIDUAL) {
+      if (ensure_part(h, (size_t)a.P * gx)) return -2;
+      r.part = h->part;
+    }
+    prof_mark(h, a.stream, 0);
+    value_kernel<LAW, NB, NQ, NS><<<dim3(gx, a.P), 128, 0, a.stream>>>(prm);
+    prof_mark(h, a.stream, 1);
+    CK(cudaGetLastError());
+    if (a.mode != MODE_RESIDUAL) {
+      sum_partials_kernel<<<(a.P + 127) / 128, 128, 0, a.stream>>>(h->part, gx, a.P, a.out, a.mask);
+      CK(cudaGetLastError());
+    }
+    return 0;
+  }
+  if (h->ku < 1) return fail(-1, "derivative modes need k_u >= 1");
+  if (h->ku > 32) return fail(-1, "derivative modes need k_u <= 32");
+  if (h->ku <= 16) return launch_warp<LAW, NB, NQ, NS, 16>(h, a, prm, nunits);
+  return launch_warp<LAW, NB, NQ, NS, 32>(h, a, prm, nunits);
+}
+
+template <class LAW>
+static int dispatch_shape(strom_handle* h, const EvalArgs& a) {
+  if (h->nb == 6 && h->nq == 12 && h->ns == 4) return eval_impl<LAW, 6, 12, 4>(h, a);
+  if (h->nb == 6 && h->nq == 25 && h->ns == 4) return eval_impl<LAW, 6, 25, 4>(h, a);
+  if (h->nb == 3 && h->nq == 7 && h->ns == 3) return eval_impl<LAW, 3, 7, 3>(h, a);
+  return fail(-1, "no compiled kernel for (p, n_q, n_s) = (" + std::to_string(h->p) + ", " + std::to_string(h->nq) +
+                      ", " + std::to_string(h->ns) + ")");
+}
+
+
+}  // namespace strom_host

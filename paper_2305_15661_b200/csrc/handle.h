@@ -1,0 +1,94 @@
+// Internal header shared by the C-ABI translation unit and the per-law kernel units.
+#pragma once
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+#include "../../include/strom_b200.h"
+#include "element_kernels.cuh"
+
+namespace strom {
+struct LmWork {
+  int P = 0, K = 0, ku = 0, kx = 0, nmu = 0;
+  void* buf = nullptr;
+  size_t bytes = 0;
+  int* counters_h = nullptr;  // pinned
+};
+
+inline void lm_free(LmWork& w) {
+  if (w.buf) cudaFree(w.buf);
+  if (w.counters_h) cudaFreeHost(w.counters_h);
+  w = LmWork();
+}
+
+}  // namespace strom
+
+namespace strom_host {
+using namespace strom;
+
+int fail(int code, const std::string& msg);
+
+#define CK(x)                                                                      \
+  do {                                                                             \
+    cudaError_t _e = (x);                                                          \
+    if (_e != cudaSuccess) return strom_host::fail(-2, std::string(#x ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+struct EvalArgs {
+  int mode;
+  const int* mask;
+  const double *w, *tau, *mu;
+  int P;
+  const int* active;
+  const double* rho;
+  int A;
+  double* out;
+  int* degen;
+  cudaStream_t stream;
+};
+
+}  // namespace strom_host
+
+using strom_host::EvalArgs;
+
+struct strom_handle {
+  int device = 0;
+  int ne = 0, nv = 0;
+  const int* elem_nodes = nullptr;
+  const double* nodes = nullptr;
+  const int* nbr = nullptr;
+  const uint8_t* finfo = nullptr;
+  strom_law_desc law{};
+  int p = 0, nb = 0, nq = 0, ns = 0, nf = 0;
+  std::vector<double> phi, dphi, wq, bary, trace, ws;
+  double wsum = 0.0;
+  double kappa = 1.0, eps = 1e-8;
+  double* eta_ref = nullptr;
+  const double *Phi = nullptr, *Psi = nullptr, *xref = nullptr, *u0 = nullptr;
+  int ku = 0, kx = 0;
+  double* part = nullptr;
+  size_t part_cap = 0;
+  int* degen_fill = nullptr;
+  int* degen_list = nullptr;
+  int degen_cap = 0;
+  int* degen_scratch = nullptr;
+  int degen_scratch_cap = 0;
+  std::vector<std::vector<int>> last_degen;
+  int num_sms = 148;
+  strom::LmWork lm;
+  // benchmark probe
+  int lm_rounds = 0;
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  int nprof = 0;
+};
+
+namespace strom_host {
+int ensure_part(strom_handle* h, size_t n);
+void prof_mark(strom_handle* h, cudaStream_t st, int which);
+int eval_linadv(strom_handle* h, const EvalArgs& a);
+int eval_burgers_st(strom_handle* h, const EvalArgs& a);
+int eval_strip(strom_handle* h, const EvalArgs& a);
+int eval_euler(strom_handle* h, const EvalArgs& a);
+}  // namespace strom_host

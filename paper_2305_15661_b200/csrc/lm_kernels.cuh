@@ -1,6 +1,442 @@
-// Batched Levenberg-Marquardt (placeholder until the LM milestone).
+// K5: batched Levenberg-Marquardt over many parameter points (one CTA per mu).
+//
+// Device restatement of strom/lm.py:129-271 as a resumable state machine.
+// Each round the control kernel advances every mu until it needs an
+// evaluation, then posts a request: a derivatives pass at (w, tau) or a
+// batch of objective trials at w + alpha_j dw (speculative backtracking:
+// alpha_j = 2^-j for the next LM_B values of j; the accepted step is the
+// first j that passes Armijo, exactly the sequential loop's choice).  The
+// host loop launches the masked batched evaluations and the next round.
+// The K x K normal equations [[H_ww, H_wt],[H_wt^T, H_tt + lam I]] dz = -[S;T]
+// are solved in-kernel by LDL^T (no pivoting; singular = zero / non-finite
+// pivot or non-finite solution, lm.py:111-126).
 #pragma once
+#include <cmath>
+#include <cstdint>
+
 namespace strom {
-struct LmWork { void* dummy = nullptr; };
-inline void lm_free(LmWork&) {}
+
+constexpr int LM_B = 4;        // speculative objective trials per round
+constexpr int LM_THREADS = 64;
+
+enum LmPhase {
+  PH_START = 0, PH_SI_DERIV, PH_SI_BASEJ, PH_SI_LS, PH_MAIN_DERIV, PH_MAIN_ITER_READY, PH_MAIN_LS,
+  PH_MAIN_ACCEPT_DERIV, PH_DONE
+};
+enum LmReason { R_FIRST_ORDER = 0, R_MAX_ITERS = 1, R_LS_FAIL = 2, R_DEGENERATE = 3 };
+
+struct LmCfg {
+  double eps1, eps2, lambda0, lambda_inc, lambda_dec, ratio_hi, ratio_lo;
+  int max_iters;
+  double c1, c2;
+  int max_backtracks;
+  double lambda_cap, w0_tol;
+  int w0_iters, w0_lsq;
+};
+
+struct LmState {
+  int phase, it, si_cnt, attempts, j0, done, reason, n_done, nhist, have_best, lam_set, si_have_J, evals;
+  double lam, lam_floor, J, J_si, gdot, J_new, alpha, si_target, nS_prev, nT_prev, J_prev;
+  double best_J, best_nS, best_nT;
+};
+
+struct LmRun {
+  int P, ku, kx, K, nmu;
+  LmCfg cfg;
+  LmState* st;
+  double* w;        // (P, ku) current
+  double* tau;      // (P, kx)
+  double* dw;       // (P, K) step
+  double* best_w;   // (P, K)
+  double* S;        // (P, K) current gradient (S;T)
+  double* H;        // (P, K*K) current Gauss-Newton matrix
+  const double* mu; // (P, nmu)
+  const double* dout;  // (P, 1+K+K*K) derivs results
+  const int* ddeg;     // (P)
+  const double* oout;  // (P*LM_B) objective trial results
+  const int* odeg;     // (P*LM_B)
+  int* req_d;          // (P) derivs requested
+  int* req_o;          // (P*LM_B) objective rows requested
+  double* tw;          // (P*LM_B, ku) trial points
+  double* ttau;        // (P*LM_B, kx)
+  double* tmu;         // (P*LM_B, nmu)
+  int* counters;       // [n_active, n_derivs, n_obj]
+  double* hist;        // (P, max_iters+1, 6) or null
+  double* status;      // (P, 8)
+};
+
+__device__ __forceinline__ double nrm2(const double* v, int n) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s = fma(v[i], v[i], s);
+  return sqrt(s);
 }
+
+// LDL^T solve of the n x n symmetric system in A (row-major, overwritten) for
+// x = A^{-1} b; all threads of the block participate.  Returns false when a
+// pivot is zero / non-finite or the solution is non-finite.
+static __device__ bool ldlt_solve(double* A, int n, double* b, double* x, int* flag) {
+  const int t = threadIdx.x, nt = blockDim.x;
+  if (t == 0) *flag = 1;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const double d = A[j * n + j];
+    if (!(d != 0.0) || !isfinite(d)) {
+      if (t == 0) *flag = 0;
+    }
+    __syncthreads();
+    if (*flag == 0) return false;
+    for (int i = j + 1 + t; i < n; i += nt) A[i * n + j] = A[i * n + j] / d;  // L[i][j]
+    __syncthreads();
+    for (int i = j + 1 + t; i < n; i += nt) {
+      const double lij = A[i * n + j] * d;
+      for (int k = j + 1; k <= i; ++k) A[i * n + k] -= lij * A[k * n + j];
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    for (int i = 0; i < n; ++i) {  // L y = b
+      double v = b[i];
+      for (int k = 0; k < i; ++k) v -= A[i * n + k] * x[k];
+      x[i] = v;
+    }
+    for (int i = 0; i < n; ++i) x[i] /= A[i * n + i];
+    for (int i = n - 1; i >= 0; --i) {  // L^T x = z
+      double v = x[i];
+      for (int k = i + 1; k < n; ++k) v -= A[k * n + i] * x[k];
+      x[i] = v;
+    }
+    bool ok = true;
+    for (int i = 0; i < n; ++i) ok = ok && isfinite(x[i]);
+    *flag = ok ? 1 : 0;
+  }
+  __syncthreads();
+  return *flag != 0;
+}
+
+static __global__ void lm_init_kernel(LmRun R, const double* w0, const double* tau0) {
+  const int p = blockIdx.x;
+  for (int i = threadIdx.x; i < R.ku; i += blockDim.x) R.w[p * R.ku + i] = w0[p * R.ku + i];
+  for (int i = threadIdx.x; i < R.kx; i += blockDim.x) R.tau[p * R.kx + i] = tau0[p * R.kx + i];
+  if (threadIdx.x == 0) {
+    LmState s;
+    memset(&s, 0, sizeof(s));
+    s.phase = PH_START;
+    s.lam = R.cfg.lambda0;
+    s.lam_set = R.cfg.lambda0 >= 0.0;
+    R.st[p] = s;
+  }
+}
+
+// post objective trials at w + alpha_j dw (state init: tau frozen, dz = dw only)
+static __device__ void post_trials(const LmRun& R, int p, int j0, bool frozen_tau, int ntr) {
+  for (int j = 0; j < LM_B; ++j) {
+    const int row = p * LM_B + j;
+    const bool on = j < ntr;
+    R.req_o[row] = on;
+    if (!on) continue;
+    const double alpha = ldexp(1.0, -(j0 + j));
+    for (int i = 0; i < R.ku; ++i) R.tw[row * R.ku + i] = R.w[p * R.ku + i] + alpha * R.dw[p * R.K + i];
+    for (int i = 0; i < R.kx; ++i)
+      R.ttau[row * R.kx + i] = R.tau[p * R.kx + i] + (frozen_tau ? 0.0 : alpha * R.dw[p * R.K + R.ku + i]);
+    for (int i = 0; i < R.nmu; ++i) R.tmu[row * R.nmu + i] = R.mu[p * R.nmu + i];
+  }
+}
+
+static __device__ void hist_row(const LmRun& R, int p, int it, double J, double nS, double nT, double lam, double alpha) {
+  if (!R.hist) return;
+  double* h = R.hist + ((size_t)p * (R.cfg.max_iters + 1) + it) * 6;
+  h[0] = it; h[1] = J; h[2] = nS; h[3] = nT; h[4] = lam; h[5] = alpha;
+}
+
+enum LmAction { ACT_ADVANCE = 0, ACT_SOLVE_SI = 1, ACT_SOLVE_MAIN = 2, ACT_WAIT = 3 };
+
+__device__ __forceinline__ void lm_fill_main(const LmRun& R, int p, const LmState& s, double* A, double* rhs) {
+  const int K = R.K, ku = R.ku, kx = R.kx;
+  const double* Hm = R.H + (size_t)p * K * K;
+  const double* Sv = R.S + p * K;
+  for (int i = 0; i < K * K; ++i) A[i] = Hm[i];
+  for (int i = 0; i < kx; ++i) A[(ku + i) * K + ku + i] += s.lam;
+  for (int i = 0; i < K; ++i) rhs[i] = -Sv[i];
+}
+
+__device__ __forceinline__ void lm_request_derivs(const LmRun& R, int p, LmState& s, int phase) {
+  s.phase = phase;
+  R.req_d[p] = 1;
+  s.evals++;
+}
+
+// escalate after a failed attempt (lm.py:215-225, 237-241); returns the next action
+__device__ __forceinline__ int lm_escalate(const LmRun& R, int p, LmState& s, double* A, double* rhs, bool singular) {
+  const LmCfg& c = R.cfg;
+  s.lam = singular ? fmax(2.0 * s.lam, 1e-12) * 10.0 : fmax(4.0 * s.lam, 1e-12);
+  s.attempts += 1;
+  if (s.lam > c.lambda_cap || s.attempts >= 60) {
+    s.reason = R_LS_FAIL;
+    s.phase = PH_DONE;
+    return ACT_WAIT;
+  }
+  lm_fill_main(R, p, s, A, rhs);
+  return ACT_SOLVE_MAIN;
+}
+
+// advance the state machine from the current phase; thread 0 only
+static __device__ int lm_advance(const LmRun& R, int p, LmState& s, double* A, double* rhs) {
+  const LmCfg& c = R.cfg;
+  const int K = R.K, ku = R.ku, kx = R.kx;
+  double* Sv = R.S + p * K;
+  double* Hm = R.H + (size_t)p * K * K;
+  const double* d = R.dout + (size_t)p * (1 + K + K * K);
+  switch (s.phase) {
+    case PH_START:
+      if (c.w0_lsq && ku > 0) {
+        s.si_cnt = 0; s.si_have_J = 0;
+        lm_request_derivs(R, p, s, PH_SI_DERIV);
+      } else {
+        lm_request_derivs(R, p, s, PH_MAIN_DERIV);
+      }
+      return ACT_WAIT;
+    case PH_SI_DERIV:
+    case PH_MAIN_DERIV:
+    case PH_MAIN_ACCEPT_DERIV: {
+      if (R.ddeg[p] > 0) {  // derivatives raise DegenerateMappingError out of lm_solve
+        s.reason = R_DEGENERATE;
+        s.phase = PH_DONE;
+        return ACT_WAIT;
+      }
+      for (int i = 0; i < K; ++i) Sv[i] = d[1 + i];
+      for (int i = 0; i < K * K; ++i) Hm[i] = d[1 + K + i];
+      const double Jd = d[0];
+      if (s.phase == PH_SI_DERIV) {  // lm.py:134-141
+        const double nSw = nrm2(Sv, ku);
+        if (s.si_cnt == 0 && !s.si_have_J) s.si_target = c.w0_tol * fmax(1.0, nSw);
+        if (s.si_cnt >= c.w0_iters || nSw <= s.si_target) {
+          lm_request_derivs(R, p, s, PH_MAIN_DERIV);
+          return ACT_WAIT;
+        }
+        for (int i = 0; i < ku; ++i)
+          for (int k2 = 0; k2 < ku; ++k2) A[i * ku + k2] = Hm[i * K + k2];
+        for (int i = 0; i < ku; ++i) rhs[i] = -Sv[i];
+        return ACT_SOLVE_SI;
+      }
+      if (s.phase == PH_MAIN_DERIV) {  // lm.py:185
+        s.J = Jd;
+        s.it = 0;
+        s.phase = PH_MAIN_ITER_READY;
+        return ACT_ADVANCE;
+      }
+      // accepted step: gain ratio, curvature, damping update (lm.py:248-264)
+      const double pred = -0.5 * s.alpha * s.gdot;
+      const double ratio = pred > 0.0 ? (s.J_prev - s.J_new) / pred : 1.0;
+      s.J = isfinite(s.J_new) ? s.J_new : Jd;
+      double sd = 0.0;
+      for (int i = 0; i < K; ++i) sd = fma(Sv[i], R.dw[p * K + i], sd);
+      const bool curv_ok = sd >= c.c2 * s.gdot;
+      if (s.alpha < 0.25 || ratio < c.ratio_lo) s.lam *= c.lambda_inc;
+      else if (s.alpha == 1.0 && ratio > c.ratio_hi && curv_ok) s.lam *= c.lambda_dec;
+      s.lam = fmin(fmax(s.lam, s.lam_floor), c.lambda_cap);
+      hist_row(R, p, s.it, s.J_prev, s.nS_prev, s.nT_prev, s.lam, s.alpha);
+      s.it += 1;
+      s.phase = PH_MAIN_ITER_READY;
+      return ACT_ADVANCE;
+    }
+    case PH_SI_BASEJ: {  // J = problem.objective(w, tau) (lm.py:146)
+      const int row = p * LM_B;
+      s.J_si = R.odeg[row] > 0 ? INFINITY : R.oout[row];
+      s.si_have_J = 1;
+      s.j0 = 0;
+      s.phase = PH_SI_LS;
+      post_trials(R, p, 0, true, LM_B);
+      s.evals++;
+      return ACT_WAIT;
+    }
+    case PH_SI_LS: {  // Armijo on the frozen-tau state step (lm.py:147-160)
+      double sdw = 0.0;
+      for (int i = 0; i < ku; ++i) sdw = fma(Sv[i], R.dw[p * K + i], sdw);
+      for (int j = 0; j < LM_B && s.j0 + j < 30; ++j) {
+        const int row = p * LM_B + j;
+        const double Jt = R.odeg[row] > 0 ? INFINITY : R.oout[row];
+        const double alpha = ldexp(1.0, -(s.j0 + j));
+        if (Jt <= s.J_si + 1e-4 * alpha * sdw) {
+          for (int i = 0; i < ku; ++i) R.w[p * ku + i] += alpha * R.dw[p * K + i];
+          s.J_si = Jt;
+          s.si_cnt += 1;
+          lm_request_derivs(R, p, s, PH_SI_DERIV);
+          return ACT_WAIT;
+        }
+      }
+      if (s.j0 + LM_B < 30) {
+        s.j0 += LM_B;
+        post_trials(R, p, s.j0, true, min(LM_B, 30 - s.j0));
+        s.evals++;
+        return ACT_WAIT;
+      }
+      lm_request_derivs(R, p, s, PH_MAIN_DERIV);  // not accepted: leave the state init
+      return ACT_WAIT;
+    }
+    case PH_MAIN_ITER_READY: {  // top of the LM iteration (lm.py:187-211)
+      if (s.it >= c.max_iters) {
+        s.reason = R_MAX_ITERS;
+        s.phase = PH_DONE;
+        return ACT_WAIT;
+      }
+      const double nS = nrm2(Sv, ku), nT = nrm2(Sv + ku, kx);
+      if (!s.have_best || s.J < s.best_J) {
+        s.have_best = 1; s.best_J = s.J; s.best_nS = nS; s.best_nT = nT;
+        for (int i = 0; i < ku; ++i) R.best_w[p * K + i] = R.w[p * ku + i];
+        for (int i = 0; i < kx; ++i) R.best_w[p * K + ku + i] = R.tau[p * kx + i];
+      }
+      if (!s.lam_set) {
+        if (kx) {
+          double tr = 0.0;
+          for (int i = 0; i < kx; ++i) tr += Hm[(ku + i) * K + ku + i];
+          s.lam = 1e-4 * tr / kx;
+        } else {
+          s.lam = 0.0;
+        }
+        s.lam_floor = s.lam > 0.0 ? 1e-10 * s.lam : 0.0;
+        s.lam_set = 1;
+      }
+      hist_row(R, p, s.it, s.J, nS, nT, s.lam, NAN);
+      if (nS <= c.eps1 && nT <= c.eps2) {
+        hist_row(R, p, s.it, s.J, nS, nT, s.lam, 0.0);
+        s.reason = R_FIRST_ORDER;
+        s.n_done = s.it;
+        s.done = 2;
+        s.phase = PH_DONE;
+        return ACT_WAIT;
+      }
+      s.n_done = s.it + 1;
+      s.nS_prev = nS; s.nT_prev = nT; s.J_prev = s.J;
+      s.attempts = 0;
+      lm_fill_main(R, p, s, A, rhs);
+      return ACT_SOLVE_MAIN;
+    }
+    case PH_MAIN_LS: {  // Armijo backtracking results (lm.py:226-236)
+      for (int j = 0; j < LM_B && s.j0 + j < c.max_backtracks; ++j) {
+        const int row = p * LM_B + j;
+        const double Jt = R.odeg[row] > 0 ? INFINITY : R.oout[row];
+        const double alpha = ldexp(1.0, -(s.j0 + j));
+        if (Jt <= s.J + c.c1 * alpha * s.gdot) {
+          s.J_new = Jt;
+          s.alpha = alpha;
+          for (int i = 0; i < ku; ++i) R.w[p * ku + i] += alpha * R.dw[p * K + i];
+          for (int i = 0; i < kx; ++i) R.tau[p * kx + i] += alpha * R.dw[p * K + ku + i];
+          lm_request_derivs(R, p, s, PH_MAIN_ACCEPT_DERIV);
+          return ACT_WAIT;
+        }
+      }
+      if (s.j0 + LM_B < c.max_backtracks) {
+        s.j0 += LM_B;
+        post_trials(R, p, s.j0, false, min(LM_B, c.max_backtracks - s.j0));
+        s.evals++;
+        return ACT_WAIT;
+      }
+      return lm_escalate(R, p, s, A, rhs, false);
+    }
+    case PH_DONE:
+    default:
+      return ACT_WAIT;
+  }
+}
+
+// process a finished solve; thread 0 only
+static __device__ int lm_after_solve(const LmRun& R, int p, LmState& s, int act, bool ok, const double* x, double* A,
+                              double* rhs) {
+  const int K = R.K, ku = R.ku, kx = R.kx, nmu = R.nmu;
+  if (act == ACT_SOLVE_SI) {
+    if (!ok) {  // LinAlgError ends the state init (lm.py:142-143)
+      lm_request_derivs(R, p, s, PH_MAIN_DERIV);
+      return ACT_WAIT;
+    }
+    for (int i = 0; i < ku; ++i) R.dw[p * K + i] = x[i];
+    if (!s.si_have_J) {
+      s.phase = PH_SI_BASEJ;
+      const int row = p * LM_B;
+      R.req_o[row] = 1;
+      for (int i = 0; i < ku; ++i) R.tw[row * ku + i] = R.w[p * ku + i];
+      for (int i = 0; i < kx; ++i) R.ttau[row * kx + i] = R.tau[p * kx + i];
+      for (int i = 0; i < nmu; ++i) R.tmu[row * nmu + i] = R.mu[p * nmu + i];
+    } else {
+      s.j0 = 0;
+      s.phase = PH_SI_LS;
+      post_trials(R, p, 0, true, LM_B);
+    }
+    s.evals++;
+    return ACT_WAIT;
+  }
+  // main iteration attempt (lm.py:212-225)
+  if (!ok) return lm_escalate(R, p, s, A, rhs, true);
+  const double* Sv = R.S + p * K;
+  double gd = 0.0;
+  for (int i = 0; i < K; ++i) gd = fma(Sv[i], x[i], gd);
+  if (!isfinite(gd) || gd >= 0.0) return lm_escalate(R, p, s, A, rhs, false);
+  s.gdot = gd;
+  for (int i = 0; i < K; ++i) R.dw[p * K + i] = x[i];
+  s.j0 = 0;
+  s.phase = PH_MAIN_LS;
+  post_trials(R, p, 0, false, min(LM_B, R.cfg.max_backtracks));
+  s.evals++;
+  return ACT_WAIT;
+}
+
+// one control round; blockDim = LM_THREADS, dynamic smem (K*K + 2K) doubles
+static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) {
+  extern __shared__ double sm[];
+  const int p = blockIdx.x, K = R.K;
+  double* A = sm;
+  double* rhs = A + K * K;
+  double* x = rhs + K;
+  __shared__ int s_act, s_flag;
+  __shared__ LmState s;
+  if (threadIdx.x == 0) {
+    s = R.st[p];
+    R.req_d[p] = 0;
+    for (int j = 0; j < LM_B; ++j) R.req_o[p * LM_B + j] = 0;
+    s_act = ACT_ADVANCE;
+  }
+  __syncthreads();
+  for (int guard = 0; guard < 100000; ++guard) {
+    if (threadIdx.x == 0 && s_act == ACT_ADVANCE) s_act = lm_advance(R, p, s, A, rhs);
+    __syncthreads();
+    const int act = s_act;
+    if (act == ACT_WAIT) break;
+    if (act == ACT_ADVANCE) continue;
+    const int n = act == ACT_SOLVE_SI ? R.ku : K;
+    const bool ok = ldlt_solve(A, n, rhs, x, &s_flag);
+    if (threadIdx.x == 0) s_act = lm_after_solve(R, p, s, act, ok, x, A, rhs);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    R.st[p] = s;
+    if (s.phase != PH_DONE) atomicAdd(&R.counters[0], 1);
+    if (R.req_d[p]) atomicAdd(&R.counters[1], 1);
+    if (R.req_o[p * LM_B]) atomicAdd(&R.counters[2], 1);
+  }
+}
+
+// results: best-iterate fallback (lm.py:266-270) and status rows
+static __global__ void lm_finish_kernel(LmRun R) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= R.P) return;
+  LmState& s = R.st[p];
+  const int K = R.K, ku = R.ku, kx = R.kx;
+  double J = s.J;
+  double nS = nrm2(R.S + p * K, ku), nT = nrm2(R.S + p * K + ku, kx);
+  const bool conv = s.reason == R_FIRST_ORDER;
+  if (!conv && s.reason != R_DEGENERATE && s.have_best && s.best_J < J) {
+    J = s.best_J; nS = s.best_nS; nT = s.best_nT;
+    for (int i = 0; i < ku; ++i) R.w[p * ku + i] = R.best_w[p * K + i];
+    for (int i = 0; i < kx; ++i) R.tau[p * kx + i] = R.best_w[p * K + ku + i];
+  }
+  double* o = R.status + (size_t)p * 8;
+  o[0] = conv ? 1.0 : 0.0;
+  o[1] = J;
+  o[2] = nS;
+  o[3] = nT;
+  o[4] = conv ? s.n_done : s.n_done;
+  o[5] = s.reason;
+  o[6] = s.lam;
+  o[7] = s.evals;
+}
+
+}  // namespace strom

@@ -1,0 +1,149 @@
+"""Batched Levenberg-Marquardt on the GPU (strom/lm.py:30-271 semantics).
+
+``lm_solve(problem, config, w0_mode)`` keeps the reference signature and
+result type; ``problem`` must be a ``ReducedTrackingProblem`` over a
+``GpuReducedOperator`` (the whole solve then runs as the device-side state
+machine of csrc/lm_kernels.cuh).  ``lm_solve_batched`` solves many
+parameter points at once — the online EQP-IFT solve of SURVEY §8 row a21
+with P parameters in flight.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .reduced import GpuReducedOperator, degenerate_error
+
+REASONS = {0: "first-order", 1: "max-iters", 2: "line-search-failure", 3: "degenerate"}
+
+
+@dataclass
+class LmConfig:
+    """Mirror of strom.lm.LmConfig (lm.py:30-51)."""
+
+    eps1: float = 1e-8
+    eps2: float = 1e-8
+    lambda0: float = None
+    lambda_inc: float = 2.0
+    lambda_dec: float = 1.0 / 3.0
+    ratio_hi: float = 0.75
+    ratio_lo: float = 0.25
+    max_iters: int = 200
+    wolfe_c1: float = 1e-4
+    wolfe_c2: float = 0.9
+    max_backtracks: int = 30
+    lambda_cap: float = 1e14
+    w0_inner_tol: float = 1e-10
+    w0_inner_iters: int = 50
+
+    def __post_init__(self):
+        if self.eps1 <= 0 or self.eps2 <= 0:
+            raise ValueError("termination tolerances must be positive")
+        if not (0.0 < self.wolfe_c1 < self.wolfe_c2 < 1.0):
+            raise ValueError("need 0 < c1 < c2 < 1")
+
+    def packed(self, w0_mode):
+        lam0 = -1.0 if self.lambda0 is None else float(self.lambda0)
+        return np.array([self.eps1, self.eps2, lam0, self.lambda_inc, self.lambda_dec, self.ratio_hi, self.ratio_lo,
+                         self.max_iters, self.wolfe_c1, self.wolfe_c2, self.max_backtracks, self.lambda_cap,
+                         self.w0_inner_tol, self.w0_inner_iters, 1.0 if w0_mode == "lsq" else 0.0], dtype=np.float64)
+
+
+@dataclass
+class LmResult:
+    """Mirror of strom.lm.LmResult (lm.py:54-64)."""
+
+    w: np.ndarray
+    tau: np.ndarray
+    converged: bool
+    objective: float
+    grad_w_norm: float
+    grad_tau_norm: float
+    n_iters: int
+    history: np.ndarray
+    reason: str = ""
+
+
+class ReducedTrackingProblem:
+    """LM problem over reduced coordinates at one parameter (reduced.py:254-281)."""
+
+    def __init__(self, operator, mu, rho=None, w0=None, tau0=None):
+        self.op = operator
+        self.mu = np.asarray(mu, dtype=float)
+        self.rho = rho
+        self._w0 = np.zeros(operator.bases.k_u) if w0 is None else np.asarray(w0, dtype=float)
+        self._tau0 = np.zeros(operator.bases.k_x) if tau0 is None else np.asarray(tau0, dtype=float)
+
+    @property
+    def nw(self):
+        return self.op.bases.k_u
+
+    @property
+    def ntau(self):
+        return self.op.bases.k_x
+
+    def initial_guess(self):
+        return self._w0.copy(), self._tau0.copy()
+
+    def objective(self, w, tau):
+        from .reduced import ReducedCoords
+
+        return self.op.objective(ReducedCoords(w, tau), self.mu, self.rho)
+
+    def derivatives(self, w, tau):
+        from .reduced import ReducedCoords
+
+        return self.op.derivatives(ReducedCoords(w, tau), self.mu, self.rho)
+
+
+def lm_solve_batched(op, mus, W0=None, Tau0=None, rho=None, config=None, w0_mode="lsq", want_history=True,
+                     raise_degenerate=False):
+    """Solve P reduced problems (one per row of ``mus``) on the GPU at once."""
+    if not isinstance(op, GpuReducedOperator):
+        raise TypeError("lm_solve_batched needs a GpuReducedOperator")
+    if w0_mode not in ("lsq", "keep"):
+        raise ValueError(f"unknown w0_mode {w0_mode!r}")
+    cfg = config or LmConfig()
+    mus = np.atleast_2d(np.asarray(mus, dtype=float))
+    P, ku, kx = mus.shape[0], op.k_u, op.k_x
+    dev = op.device
+    Mu = torch.as_tensor(np.stack([op._mu(m) for m in mus])).to(dev)
+    W = torch.as_tensor(np.zeros((P, ku)) if W0 is None else np.broadcast_to(np.asarray(W0, float), (P, ku)).copy()).to(dev)
+    Tau = torch.as_tensor(np.zeros((P, kx)) if Tau0 is None else np.broadcast_to(np.asarray(Tau0, float), (P, kx)).copy()).to(dev)
+    act, rw, A = op._weights(rho)
+    status = torch.zeros((P, 8), dtype=torch.float64, device=dev)
+    hist = torch.zeros((P, cfg.max_iters + 1, 6), dtype=torch.float64, device=dev) if want_history else None
+    packed = cfg.packed(w0_mode)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    lib = _lib.load()
+    rc = lib.strom_lm_solve(op._h, W.data_ptr(), Tau.data_ptr() if kx else W.data_ptr(), Mu.data_ptr(), P,
+                            act.data_ptr() if act is not None else None, rw.data_ptr() if rw is not None else None, A,
+                            packed.ctypes.data, status.data_ptr(), hist.data_ptr() if hist is not None else None, stream)
+    _lib.check(rc, "strom_lm_solve")
+    op.stats["lm_solves"] = op.stats.get("lm_solves", 0) + P
+    Wh, Th, st = W.cpu().numpy(), Tau.cpu().numpy(), status.cpu().numpy()
+    H = hist.cpu().numpy() if hist is not None else None
+    out = []
+    for p in range(P):
+        conv = bool(st[p, 0])
+        reason = REASONS[int(st[p, 5])]
+        if reason == "degenerate" and raise_degenerate:
+            raise degenerate_error(np.zeros(0, dtype=np.int64))
+        n = int(st[p, 4])
+        rows = n + 1 if conv else n
+        out.append(LmResult(Wh[p].copy(), Th[p].copy(), conv, float(st[p, 1]), float(st[p, 2]), float(st[p, 3]), n,
+                            H[p, :rows].copy() if H is not None else None, reason))
+    return out
+
+
+def lm_solve(problem, config=None, w0_mode="lsq"):
+    """Reference-signature LM solve (lm.py:164); the problem must wrap a GpuReducedOperator."""
+    op = getattr(problem, "op", None)
+    if not isinstance(op, GpuReducedOperator):
+        raise NotImplementedError("lm_solve runs on the GPU operator only (no CPU fallback)")
+    w0, tau0 = problem.initial_guess()
+    res = lm_solve_batched(op, [problem.mu], w0[None], tau0[None], problem.rho, config, w0_mode,
+                           raise_degenerate=True)
+    return res[0]
