@@ -87,6 +87,14 @@ int strom_create(const strom_mesh_desc* mesh, const strom_law_desc* law, const s
 int strom_set_bases(strom_handle* h, const double* phi, int32_t ku, const double* psi, int32_t kx,
                     const double* ref_coords, const double* state_offset);
 
+/* Per-parameter affine offsets (training snapshots, config 4): evaluation row
+ * p uses U0 = state_offset + p*state_stride and X = ref_coords + p*coord_stride
+ * (strides in doubles; 0 = shared).  Replaces the offsets of strom_set_bases.
+ * There is no reference counterpart (the reference evaluates one snapshot per
+ * call, eqp.py:104-106). */
+int strom_set_offsets(strom_handle* h, const double* state_offset, int64_t state_stride,
+                      const double* ref_coords, int64_t coord_stride);
+
 /* Size the workspace for up to max_P parameters and max_active elements. */
 int strom_reserve(strom_handle* h, int32_t max_P, int32_t max_active);
 

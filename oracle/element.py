@@ -328,3 +328,13 @@ class OracleReducedOperator:
                 np.einsum("bik,bi->bk", Jw, out.res_face.val),
                 np.einsum("bik,bi->bk", Jt, out.res_vol.val) + dN * N.val[:, None],
                 np.einsum("bik,bi->bk", Jt, out.res_face.val))
+
+
+def elemental_objective(op, w, tau, mu):
+    """Per-element 0.5(|R_e|^2 + N_e^2) over all elements (the LP 'output' row of
+    config 4; the summand of reduced.py:181-184)."""
+    els = np.arange(op.geom.mesh.num_elements)
+    Ue, Un, xe = op._inputs(els, w, tau, False)
+    out = element_eval(op.law, op.geom, els, Ue, Un, xe, mu)
+    N = distortion_eval(op.geom, els, xe, op.kappa, op.eps)
+    return 0.5 * (np.sum(out.res ** 2, axis=1) + N ** 2)

@@ -28,7 +28,7 @@ class DistDesc(C.Structure):
     _fields_ = [("kappa", C.c_double), ("eps", C.c_double)]
 
 
-EXPORTS = ("strom_create", "strom_set_bases", "strom_reserve", "strom_eval", "strom_degenerate_elements",
+EXPORTS = ("strom_create", "strom_set_bases", "strom_set_offsets", "strom_reserve", "strom_eval", "strom_degenerate_elements",
            "strom_lm_solve", "strom_profile", "strom_profile_ms", "strom_last_error", "strom_destroy")
 
 _lib = None
@@ -51,6 +51,7 @@ def load(path=SO_PATH):
                                  C.POINTER(DistDesc), C.c_int, C.POINTER(vp)]
     lib.strom_set_bases.argtypes = [vp, vp, i32, vp, i32, vp, vp]
     lib.strom_reserve.argtypes = [vp, i32, i32]
+    lib.strom_set_offsets.argtypes = [vp, vp, C.c_int64, vp, C.c_int64]
     lib.strom_eval.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp, i32]
     lib.strom_degenerate_elements.argtypes = [vp, i32, vp, i32]
     lib.strom_lm_solve.argtypes = [vp, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp, vp]

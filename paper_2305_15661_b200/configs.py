@@ -91,10 +91,17 @@ def displacement(rng, nodes, h, n_modes=4, amp=0.05):
     return d
 
 
-def freestream_field(rng, ne, nb, mach, gamma=1.4, jitter=0.05):
-    """Freestream times (1 + U(-jitter, jitter)), one factor per DG node."""
+def freestream_field(rng, ne, nb, mach, gamma=1.4, jitter=0.05, per_component=False):
+    """Freestream times (1 + U(-jitter, jitter)), one factor per DG node
+    (config 2's definition) or one per node and component.
+
+    With a common factor the velocity and sound speed are identical on both
+    sides of every face, so the LLF max(ws_in, ws_out) is an exact tie whose
+    one-sided derivative is decided by last-bit rounding (reference and GPU
+    may legitimately differ there); parity inputs use ``per_component``.
+    """
     ff = L.euler_freestream(mach, gamma)
-    fac = 1.0 + rng.uniform(-jitter, jitter, size=(ne, nb, 1))
+    fac = 1.0 + rng.uniform(-jitter, jitter, size=(ne, nb, 4 if per_component else 1))
     return (fac * ff[None, None, :]).reshape(-1)
 
 
@@ -166,6 +173,6 @@ def snapshot_fields(case, S, seed, mach_range=(2.0, 4.0)):
     mesh = case.mesh
     h = (1.5 - 0.5) / max(1, int(round(np.sqrt(mesh.num_elements / 2))))
     mus = rng.uniform(*mach_range, size=(S, 1))
-    U = np.stack([freestream_field(rng, mesh.num_elements, 6, m[0]) for m in mus])
+    U = np.stack([freestream_field(rng, mesh.num_elements, 6, m[0], per_component=True) for m in mus])
     X = np.stack([(mesh.nodes + displacement(rng, mesh.nodes, h)).ravel() for _ in range(S)])
     return mus, U, X

@@ -132,6 +132,16 @@ extern "C" int strom_set_bases(strom_handle* h, const double* phi, int32_t ku, c
   if (ku > DERIV_THREADS) return fail(-1, "k_u too large");
   if ((ku && !phi) || (kx && !psi) || !ref_coords) return fail(-1, "missing basis pointer");
   h->Phi = phi; h->ku = ku; h->Psi = psi; h->kx = kx; h->xref = ref_coords; h->u0 = state_offset;
+  h->u0_stride = 0; h->x_stride = 0;
+  return 0;
+}
+
+extern "C" int strom_set_offsets(strom_handle* h, const double* state_offset, int64_t state_stride,
+                                 const double* ref_coords, int64_t coord_stride) {
+  if (!h || !ref_coords) return fail(-1, "strom_set_offsets: null argument");
+  if (state_stride < 0 || coord_stride < 0) return fail(-1, "strom_set_offsets: negative stride");
+  h->u0 = state_offset; h->u0_stride = state_offset ? state_stride : 0;
+  h->xref = ref_coords; h->x_stride = coord_stride;
   return 0;
 }
 

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(WTHREADS) derivs_warp_kernel(
     if (k < 6) {
       const int n = r.elem_nodes[3 * e + (k >> 1)];
       const int row = 2 * n + (k & 1);
-      double v = r.xref[row];
+      double v = r.xref[(size_t)p * r.x_stride + row];
       const double* ps = r.psi + (size_t)row * kx;
       for (int a = 0; a < kx; ++a) v = fma(ps[a], s_tau[a], v);
       S[SH::MX + k] = v;
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(WTHREADS) derivs_warp_kernel(
 #pragma unroll
       for (int j = 0; j < 32 / TPU; ++j) {
         const int i = k * (32 / TPU) + j;
-        if (i < NU) S[SH::UE + i] = v[j] + (r.u0 ? r.u0[(size_t)e * NU + i] : 0.0);
+        if (i < NU) S[SH::UE + i] = v[j] + (r.u0 ? r.u0[(size_t)p * r.u0_stride + (size_t)e * NU + i] : 0.0);
       }
     }
     {
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(WTHREADS) derivs_warp_kernel(
           if (r.u0 && (fin[f] >> 3) == 0) {
             const int nf = fin[f] & 3;
             const int node = jj == 0 ? nf : (jj == 1 ? (nf + 1) % 3 : 3 + nf * (PD - 1) + (jj - 2));
-            off = r.u0[(size_t)nbr[f] * NU + node * M + c];
+            off = r.u0[(size_t)p * r.u0_stride + (size_t)nbr[f] * NU + node * M + c];
           }
           S[SH::UNF + i] = v[j] + off;
         }

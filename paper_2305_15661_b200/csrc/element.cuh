@@ -42,6 +42,7 @@ struct Run {
   const double* __restrict__ psi;
   const double* __restrict__ xref;
   const double* __restrict__ u0;
+  long long u0_stride, x_stride;  // per-parameter offsets (snapshots): U0 + p*u0_stride, X + p*x_stride
   int ku, kx, K, KP, LDJ;
   // call
   const double* __restrict__ w;

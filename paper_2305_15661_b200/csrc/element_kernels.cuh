@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(128) value_kernel(const __grid_constant__ Para
 #pragma unroll
       for (int ic = 0; ic < 2; ++ic) {
         int row = 2 * n + ic;
-        double v = r.xref[row];
+        double v = r.xref[(size_t)p * r.x_stride + row];
         const double* ps = r.psi + (size_t)row * r.kx;
         for (int a = 0; a < r.kx; ++a) v = fma(ps[a], tau[a], v);
         x[2 * g + ic] = v;
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(128) value_kernel(const __grid_constant__ Para
       const double* ph = r.phi + (size_t)e * NU * r.ku;
 #pragma unroll
       for (int i = 0; i < NU; ++i) {
-        double v = r.u0 ? r.u0[(size_t)e * NU + i] : 0.0;
+        double v = r.u0 ? r.u0[(size_t)p * r.u0_stride + (size_t)e * NU + i] : 0.0;
         for (int k = 0; k < r.ku; ++k) v = fma(ph[i * r.ku + k], w[k], v);
         U[i] = v;
       }
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(128) value_kernel(const __grid_constant__ Para
 #pragma unroll
           for (int c = 0; c < M; ++c) {
             int row = node * M + c;
-            double v = r.u0 ? r.u0[(size_t)nb * NU + row] : 0.0;
+            double v = r.u0 ? r.u0[(size_t)p * r.u0_stride + (size_t)nb * NU + row] : 0.0;
             for (int k = 0; k < r.ku; ++k) v = fma(ph[row * r.ku + k], w[k], v);
             Un[j][c] = v;
           }

@@ -77,7 +77,7 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
   memset(&r, 0, sizeof(r));
   r.ne = h->ne; r.elem_nodes = h->elem_nodes; r.nodes = h->nodes; r.nbr = h->nbr; r.finfo = h->finfo;
   r.eta_ref = h->eta_ref;
-  r.phi = h->Phi; r.psi = h->Psi; r.xref = h->xref; r.u0 = h->u0; r.ku = h->ku; r.kx = h->kx;
+  r.phi = h->Phi; r.psi = h->Psi; r.xref = h->xref; r.u0 = h->u0; r.u0_stride = h->u0_stride; r.x_stride = h->x_stride; r.ku = h->ku; r.kx = h->kx;
   r.K = h->ku + h->kx;
   r.KP = (r.K + 7) / 8 * 8;
   if (r.KP < 8) r.KP = 8;

@@ -67,6 +67,7 @@ struct strom_handle {
   double* eta_ref = nullptr;
   const double *Phi = nullptr, *Psi = nullptr, *xref = nullptr, *u0 = nullptr;
   int ku = 0, kx = 0;
+  long long u0_stride = 0, x_stride = 0;
   double* part = nullptr;
   size_t part_cap = 0;
   int* degen_fill = nullptr;

@@ -284,6 +284,36 @@ class GpuReducedOperator:
         (dg.assemble_global(..., want_jacobians=False), dg.py:238-240)."""
         return self._single(_lib.RESIDUAL, coords, mu, None)
 
+    def contributions_at_snapshots(self, U, X, mus, layout="lprows", out=None):
+        """Element contributions at S explicit training snapshots in one batched pass.
+
+        ``U`` (S, N_u) states and ``X`` (S, N_x) deformed coordinates (cuda
+        float64 tensors) enter as per-snapshot affine offsets at w = 0,
+        tau = 0; ``layout``: "lprows" -> (S, K+1, ne) rows S_e, T_e and
+        0.5(|R_e|^2 + N_e^2) (config 4), "split" -> (S, ne, 2K) (Sv, Sf, Tv,
+        Tf) as in eqp.build_lp (eqp.py:104-114), "total" -> (S, ne, K).
+        """
+        S = int(X.shape[0])
+        mode = {"lprows": _lib.CONTRIB_LPROWS, "split": _lib.CONTRIB_SPLIT, "total": _lib.CONTRIB}[layout]
+        lib = self._lib
+        U = None if U is None else U.contiguous()
+        X = X.contiguous()
+        _lib.check(lib.strom_set_offsets(self._h, U.data_ptr() if U is not None else None,
+                                         int(U.shape[1]) if U is not None else 0, X.data_ptr(), int(X.shape[1])),
+                   "strom_set_offsets")
+        try:
+            W = torch.zeros((S, max(self.k_u, 1)), dtype=torch.float64, device=self.device)
+            Tau = torch.zeros((S, max(self.k_x, 1)), dtype=torch.float64, device=self.device)
+            Mu = torch.as_tensor(np.stack([self._mu(m) for m in np.atleast_2d(mus)])).to(self.device)
+            res, _ = self.eval_batched(mode, W, Tau, Mu, None, out=out)
+        finally:
+            _lib.check(lib.strom_set_offsets(self._h, self.u0.data_ptr() if self.u0 is not None else None, 0,
+                                             self.ref_coords.data_ptr(), 0), "strom_set_offsets")
+        K = self.k_u + self.k_x
+        ne = self.dm.ne
+        shape = {"lprows": (S, K + 1, ne), "split": (S, ne, 2 * K), "total": (S, ne, K)}[layout]
+        return res.view(shape)
+
     def residual_norm(self, coords, mu):
         """||R||_2 of the full-mesh residual (greedy error indicator)."""
         return float(np.sqrt(self._single(_lib.RESNORM2, coords, mu, None)[0]))
