@@ -1,0 +1,660 @@
+// K1 / K3 derivatives kernel on DMMA for 4-component laws with p = 2 (Euler).
+//
+// One warp per element.  The reduced Jacobian is formed as a projection of
+// the element's local Jacobian instead of propagating k_u tangents:
+//   L    = -sum_q Dq^T B_q Pq + sum_f (face-in blocks)        (24 x 24)
+//   J_U  = L Phi_e + sum_f E_f Lout_f Phi_nf                  (24 x k_u)
+//   J_x  = (dR/dx_e) Psi_e                                    (24 x k_x)
+//   H   += rho J^T J   (upper 8x8 tiles)
+// with every GEMM on mma.sync.m8n8k4.f64 (DMMA): the Dq^T B_q product is
+// fused into the A-fragment loads of the L GEMM (no explicit X matrix), the
+// basis rows are read as B fragments straight from global memory (L1/L2
+// hits: the gather stage touched them), and the reference-element trace /
+// basis tables are per-lane constant registers.  Pointwise physics, residual
+// rows, gathers and the Gram are shared with derivs_warp.cuh's design.
+#pragma once
+#include "derivs_warp.cuh"
+
+namespace strom {
+
+constexpr int MTHREADS = 256;
+
+template <int NQ>
+struct MShape {
+  static constexpr int M = 4, NB = 6, NU = 24, NF = 3, NS = 4, NFS = 12, NNB = 36, P = 2;
+  static constexpr int NQ4 = (NQ + 3) / 4 * 4;
+  static constexpr int NQC = NQ4 % 8 == 4 ? NQ4 : NQ4 + 4;  // BQ point stride (== 4 mod 8: conflict-free fragments)
+  static constexpr int NQP = NQ % 2 ? NQ : NQ + 1;
+  static constexpr int NFSP = 13;
+  static constexpr int FXS = 3 * M + 3;
+  // per-warp smem layout (doubles)
+  static constexpr int MX = 0, MJ = 6, MADJ = 10, MDET = 14, MDETR = 15, MNU = 16, MNLEN = 22, MNHAT = 25, MN = 31,
+                       MRHO = 32, DNX = 33, DNP = 40, MINT = 56;
+  static constexpr int UE = 64;
+  static constexpr int UNF = UE + NU;
+  static constexpr int RT = UNF + NNB;
+  static constexpr int RV = RT + NU;
+  static constexpr int RF = RV + NU;
+  static constexpr int TQ = RF + NU;            // [4][NU]
+  static constexpr int FX = TQ + 4 * NU;        // [field][NFSP]
+  static constexpr int FQ = FX + FXS * NFSP;    // [c][i][NQP]
+  static constexpr int HS = FQ + 2 * M * NQP;   // [c][NFSP]
+  static constexpr int FD = HS + M * NFSP;      // face mesh-response [f][s][c][2]
+  static constexpr int RA = FD + 2 * M * NFSP;
+  static constexpr int LDX = 12;
+  // region A (offsets from RA), by phase:
+  //   P/L : BQ [q][c][kk][c'] at 0           -> L [NU][LDL] at 0 once the L GEMM has read BQ
+  //   P/F : CF [fs][side][c][c'] at LA       (read by the face blocks)
+  //   F/J : LOUT [3][12][LDO] at LO          (read by the projection)
+  //   X/G : DRX [NU][LDX] at LO (LOUT dead), Jt [NU][LDJ] at 0 (L, CF dead)
+  static constexpr int LDL = 28, LDO = 20;
+  static constexpr int BQ = 0, LL = 0;
+  static constexpr int LA = (32 * NQC > NU * LDL ? 32 * NQC : NU * LDL);
+  static constexpr int CF = LA;
+  static constexpr int LO = LA + 32 * NFSP;
+  static constexpr int DRX = LO;
+  static constexpr int RAEND = LO + 3 * 12 * LDO;
+  __host__ __device__ static int warp_stride(int LDJ, int KP) {
+    int ra = RAEND > NU * LDJ ? RAEND : NU * LDJ;
+    int s = RA + ra + KP * KP + 48;
+    return (s + 15) / 16 * 16 + 4;
+  }
+};
+
+// local index of element node n on face f (-1 if not on the face), p = 2
+__device__ __forceinline__ int face_local(int f, int n) {
+  const int a = f, b = (f + 1) % 3;
+  return n == a ? 0 : (n == b ? 1 : (n == 3 + f ? 2 : -1));
+}
+
+template <class LAW, int NQ>
+__global__ void __launch_bounds__(MTHREADS) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
+  using SH = MShape<NQ>;
+  constexpr int M = 4, NB = 6, NU = 24, NF = 3, NS = 4, NFS = 12, PD = 2;
+  constexpr int NQP = SH::NQP, NFSP = SH::NFSP, LDL = SH::LDL, LDO = SH::LDO, LDX = SH::LDX;
+  static_assert(LAW::M == 4, "derivs_mma_kernel is specialised for 4-component laws");
+  const auto& T = prm.t;
+  const Run& r = prm.r;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double s_w[KMAX], s_tau[KMAX];
+  __shared__ double s_dphi[NQ * NB * 2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int p = blockIdx.y;
+  if (r.mask && !r.mask[p]) return;
+  const int ku = r.ku, kx = r.kx, K = r.K, KP = r.KP, LDJ = r.LDJ;
+  double* const S = smem + (size_t)warp * r.gx_warp_stride;
+  double* const RA = S + SH::RA;
+  double* const HA = S + r.gx_warp_stride - 4 - 48 - KP * KP;  // warp Gram accumulator (KP x KP)
+  double* const GW = HA + KP * KP;
+
+  for (int i = threadIdx.x; i < ku; i += blockDim.x) s_w[i] = r.w[(size_t)p * ku + i];
+  for (int i = threadIdx.x; i < kx; i += blockDim.x) s_tau[i] = r.tau[(size_t)p * kx + i];
+  for (int i = threadIdx.x; i < NQ * NB * 2; i += blockDim.x) s_dphi[i] = (&T.dphi[0][0][0])[i];
+  for (int i = lane; i < KP * KP; i += 32) HA[i] = 0.0;
+  LawArgs la;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) la.p[i] = r.lawp[i];
+#pragma unroll
+  for (int i = 0; i < NMU; ++i) la.mu[i] = i < r.nmu ? r.mu[p * r.nmu + i] : 0.0;
+  // per-lane constant B fragments of the L GEMM: Phi[q][n'] at (q = 4ks + lane&3, n' = lane>>2)
+  double phib[SH::NQ4 / 4];
+#pragma unroll
+  for (int ks = 0; ks < SH::NQ4 / 4; ++ks) {
+    const int q = 4 * ks + (lane & 3), np_ = lane >> 2;
+    phib[ks] = (q < NQ && np_ < NB) ? T.phi[q < NQ ? q : 0][np_ < NB ? np_ : 0] : 0.0;
+  }
+  __syncthreads();
+
+  double gacc0 = 0.0, gacc1 = 0.0, jacc = 0.0;
+  const int nunits = r.active ? r.A : r.ne;
+  const int nt8 = KP / 8, ntri = nt8 * (nt8 + 1) / 2;
+  const int ntu = (ku + 7) / 8;
+
+  for (int idx = blockIdx.x * nwarps + warp; idx < nunits; idx += gridDim.x * nwarps) {
+    const int e = r.active ? r.active[idx] : idx;
+    const double rho = r.active ? r.rho[idx] : 1.0;
+    int nbr[3], fin[3];
+#pragma unroll
+    for (int f = 0; f < 3; ++f) { nbr[f] = r.nbr[3 * e + f]; fin[f] = r.finfo[3 * e + f]; }
+    // ---- G: coordinates and gathers (lane k = basis column k) --------------------
+    if (lane < 6) {
+      const int n = r.elem_nodes[3 * e + (lane >> 1)];
+      const int row = 2 * n + (lane & 1);
+      double v = r.xref[(size_t)p * r.x_stride + row];
+      const double* ps = r.psi + (size_t)row * kx;
+      for (int a = 0; a < kx; ++a) v = fma(ps[a], s_tau[a], v);
+      S[SH::MX + lane] = v;
+    }
+    // element rows (0..23) and neighbor face-node rows (24..59): one dot product
+    // U = U0 + Phi_row . w per lane, vectorised 16-byte loads of the 8*k_u-byte rows
+    for (int rr = lane; rr < NU + SH::NNB; rr += 32) {
+      const double* src = nullptr;
+      double v = 0.0;
+      int dst;
+      if (rr < NU) {
+        src = r.phi + ((size_t)e * NU + rr) * ku;
+        if (r.u0) v = r.u0[(size_t)p * r.u0_stride + (size_t)e * NU + rr];
+        dst = SH::UE + rr;
+      } else {
+        const int i = rr - NU, f = i / (NF * M), jj = (i / M) % NF, c = i % M;
+        dst = SH::UNF + i;
+        if ((fin[f] >> 3) == 0) {
+          const int nf = fin[f] & 3;
+          const int node = jj == 0 ? nf : (jj == 1 ? (nf + 1) % 3 : 3 + nf);
+          src = r.phi + ((size_t)nbr[f] * NU + node * M + c) * ku;
+          if (r.u0) v = r.u0[(size_t)p * r.u0_stride + (size_t)nbr[f] * NU + node * M + c];
+        }
+      }
+      if (src) {
+        if ((ku & 1) == 0) {
+          const double2* s2 = reinterpret_cast<const double2*>(src);
+          for (int k2 = 0; k2 < (ku >> 1); ++k2) {
+            const double2 t2 = __ldg(s2 + k2);
+            v = fma(t2.x, s_w[2 * k2], v);
+            v = fma(t2.y, s_w[2 * k2 + 1], v);
+          }
+        } else {
+          for (int k = 0; k < ku; ++k) v = fma(__ldg(src + k), s_w[k], v);
+        }
+      }
+      S[dst] = v;
+    }
+    __syncwarp();
+    {  // element geometry (all lanes), distortion gradient (lanes 0-5), face normals (lanes 0-2)
+      double X[6];
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {
+        const int n = r.elem_nodes[3 * e + g];
+        X[2 * g] = r.nodes[2 * n];
+        X[2 * g + 1] = r.nodes[2 * n + 1];
+      }
+      Geo o;
+      element_geo(S + SH::MX, X, o);
+      if (lane < 6) S[SH::DNX + lane] = distortion_grad_dir(o, T.wsum, r.eps, r.kappa, lane);
+      if (lane < 3) face_normal(S + SH::MX, lane, S + SH::MNU + 2 * lane, S[SH::MNLEN + lane], S + SH::MNHAT + 2 * lane);
+      if (lane == 0) {
+        if (o.g <= 0.0) flag_degenerate(r, p, e);
+        S[SH::MJ + 0] = o.J[0][0]; S[SH::MJ + 1] = o.J[0][1]; S[SH::MJ + 2] = o.J[1][0]; S[SH::MJ + 3] = o.J[1][1];
+        S[SH::MADJ + 0] = o.adj[0][0]; S[SH::MADJ + 1] = o.adj[0][1]; S[SH::MADJ + 2] = o.adj[1][0]; S[SH::MADJ + 3] = o.adj[1][1];
+        S[SH::MDET] = o.detJ;
+        S[SH::MDETR] = o.detr;
+        S[SH::MRHO] = rho;
+        S[SH::MN] = r.kappa * (distortion_eta(o, T.wsum, r.eps, nullptr, nullptr) - r.eta_ref[e]);
+      }
+    }
+    __syncwarp();
+    // ---- P: pointwise physics (lanes = face points, then volume points) -----------
+    if (lane < NFS) {
+      const int fs = lane, f = fs / NS, s = fs % NS;
+      const int fi = fin[f], bc = fi >> 3;
+      const double* nu = S + SH::MNU + 2 * f;
+      const double len = S[SH::MNLEN + f];
+      const double* nh = S + SH::MNHAT + 2 * f;
+      double ui[M], uo[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < NF; ++j) v = fma(T.trace[0][s][j], S[SH::UE + fnode_of(PD, f, j) * M + c], v);
+        ui[c] = v;
+      }
+      if (bc == 0) {
+        const int sp = ((fi >> 2) & 1) ? NS - 1 - s : s;
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j < NF; ++j) v = fma(T.trace[0][sp][j], S[SH::UNF + (f * NF + j) * M + c], v);
+          uo[c] = v;
+        }
+      } else if (bc == 1) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) uo[c] = ui[c];
+      } else {
+        LAW::ghost(bc - 2, la, uo);
+      }
+      double fi2[M][2], fo2[M][2], Ai[M][M], Ao[M][M], gi[M], go[M], gni[2], gno[2];
+      const double wsi = PointOps<LAW>::face_side(ui, nu, nh, fi2, Ai, gi, gni, la);
+      const double wso = PointOps<LAW>::face_side(uo, nu, nh, fo2, Ao, go, gno, la);
+      const bool in_wins = wsi >= wso;  // dual.maximum tie -> first argument (dual.py:171)
+      const double lam = in_wins ? wsi : wso;
+      const double ws = T.ws[s];
+      double* FXp = S + SH::FX;
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        const double du = uo[c] - ui[c];
+        const double fni = fi2[c][0] * nu[0] + fi2[c][1] * nu[1], fno = fo2[c][0] * nu[0] + fo2[c][1] * nu[1];
+        S[SH::HS + c * NFSP + fs] = ws * (0.5 * (fni + fno) - 0.5 * (lam * len) * du);
+        FXp[(2 * c + 0) * NFSP + fs] = 0.5 * ws * (fi2[c][0] + fo2[c][0]);
+        FXp[(2 * c + 1) * NFSP + fs] = 0.5 * ws * (fi2[c][1] + fo2[c][1]);
+        FXp[(2 * M + c) * NFSP + fs] = 0.5 * ws * du;
+#pragma unroll
+        for (int cp = 0; cp < M; ++cp) {
+          const double dl_in = in_wins ? gi[cp] : 0.0;
+          const double dl_out = in_wins ? 0.0 : go[cp];
+          double cin = 0.5 * Ai[c][cp] + (c == cp ? 0.5 * lam * len : 0.0) - 0.5 * len * du * dl_in;
+          double cout = 0.5 * Ao[c][cp] - (c == cp ? 0.5 * lam * len : 0.0) - 0.5 * len * du * dl_out;
+          if (bc == 1) { cin += cout; cout = 0.0; }
+          if (bc >= 2) cout = 0.0;
+          RA[SH::CF + ((0 * M + c) * M + cp) * NFSP + fs] = ws * cin;
+          RA[SH::CF + ((1 * M + c) * M + cp) * NFSP + fs] = ws * cout;
+        }
+      }
+      FXp[(3 * M + 0) * NFSP + fs] = lam;
+      FXp[(3 * M + 1) * NFSP + fs] = in_wins ? gni[0] : gno[0];
+      FXp[(3 * M + 2) * NFSP + fs] = in_wins ? gni[1] : gno[1];
+    }
+    for (int q = lane; q < NQ; q += 32) {
+      double uq[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        double v = 0.0;
+#pragma unroll
+        for (int n = 0; n < NB; ++n) v = fma(T.phi[q][n], S[SH::UE + n * M + c], v);
+        uq[c] = v;
+      }
+      const double wq = T.wq[q];
+      double f2[M][2], A0[M][M], A1[M][M];
+      const double d0[2] = {S[SH::MADJ + 0], S[SH::MADJ + 1]}, d1[2] = {S[SH::MADJ + 2], S[SH::MADJ + 3]};
+      PointOps<LAW>::vol_point(uq, d0, d1, f2, A0, A1, la);
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        S[SH::FQ + (c * 2 + 0) * NQP + q] = wq * f2[c][0];
+        S[SH::FQ + (c * 2 + 1) * NQP + q] = wq * f2[c][1];
+#pragma unroll
+        for (int cp = 0; cp < M; ++cp) {
+          RA[SH::BQ + ((0 * M + cp) * M + c) * SH::NQC + q] = wq * A0[c][cp];
+          RA[SH::BQ + ((1 * M + cp) * M + c) * SH::NQC + q] = wq * A1[c][cp];
+        }
+      }
+    }
+    __syncwarp();
+    // ---- R: residual rows (volume / face split) and Tq ------------------------------
+    if (lane < NU) {
+      const int i = lane, n = i / M, c = i % M;
+      double tq[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const double f0 = S[SH::FQ + (c * 2 + 0) * NQP + q], f1 = S[SH::FQ + (c * 2 + 1) * NQP + q];
+        const double d0 = s_dphi[(q * NB + n) * 2 + 0], d1 = s_dphi[(q * NB + n) * 2 + 1];
+        tq[0][0] = fma(d0, f0, tq[0][0]);
+        tq[0][1] = fma(d0, f1, tq[0][1]);
+        tq[1][0] = fma(d1, f0, tq[1][0]);
+        tq[1][1] = fma(d1, f1, tq[1][1]);
+      }
+      const double* adj = S + SH::MADJ;
+      const double rv = -(adj[0] * tq[0][0] + adj[1] * tq[0][1] + adj[2] * tq[1][0] + adj[3] * tq[1][1]);
+      double rf = 0.0;
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        const int j = face_local(f, n);
+        if (j >= 0)
+#pragma unroll
+          for (int s = 0; s < NS; ++s) rf = fma(T.trace[0][s][j], S[SH::HS + c * NFSP + f * NS + s], rf);
+      }
+      S[SH::TQ + 0 * NU + i] = tq[0][0];
+      S[SH::TQ + 1 * NU + i] = tq[0][1];
+      S[SH::TQ + 2 * NU + i] = tq[1][0];
+      S[SH::TQ + 3 * NU + i] = tq[1][1];
+      S[SH::RV + i] = rv;
+      S[SH::RF + i] = rf;
+      S[SH::RT + i] = rv + rf;
+    }
+    // face responses to unit normal-vector perturbations (for the mesh tangents)
+    if (lane < NFS) {
+      const int fs = lane, f = fs / NS;
+      const double* nh = S + SH::MNHAT + 2 * f;
+      const double len = S[SH::MNLEN + f];
+      const double* FXp = S + SH::FX + fs;
+      const double lam = FXp[(3 * M) * NFSP];
+#pragma unroll
+      for (int dir = 0; dir < 2; ++dir) {  // dnu = e_x or e_y
+        const double dnu0 = dir == 0 ? 1.0 : 0.0, dnu1 = dir == 0 ? 0.0 : 1.0;
+        const double dlen = nh[0] * dnu0 + nh[1] * dnu1;
+        const double dnh0 = (dnu0 - nh[0] * dlen) / len, dnh1 = (dnu1 - nh[1] * dlen) / len;
+        const double dlam = FXp[(3 * M + 1) * NFSP] * dnh0 + FXp[(3 * M + 2) * NFSP] * dnh1;
+        const double coef = dlam * len + lam * dlen;
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+          S[SH::FD + (c * 2 + dir) * NFSP + fs] =
+              FXp[(2 * c) * NFSP] * dnu0 + FXp[(2 * c + 1) * NFSP] * dnu1 - FXp[(2 * M + c) * NFSP] * coef;
+      }
+    }
+    __syncwarp();
+    // prefetch the projection's B fragments (basis rows of the element and of the
+    // neighbors' face nodes) so their load latency overlaps the L stage
+    double pfe[6][2], pfn[3][3][2];
+    const bool pref = ntu <= 2;
+    if (pref) {
+      const double* phe = r.phi + (size_t)e * NU * ku;
+#pragma unroll
+      for (int ks = 0; ks < 6; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const int col = nt * 8 + (lane >> 2);
+          pfe[ks][nt] = (nt < ntu && col < ku) ? __ldg(phe + (size_t)(4 * ks + (lane & 3)) * ku + col) : 0.0;
+        }
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        const bool interior = (fin[f] >> 3) == 0;
+        const int nf = fin[f] & 3;
+        const bool flip = (fin[f] >> 2) & 1;
+        const double* phn = r.phi + (size_t)(interior ? nbr[f] : 0) * NU * ku;
+#pragma unroll
+        for (int ks = 0; ks < 3; ++ks) {
+          const int jn = flip ? (ks == 0 ? 1 : (ks == 1 ? 0 : 2)) : ks;
+          const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const int col = nt * 8 + (lane >> 2);
+            pfn[f][ks][nt] = (interior && nt < ntu && col < ku)
+                                 ? __ldg(phn + (size_t)(node * M + (lane & 3)) * ku + col) : 0.0;
+          }
+        }
+      }
+    }
+    // ---- L: volume local Jacobian on DMMA; X = Dq^T B_q fused into the A fragments ------
+    {
+      double lv[4][3][2];
+#pragma unroll
+      for (int cp = 0; cp < 4; ++cp)
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt) lv[cp][mt][0] = lv[cp][mt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < SH::NQ4 / 4; ++ks) {
+        const int q = 4 * ks + (lane & 3);
+        const bool qv = q < NQ;
+        const int qq = qv ? q : 0;
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt) {
+          const int row = mt * 8 + (lane >> 2), n = row >> 2, c = row & 3;
+          const double d0 = qv ? s_dphi[(qq * NB + n) * 2 + 0] : 0.0;
+          const double d1 = qv ? s_dphi[(qq * NB + n) * 2 + 1] : 0.0;
+          const double* B = RA + SH::BQ + c * SH::NQC + qq;
+#pragma unroll
+          for (int cp = 0; cp < 4; ++cp) {
+            const double a = fma(d0, B[(0 * M + cp) * M * SH::NQC], d1 * B[(1 * M + cp) * M * SH::NQC]);
+            dmma(lv[cp][mt][0], lv[cp][mt][1], a, phib[ks]);
+          }
+        }
+      }
+      __syncwarp();  // BQ / CF reads of other lanes finished before L overwrites region A? (L lives after CF)
+      // write -L into L[(n,c)][(n',c')], n' = 2(lane&3) + {0,1}
+#pragma unroll
+      for (int cp = 0; cp < 4; ++cp)
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int np_ = 2 * (lane & 3) + h2;
+            if (np_ < NB) RA[SH::LL + (mt * 8 + (lane >> 2)) * LDL + np_ * M + cp] = -lv[cp][mt][h2];
+          }
+    }
+    __syncwarp();
+    // face blocks: lanes 0-15 add the in-side block into L, lanes 16-31 form Lout
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      const int c = (lane & 15) >> 2, cp = lane & 3, side = lane >> 4;
+      double cs[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) cs[s] = RA[SH::CF + ((side * M + c) * M + cp) * NFSP + f * NS + s];
+#pragma unroll
+      for (int j = 0; j < NF; ++j)
+#pragma unroll
+        for (int jp = 0; jp < NF; ++jp) {
+          double v = 0.0;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) v = fma(T.trace[0][s][j] * T.trace[0][s][jp], cs[s], v);
+          if (side == 0) {
+            RA[SH::LL + (fnode_of(PD, f, j) * M + c) * LDL + fnode_of(PD, f, jp) * M + cp] += v;
+          } else {
+            RA[SH::LO + (f * 12 + j * M + c) * LDO + jp * M + cp] = v;
+          }
+        }
+      __syncwarp();
+    }
+    // ---- J: projection J_U = L Phi_e + sum_f E_f Lout_f Phi_nf on DMMA -----------------
+    const double* L = RA + SH::LL;
+    const double* Lo = RA + SH::LO;
+    double ju[4][3][2];  // up to 4 n-tiles (k_u <= 32)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int mt = 0; mt < 3; ++mt) ju[nt][mt][0] = ju[nt][mt][1] = 0.0;
+    {
+      const double* phe = r.phi + (size_t)e * NU * ku;
+#pragma unroll
+      for (int ks = 0; ks < 6; ++ks) {
+        double af[3];
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt) af[mt] = L[(mt * 8 + (lane >> 2)) * LDL + 4 * ks + (lane & 3)];
+        const int brow = 4 * ks + (lane & 3);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          if (nt < ntu) {
+            const int col = nt * 8 + (lane >> 2);
+            const double b = pref ? pfe[ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phe + (size_t)brow * ku + col) : 0.0);
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
+          }
+        }
+      }
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        if ((fin[f] >> 3) != 0) continue;
+        const int nf = fin[f] & 3;
+        const bool flip = (fin[f] >> 2) & 1;
+        const double* phn = r.phi + (size_t)nbr[f] * NU * ku;
+#pragma unroll
+        for (int ks = 0; ks < 3; ++ks) {  // k = (j', c') = 4 ks + lane&3 -> j' = ks
+          // neighbor face node j' (flip: the two vertex nodes swap, trace(1-s) = trace(s) with swapped vertices)
+          const int jn = flip ? (ks == 0 ? 1 : (ks == 1 ? 0 : 2)) : ks;
+          const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
+          const int brow = node * M + (lane & 3);
+          double af[3];
+#pragma unroll
+          for (int mt = 0; mt < 3; ++mt) {
+            const int row = mt * 8 + (lane >> 2), n = row >> 2, c = row & 3;
+            const int j = face_local(f, n);
+            af[mt] = j >= 0 ? Lo[(f * 12 + j * M + c) * LDO + 4 * ks + (lane & 3)] : 0.0;
+          }
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            if (nt < ntu) {
+              const int col = nt * 8 + (lane >> 2);
+              const double b = pref ? pfn[f][ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phn + (size_t)brow * ku + col) : 0.0);
+#pragma unroll
+              for (int mt = 0; mt < 3; ++mt) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();  // LOUT reads done before DRX overwrites it
+    // ---- X: local mesh Jacobian dR/dx (24 x 6) -------------------------------------------
+    if (lane < NU) {
+      const int i = lane, n = i / M, c = i % M;
+      const double t00 = S[SH::TQ + i], t01 = S[SH::TQ + NU + i], t10 = S[SH::TQ + 2 * NU + i], t11 = S[SH::TQ + 3 * NU + i];
+      double dr[6];
+#pragma unroll
+      for (int d = 0; d < 6; ++d) {
+        const int gv = d >> 1, ic = d & 1;
+        const double c0 = (gv == 1) - (gv == 0), c1 = (gv == 2) - (gv == 0);
+        // ic = 0: dadj = [[0,-c1],[0,c0]]; ic = 1: dadj = [[c1,0],[-c0,0]]
+        dr[d] = ic == 0 ? (c1 * t01 - c0 * t11) : -(c1 * t00 - c0 * t10);
+      }
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        const int j = face_local(f, n);
+        if (j < 0) continue;
+        double rx = 0.0, ry = 0.0;  // face response to dnu = e_x, e_y
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          rx = fma(T.trace[0][s][j], S[SH::FD + (c * 2 + 0) * NFSP + f * NS + s], rx);
+          ry = fma(T.trace[0][s][j], S[SH::FD + (c * 2 + 1) * NFSP + f * NS + s], ry);
+        }
+        const int a = f, b = (f + 1) % 3;
+        // vertex g in {a, b}: del = (g == b) - (g == a); ic = 1 -> dnu = del e_x, ic = 0 -> dnu = -del e_y
+        dr[2 * b + 1] += rx;  dr[2 * a + 1] -= rx;
+        dr[2 * b + 0] -= ry;  dr[2 * a + 0] += ry;
+      }
+#pragma unroll
+      for (int d = 0; d < 6; ++d) RA[SH::DRX + i * LDX + d] = dr[d];
+#pragma unroll
+      for (int d = 6; d < 8; ++d) RA[SH::DRX + i * LDX + d] = 0.0;
+    }
+    __syncwarp();
+    // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
+    double* Jt = RA;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int col = nt * 8 + 2 * (lane & 3) + h2;
+          if (nt < ntu && col < ku) Jt[(mt * 8 + (lane >> 2)) * LDJ + col] = ju[nt][mt][h2];
+        }
+    {
+      double jx[2][3][2];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt) jx[nt][mt][0] = jx[nt][mt][1] = 0.0;
+      const int ntx = (kx + 7) / 8;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int d = 4 * ks + (lane & 3);
+        double af[3];
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt) af[mt] = RA[SH::DRX + (mt * 8 + (lane >> 2)) * LDX + d];
+        const int node = d < 6 ? r.elem_nodes[3 * e + (d >> 1)] : 0;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          if (nt < ntx) {
+            const int col = nt * 8 + (lane >> 2);
+            const double b = (d < 6 && col < kx) ? __ldg(r.psi + (size_t)(2 * node + (d & 1)) * kx + col) : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) dmma(jx[nt][mt][0], jx[nt][mt][1], af[mt], b);
+          }
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int col = nt * 8 + 2 * (lane & 3) + h2;
+            if (col < kx) Jt[(mt * 8 + (lane >> 2)) * LDJ + ku + col] = jx[nt][mt][h2];
+          }
+      // Gram padding columns
+      for (int col = K + lane; col < KP; col += 32)
+#pragma unroll
+        for (int i = 0; i < NU; ++i) Jt[i * LDJ + col] = 0.0;
+      if (lane < kx) {
+        double dn = 0.0;
+#pragma unroll
+        for (int d = 0; d < 6; ++d) {
+          const int node = r.elem_nodes[3 * e + (d >> 1)];
+          dn = fma(S[SH::DNX + d], __ldg(r.psi + (size_t)(2 * node + (d & 1)) * kx + lane), dn);
+        }
+        S[SH::DNP + lane] = dn;
+      }
+    }
+    __syncwarp();
+    {  // L2 prefetch of the next element's basis block (3 KB at k_u = 16)
+      const int nidx = idx + gridDim.x * nwarps;
+      if (nidx < nunits) {
+        const int ne_ = r.active ? r.active[nidx] : nidx;
+        const char* base = reinterpret_cast<const char*>(r.phi + (size_t)ne_ * NU * ku);
+        for (int off = lane * 128; off < NU * ku * 8; off += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+      }
+    }
+    // ---- G: Gram and gradient, or per-element contributions --------------------------------
+    if (r.mode == MODE_DERIVS) {
+      for (int t = 0; t < ntri; ++t) {
+        int ti = 0, rem = t;
+        while (rem >= nt8 - ti) { rem -= nt8 - ti; ++ti; }
+        const int tj = ti + rem;
+        double c0 = 0.0, c1 = 0.0;
+        const double* ja = Jt + (lane & 3) * LDJ + ti * 8 + (lane >> 2);
+        const double* jb = Jt + (lane & 3) * LDJ + tj * 8 + (lane >> 2);
+#pragma unroll
+        for (int rs = 0; rs < NU / 4; ++rs) dmma(c0, c1, ja[rs * 4 * LDJ], jb[rs * 4 * LDJ]);
+        double* Hp = HA + (ti * 8 + (lane >> 2)) * KP + tj * 8 + 2 * (lane & 3);
+        Hp[0] = fma(rho, c0, Hp[0]);
+        Hp[1] = fma(rho, c1, Hp[1]);
+      }
+      __syncwarp();
+      for (int pi = lane; pi < kx * kx; pi += 32) {
+        const int a = pi / kx, b = pi % kx;
+        if (a <= b) HA[(ku + a) * KP + ku + b] += rho * S[SH::DNP + a] * S[SH::DNP + b];
+      }
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int j = lane + 32 * half;
+        if (j < K) {
+          double v = 0.0;
+#pragma unroll
+          for (int i = 0; i < NU; ++i) v = fma(Jt[i * LDJ + j], S[SH::RT + i], v);
+          if (j >= ku) v = fma(S[SH::DNP + j - ku], S[SH::MN], v);
+          if (half == 0) gacc0 = fma(rho, v, gacc0); else gacc1 = fma(rho, v, gacc1);
+        }
+      }
+      if (lane == 0) {
+        double r2 = S[SH::MN] * S[SH::MN];
+#pragma unroll
+        for (int i = 0; i < NU; ++i) r2 = fma(S[SH::RT + i], S[SH::RT + i], r2);
+        jacc = fma(rho, r2, jacc);
+      }
+    } else {
+      const int extra = r.mode == MODE_CONTRIB_LPROWS ? 1 : 0;
+      const int nk = r.mode == MODE_CONTRIB_SPLIT ? 2 * K : K + extra;
+      for (int k2 = lane; k2 < nk; k2 += 32) {
+        double v = 0.0;
+        if (r.mode == MODE_CONTRIB_SPLIT) {
+          int kk, part;
+          if (k2 < 2 * ku) { kk = k2 % ku; part = k2 / ku; }
+          else { kk = ku + (k2 - 2 * ku) % kx; part = (k2 - 2 * ku) / kx; }
+          const double* Rp = S + (part == 0 ? SH::RV : SH::RF);
+#pragma unroll
+          for (int i = 0; i < NU; ++i) v = fma(Jt[i * LDJ + kk], Rp[i], v);
+          if (kk >= ku && part == 0) v = fma(S[SH::DNP + kk - ku], S[SH::MN], v);
+          r.out[((size_t)p * r.ne + e) * nk + k2] = v;
+        } else if (k2 < K) {
+#pragma unroll
+          for (int i = 0; i < NU; ++i) v = fma(Jt[i * LDJ + k2], S[SH::RT + i], v);
+          if (k2 >= ku) v = fma(S[SH::DNP + k2 - ku], S[SH::MN], v);
+          if (r.mode == MODE_CONTRIB) r.out[((size_t)p * r.ne + e) * K + k2] = v;
+          else r.out[((size_t)p * (K + 1) + k2) * r.ne + e] = v;
+        } else {
+          double r2 = S[SH::MN] * S[SH::MN];
+#pragma unroll
+          for (int i = 0; i < NU; ++i) r2 = fma(S[SH::RT + i], S[SH::RT + i], r2);
+          r.out[((size_t)p * (K + 1) + K) * r.ne + e] = 0.5 * r2;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (r.mode != MODE_DERIVS) return;
+  if (lane < K) GW[lane] = gacc0;
+  if (lane + 32 < K) GW[lane + 32] = gacc1;
+  if (lane == 0) GW[K] = jacc;
+  __syncthreads();
+  const int PSZ = 1 + K + KP * KP;
+  double* dst = r.part + ((size_t)p * gridDim.x + blockIdx.x) * PSZ;
+  for (int i = threadIdx.x; i < PSZ; i += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < nwarps; ++w) {
+      const double* Sw = smem + (size_t)w * r.gx_warp_stride;
+      const double* Hw = Sw + r.gx_warp_stride - 4 - 48 - KP * KP;
+      const double* Gw = Hw + KP * KP;
+      v += i == 0 ? Gw[K] : (i <= K ? Gw[i - 1] : Hw[i - 1 - K]);
+    }
+    dst[i] = v;
+  }
+}
+
+}  // namespace strom

@@ -116,6 +116,22 @@ __device__ __forceinline__ double distortion_eta(const Geo& o, double wsum, doub
   return wsum * o.detr * ratio * ratio;
 }
 
+// d N / d x_d for one local coordinate direction d = 2*vertex + component
+__device__ __forceinline__ double distortion_grad_dir(const Geo& o, double wsum, double eps, double kappa, int d) {
+  double ratio, den;
+  distortion_eta(o, wsum, eps, &ratio, &den);
+  const int gv = d >> 1, ic = d & 1;
+  const double c0 = (gv == 1) - (gv == 0), c1 = (gv == 2) - (gv == 0);
+  const double dJ00 = ic == 0 ? c0 : 0.0, dJ01 = ic == 0 ? c1 : 0.0, dJ10 = ic == 1 ? c0 : 0.0, dJ11 = ic == 1 ? c1 : 0.0;
+  const double dG00 = dJ00 * o.invr[0][0] + dJ01 * o.invr[1][0], dG01 = dJ00 * o.invr[0][1] + dJ01 * o.invr[1][1];
+  const double dG10 = dJ10 * o.invr[0][0] + dJ11 * o.invr[1][0], dG11 = dJ10 * o.invr[0][1] + dJ11 * o.invr[1][1];
+  const double dg = dG00 * o.G[1][1] + o.G[0][0] * dG11 - dG01 * o.G[1][0] - o.G[0][1] * dG10;
+  const double dfro = 2.0 * (o.G[0][0] * dG00 + o.G[0][1] * dG01 + o.G[1][0] * dG10 + o.G[1][1] * dG11);
+  const double dden = o.g >= eps ? dg : 0.0;
+  const double dratio = (dfro - ratio * dden) / den;
+  return kappa * wsum * o.detr * 2.0 * ratio * dratio;
+}
+
 __device__ __forceinline__ void distortion_grad(const Geo& o, double wsum, double eps, double kappa, double* dN) {
   double ratio, den;
   distortion_eta(o, wsum, eps, &ratio, &den);

@@ -2,6 +2,7 @@
 #pragma once
 #include "handle.h"
 #include "derivs_warp.cuh"
+#include "derivs_mma.cuh"
 
 namespace strom_host {
 template <int NB, int NQ, int NS, int NF>
@@ -50,6 +51,46 @@ static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WS
   int gx = std::max(1, std::min(maxb, (target + a.P - 1) / a.P));
   r.gx = gx;
   r.ntiles = ngroups;
+  const int PSZ = 1 + r.K + r.KP * r.KP;
+  if (a.mode == MODE_DERIVS) {
+    if (ensure_part(h, (size_t)a.P * gx * PSZ)) return -2;
+    r.part = h->part;
+  }
+  prof_mark(h, a.stream, 0);
+  kern<<<dim3(gx, a.P), nwarps * 32, smem, a.stream>>>(prm);
+  prof_mark(h, a.stream, 1);
+  CK(cudaGetLastError());
+  if (a.mode == MODE_DERIVS) {
+    const int OSZ = 1 + r.K + r.K * r.K;
+    finalize_derivs_kernel<<<dim3((OSZ + 127) / 128, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
+template <class LAW, int NQ>
+static int launch_mma(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& prm, int nunits) {
+  using SH = MShape<NQ>;
+  Run& r = prm.r;
+  r.LDJ = r.KP + 4;  // == 4 mod 8 doubles: conflict-free half-warp fragment loads
+  r.U = 1;
+  r.unit_stride = 0;
+  r.gx_warp_stride = SH::warp_stride(r.LDJ, r.KP);
+  const int smem_cap = 227 * 1024;
+  const size_t warp_bytes = (size_t)r.gx_warp_stride * sizeof(double);
+  int nwarps = std::min<int>(MTHREADS / 32, (int)(smem_cap / warp_bytes));
+  if (nwarps < 1) return fail(-1, "element does not fit in shared memory");
+  const size_t smem = nwarps * warp_bytes;
+  auto kern = derivs_mma_kernel<LAW, NQ>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nwarps * 32, smem));
+  per_sm = std::max(per_sm, 1);
+  const int target = h->num_sms * per_sm;
+  const int maxb = std::max(1, (nunits + nwarps - 1) / nwarps);
+  int gx = std::max(1, std::min(maxb, (target + a.P - 1) / a.P));
+  r.gx = gx;
+  r.ntiles = nunits;
   const int PSZ = 1 + r.K + r.KP * r.KP;
   if (a.mode == MODE_DERIVS) {
     if (ensure_part(h, (size_t)a.P * gx * PSZ)) return -2;
@@ -116,6 +157,9 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
   }
   if (h->ku < 1) return fail(-1, "derivative modes need k_u >= 1");
   if (h->ku > 32) return fail(-1, "derivative modes need k_u <= 32");
+  if constexpr (LAW::M == 4 && NB == 6 && NS == 4) {
+    if (!h->force_warp_kernel) return launch_mma<LAW, NQ>(h, a, prm, nunits);
+  }
   if (h->ku <= 16) return launch_warp<LAW, NB, NQ, NS, 16>(h, a, prm, nunits);
   return launch_warp<LAW, NB, NQ, NS, 32>(h, a, prm, nunits);
 }

@@ -80,6 +80,7 @@ struct strom_handle {
   strom::LmWork lm;
   // benchmark probe
   int lm_rounds = 0;
+  int force_warp_kernel = 0;  // testing / A-B: use the tangent-lane kernel instead of the DMMA one
   bool prof = false;
   std::vector<cudaEvent_t> ev;
   int nprof = 0;

@@ -190,6 +190,58 @@ struct Euler {
     A[2][0] = gk * n[1] - vy * qn;     A[2][1] = vy * n[0] - gm * vx * n[1];       A[2][2] = qn + vy * n[1] - gm * vy * n[1];  A[2][3] = gm * n[1];
     A[3][0] = qn * (gk - H);           A[3][1] = H * n[0] - gm * vx * qn;          A[3][2] = H * n[1] - gm * vy * qn;          A[3][3] = g * qn;
   }
+  // fused face side: flux components f, A(nu) = d(f.nu)/du, ws(u, nh) and its gradients
+  __device__ static double face_side(const double* u, const double* nu, const double* nh, double (*f)[2],
+                                     double (*A)[4], double* dwdu, double* dwdn, const LawArgs& a) {
+    const double g = a.p[0], gm = g - 1.0;
+    const double r = u[0], ir = 1.0 / r, vx = u[1] * ir, vy = u[2] * ir;
+    const double p = gm * (u[3] - 0.5 * (u[1] * vx + u[2] * vy));
+    const double ke = 0.5 * (vx * vx + vy * vy);
+    const double Ep = u[3] + p, H = Ep * ir, gk = gm * ke;
+    f[0][0] = u[1];          f[0][1] = u[2];
+    f[1][0] = u[1] * vx + p; f[1][1] = u[1] * vy;
+    f[2][0] = u[2] * vx;     f[2][1] = u[2] * vy + p;
+    f[3][0] = Ep * vx;       f[3][1] = Ep * vy;
+    const double qn = vx * nu[0] + vy * nu[1];
+    A[0][0] = 0.0;                 A[0][1] = nu[0];                              A[0][2] = nu[1];                              A[0][3] = 0.0;
+    A[1][0] = gk * nu[0] - vx * qn; A[1][1] = qn + vx * nu[0] - gm * vx * nu[0]; A[1][2] = vx * nu[1] - gm * vy * nu[0];       A[1][3] = gm * nu[0];
+    A[2][0] = gk * nu[1] - vy * qn; A[2][1] = vy * nu[0] - gm * vx * nu[1];       A[2][2] = qn + vy * nu[1] - gm * vy * nu[1]; A[2][3] = gm * nu[1];
+    A[3][0] = qn * (gk - H);        A[3][1] = H * nu[0] - gm * vx * qn;           A[3][2] = H * nu[1] - gm * vy * qn;           A[3][3] = g * qn;
+    const double qh = vx * nh[0] + vy * nh[1];
+    const double c = sqrt(g * p / r);
+    const double sg = qh > 0.0 ? 1.0 : (qh < 0.0 ? -1.0 : 0.0);
+    const double cf = g / (2.0 * c * r);
+    dwdu[0] = sg * (-qh * ir) + cf * (gm * ke - p * ir);
+    dwdu[1] = sg * nh[0] * ir - cf * gm * vx;
+    dwdu[2] = sg * nh[1] * ir - cf * gm * vy;
+    dwdu[3] = cf * gm;
+    dwdn[0] = sg * vx;
+    dwdn[1] = sg * vy;
+    return fabs(qh) + c;
+  }
+  // fused volume point: flux components f and the two directional Jacobians A(d0), A(d1)
+  __device__ static void vol_point(const double* u, const double* d0, const double* d1, double (*f)[2],
+                                   double (*A0)[4], double (*A1)[4], const LawArgs& a) {
+    const double g = a.p[0], gm = g - 1.0;
+    const double r = u[0], ir = 1.0 / r, vx = u[1] * ir, vy = u[2] * ir;
+    const double p = gm * (u[3] - 0.5 * (u[1] * vx + u[2] * vy));
+    const double ke = 0.5 * (vx * vx + vy * vy);
+    const double Ep = u[3] + p, H = Ep * ir, gk = gm * ke;
+    f[0][0] = u[1];          f[0][1] = u[2];
+    f[1][0] = u[1] * vx + p; f[1][1] = u[1] * vy;
+    f[2][0] = u[2] * vx;     f[2][1] = u[2] * vy + p;
+    f[3][0] = Ep * vx;       f[3][1] = Ep * vy;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const double* n = t == 0 ? d0 : d1;
+      double (*A)[4] = t == 0 ? A0 : A1;
+      const double qn = vx * n[0] + vy * n[1];
+      A[0][0] = 0.0;                A[0][1] = n[0];                            A[0][2] = n[1];                            A[0][3] = 0.0;
+      A[1][0] = gk * n[0] - vx * qn; A[1][1] = qn + vx * n[0] - gm * vx * n[0]; A[1][2] = vx * n[1] - gm * vy * n[0];     A[1][3] = gm * n[0];
+      A[2][0] = gk * n[1] - vy * qn; A[2][1] = vy * n[0] - gm * vx * n[1];      A[2][2] = qn + vy * n[1] - gm * vy * n[1]; A[2][3] = gm * n[1];
+      A[3][0] = qn * (gk - H);       A[3][1] = H * n[0] - gm * vx * qn;         A[3][2] = H * n[1] - gm * vy * qn;         A[3][3] = g * qn;
+    }
+  }
   // ws = |v.nh| + c and its gradients wrt u and nh (sign(0) = 0)
   __device__ static double wavespeed_grad(const double* u, const double* nh, double* dwdu, double* dwdn, const LawArgs& a) {
     const double g = a.p[0], gm = g - 1.0;
@@ -241,6 +293,14 @@ struct PointOps;
 
 template <class LAW>
 struct PointOps<LAW, true> {
+  __device__ static double face_side(const double* u, const double* nu, const double* nh, double (*f)[2],
+                                     double (*Am)[LAW::M], double* dwdu, double* dwdn, const LawArgs& a) {
+    return LAW::face_side(u, nu, nh, f, Am, dwdu, dwdn, a);
+  }
+  __device__ static void vol_point(const double* u, const double* d0, const double* d1, double (*f)[2],
+                                   double (*A0)[LAW::M], double (*A1)[LAW::M], const LawArgs& a) {
+    LAW::vol_point(u, d0, d1, f, A0, A1, a);
+  }
   __device__ static void flux_dir(const double* u, const double* n, double* fn, double (*Am)[LAW::M], const LawArgs& a) {
     LAW::flux_dir(u, n, fn, Am, a);
   }
@@ -252,6 +312,10 @@ struct PointOps<LAW, true> {
 template <class LAW>
 struct PointOps<LAW, false> {
   static constexpr int M = LAW::M;
+  __device__ static double face_side(const double* u, const double* nu, const double* nh, double (*f)[2],
+                                     double (*Am)[M], double* dwdu, double* dwdn, const LawArgs& a);
+  __device__ static void vol_point(const double* u, const double* d0, const double* d1, double (*f)[2],
+                                   double (*A0)[M], double (*A1)[M], const LawArgs& a);
   __device__ static void flux_dir(const double* u, const double* n, double* fn, double (*Am)[M], const LawArgs& a) {
     Dn<M> ud[M];
 #pragma unroll
@@ -279,5 +343,23 @@ struct PointOps<LAW, false> {
     return w.v;
   }
 };
+
+template <class LAW>
+__device__ double PointOps<LAW, false>::face_side(const double* u, const double* nu, const double* nh, double (*f)[2],
+                                                  double (*Am)[M], double* dwdu, double* dwdn, const LawArgs& a) {
+  double fn[M];
+  flux_dir(u, nu, fn, Am, a);
+  LAW::flux(u, f, a);
+  return wavespeed_grad(u, nh, dwdu, dwdn, a);
+}
+
+template <class LAW>
+__device__ void PointOps<LAW, false>::vol_point(const double* u, const double* d0, const double* d1, double (*f)[2],
+                                                double (*A0)[M], double (*A1)[M], const LawArgs& a) {
+  double fn[M];
+  LAW::flux(u, f, a);
+  flux_dir(u, d0, fn, A0, a);
+  flux_dir(u, d1, fn, A1, a);
+}
 
 }  // namespace strom

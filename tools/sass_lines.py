@@ -17,8 +17,12 @@ rep, kname = sys.argv[1], sys.argv[2]
 so = sys.argv[3] if len(sys.argv) > 3 else "paper_2305_15661_b200/_strom_b200.so"
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+dis = ""
+for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
+    d = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+    if kname in d:
+        dis = d
+        break
 addr2line, cur_line, infun = {}, None, False
 for ln in dis.splitlines():
     if ln.startswith("//---------------------"):

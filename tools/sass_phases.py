@@ -13,8 +13,12 @@ phases = [(int(a.split(":")[0]), int(a.split(":")[1]), a.split(":")[2]) for a in
 so = os.path.abspath("paper_2305_15661_b200/_strom_b200.so")
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=tmp, capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+dis = ""
+for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
+    d = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+    if kname in d:
+        dis = d
+        break
 a2l, a2op, cur, infun = {}, {}, None, False
 for ln in dis.splitlines():
     if ln.startswith("//---------------------"):
