@@ -4,7 +4,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "_strom_b200.so")
+SO_PATH = os.environ.get("STROM_SO") or os.path.join(HERE, "_strom_b200.so")
 
 OBJECTIVE, DERIVS, CONTRIB, CONTRIB_SPLIT, RESIDUAL, RESNORM2, CONTRIB_LPROWS = range(7)
 

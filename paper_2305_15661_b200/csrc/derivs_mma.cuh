@@ -45,7 +45,7 @@ struct MShape {
   // region A (offsets from RA), by phase:
   //   P/L : BQ [q][c][kk][c'] at 0           -> L [NU][LDL] at 0 once the L GEMM has read BQ
   //   P/F : CF [fs][side][c][c'] at LA       (read by the face blocks)
-  //   F/J : LOUT [3][12][LDO] at LO          (read by the projection)
+  //   F/J : one face's Lout [12][LDO] at LO  (projected right away)
   //   X/G : DRX [NU][LDX] at LO (LOUT dead), Jt [NU][LDJ] at 0 (L, CF dead)
   static constexpr int LDL = 28, LDO = 20;
   static constexpr int BQ = 0, LL = 0;
@@ -53,7 +53,7 @@ struct MShape {
   static constexpr int CF = LA;
   static constexpr int LO = LA + 32 * NFSP;
   static constexpr int DRX = LO;
-  static constexpr int RAEND = LO + 3 * 12 * LDO;
+  static constexpr int RAEND = LO + (12 * LDO > NU * LDX ? 12 * LDO : NU * LDX);
   __host__ __device__ static int warp_stride(int LDJ, int KP) {
     int ra = RAEND > NU * LDJ ? RAEND : NU * LDJ;
     int s = RA + ra + KP * KP + 48;
@@ -68,7 +68,7 @@ __device__ __forceinline__ int face_local(int f, int n) {
 }
 
 template <class LAW, int NQ>
-__global__ void __launch_bounds__(MTHREADS) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
+__global__ void __maxnreg__(200) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
   using SH = MShape<NQ>;
   constexpr int M = 4, NB = 6, NU = 24, NF = 3, NS = 4, NFS = 12, PD = 2;
   constexpr int NQP = SH::NQP, NFSP = SH::NFSP, LDL = SH::LDL, LDO = SH::LDO, LDX = SH::LDX;
@@ -391,36 +391,69 @@ __global__ void __launch_bounds__(MTHREADS) derivs_mma_kernel(const __grid_const
           }
     }
     __syncwarp();
-    // face blocks: lanes 0-15 add the in-side block into L, lanes 16-31 form Lout
-#pragma unroll
-    for (int f = 0; f < 3; ++f) {
-      const int c = (lane & 15) >> 2, cp = lane & 3, side = lane >> 4;
-      double cs[NS];
-#pragma unroll
-      for (int s = 0; s < NS; ++s) cs[s] = RA[SH::CF + ((side * M + c) * M + cp) * NFSP + f * NS + s];
-#pragma unroll
-      for (int j = 0; j < NF; ++j)
-#pragma unroll
-        for (int jp = 0; jp < NF; ++jp) {
-          double v = 0.0;
-#pragma unroll
-          for (int s = 0; s < NS; ++s) v = fma(T.trace[0][s][j] * T.trace[0][s][jp], cs[s], v);
-          if (side == 0) {
-            RA[SH::LL + (fnode_of(PD, f, j) * M + c) * LDL + fnode_of(PD, f, jp) * M + cp] += v;
-          } else {
-            RA[SH::LO + (f * 12 + j * M + c) * LDO + jp * M + cp] = v;
-          }
-        }
-      __syncwarp();
-    }
-    // ---- J: projection J_U = L Phi_e + sum_f E_f Lout_f Phi_nf on DMMA -----------------
-    const double* L = RA + SH::LL;
-    const double* Lo = RA + SH::LO;
+    // face blocks, one face at a time: lanes 0-15 add the in-side block into L, lanes
+    // 16-31 form Lout_f in a one-face buffer, then the warp projects it on the
+    // neighbor's face-node basis rows straight into the J accumulators
     double ju[4][3][2];  // up to 4 n-tiles (k_u <= 32)
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int mt = 0; mt < 3; ++mt) ju[nt][mt][0] = ju[nt][mt][1] = 0.0;
+    const double* L = RA + SH::LL;
+    double* Lo = RA + SH::LO;
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      {
+        const int c = (lane & 15) >> 2, cp = lane & 3, side = lane >> 4;
+        double cs[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) cs[s] = RA[SH::CF + ((side * M + c) * M + cp) * NFSP + f * NS + s];
+#pragma unroll
+        for (int j = 0; j < NF; ++j)
+#pragma unroll
+          for (int jp = 0; jp < NF; ++jp) {
+            double v = 0.0;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) v = fma(T.trace[0][s][j] * T.trace[0][s][jp], cs[s], v);
+            if (side == 0) {
+              RA[SH::LL + (fnode_of(PD, f, j) * M + c) * LDL + fnode_of(PD, f, jp) * M + cp] += v;
+            } else {
+              Lo[(j * M + c) * LDO + jp * M + cp] = v;
+            }
+          }
+      }
+      __syncwarp();
+      if ((fin[f] >> 3) == 0) {
+        const int nf = fin[f] & 3;
+        const bool flip = (fin[f] >> 2) & 1;
+        const double* phn = r.phi + (size_t)nbr[f] * NU * ku;
+#pragma unroll
+        for (int ks = 0; ks < 3; ++ks) {  // k = (j', c') = 4 ks + lane&3 -> j' = ks
+          // neighbor face node j' (flip: the two vertex nodes swap, trace(1-s) = trace(s) with swapped vertices)
+          const int jn = flip ? (ks == 0 ? 1 : (ks == 1 ? 0 : 2)) : ks;
+          const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
+          const int brow = node * M + (lane & 3);
+          double af[3];
+#pragma unroll
+          for (int mt = 0; mt < 3; ++mt) {
+            const int row = mt * 8 + (lane >> 2), n = row >> 2, c = row & 3;
+            const int j = face_local(f, n);
+            af[mt] = j >= 0 ? Lo[(j * M + c) * LDO + 4 * ks + (lane & 3)] : 0.0;
+          }
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            if (nt < ntu) {
+              const int col = nt * 8 + (lane >> 2);
+              const double b = pref ? pfn[f][ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phn + (size_t)brow * ku + col) : 0.0);
+#pragma unroll
+              for (int mt = 0; mt < 3; ++mt) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
+            }
+          }
+        }
+      }
+      __syncwarp();  // Lout_f consumed before the next face overwrites it
+    }
+    // ---- J: own-state projection J_U += L Phi_e on DMMA ----------------------------------
     {
       const double* phe = r.phi + (size_t)e * NU * ku;
 #pragma unroll
@@ -436,36 +469,6 @@ __global__ void __launch_bounds__(MTHREADS) derivs_mma_kernel(const __grid_const
             const double b = pref ? pfe[ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phe + (size_t)brow * ku + col) : 0.0);
 #pragma unroll
             for (int mt = 0; mt < 3; ++mt) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
-          }
-        }
-      }
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        if ((fin[f] >> 3) != 0) continue;
-        const int nf = fin[f] & 3;
-        const bool flip = (fin[f] >> 2) & 1;
-        const double* phn = r.phi + (size_t)nbr[f] * NU * ku;
-#pragma unroll
-        for (int ks = 0; ks < 3; ++ks) {  // k = (j', c') = 4 ks + lane&3 -> j' = ks
-          // neighbor face node j' (flip: the two vertex nodes swap, trace(1-s) = trace(s) with swapped vertices)
-          const int jn = flip ? (ks == 0 ? 1 : (ks == 1 ? 0 : 2)) : ks;
-          const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
-          const int brow = node * M + (lane & 3);
-          double af[3];
-#pragma unroll
-          for (int mt = 0; mt < 3; ++mt) {
-            const int row = mt * 8 + (lane >> 2), n = row >> 2, c = row & 3;
-            const int j = face_local(f, n);
-            af[mt] = j >= 0 ? Lo[(f * 12 + j * M + c) * LDO + 4 * ks + (lane & 3)] : 0.0;
-          }
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt) {
-            if (nt < ntu) {
-              const int col = nt * 8 + (lane >> 2);
-              const double b = pref ? pfn[f][ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phn + (size_t)brow * ku + col) : 0.0);
-#pragma unroll
-              for (int mt = 0; mt < 3; ++mt) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
-            }
           }
         }
       }

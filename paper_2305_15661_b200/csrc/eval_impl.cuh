@@ -3,6 +3,8 @@
 #include "handle.h"
 #include "derivs_warp.cuh"
 #include "derivs_mma.cuh"
+#include <cstdlib>
+#include <cstdio>
 
 namespace strom_host {
 template <int NB, int NQ, int NS, int NF>
@@ -78,7 +80,8 @@ static int launch_mma(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& p
   r.gx_warp_stride = SH::warp_stride(r.LDJ, r.KP);
   const int smem_cap = 227 * 1024;
   const size_t warp_bytes = (size_t)r.gx_warp_stride * sizeof(double);
-  int nwarps = std::min<int>(MTHREADS / 32, (int)(smem_cap / warp_bytes));
+  int nwarps = std::min<int>(2, (int)(smem_cap / warp_bytes));  // 2-warp CTAs (measured fastest)
+  if (const char* ev = getenv("STROM_MMA_WARPS")) nwarps = std::max(1, std::min(nwarps, atoi(ev)));
   if (nwarps < 1) return fail(-1, "element does not fit in shared memory");
   const size_t smem = nwarps * warp_bytes;
   auto kern = derivs_mma_kernel<LAW, NQ>;
@@ -91,6 +94,9 @@ static int launch_mma(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& p
   int gx = std::max(1, std::min(maxb, (target + a.P - 1) / a.P));
   r.gx = gx;
   r.ntiles = nunits;
+  if (getenv("STROM_DEBUG"))
+    fprintf(stderr, "[strom] mma kernel: %d warps/CTA, %zu B smem/CTA, %d CTAs/SM, grid %d x %d\n", nwarps, smem, per_sm,
+            gx, a.P);
   const int PSZ = 1 + r.K + r.KP * r.KP;
   if (a.mode == MODE_DERIVS) {
     if (ensure_part(h, (size_t)a.P * gx * PSZ)) return -2;

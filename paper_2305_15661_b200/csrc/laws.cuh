@@ -242,6 +242,42 @@ struct Euler {
       A[3][0] = qn * (gk - H);       A[3][1] = H * n[0] - gm * vx * qn;         A[3][2] = H * n[1] - gm * vy * qn;         A[3][3] = g * qn;
     }
   }
+  // everything a quadrature point needs, one code path for volume and face points:
+  // flux components, A(d0), A(d1), ws(u, nh) with its gradients
+  __device__ static double point_full(const double* u, const double* d0, const double* d1, const double* nh,
+                                      double (*f)[2], double (*A0)[4], double (*A1)[4], double* dwdu, double* dwdn,
+                                      const LawArgs& a) {
+    const double g = a.p[0], gm = g - 1.0;
+    const double r = u[0], ir = 1.0 / r, vx = u[1] * ir, vy = u[2] * ir;
+    const double p = gm * (u[3] - 0.5 * (u[1] * vx + u[2] * vy));
+    const double ke = 0.5 * (vx * vx + vy * vy);
+    const double Ep = u[3] + p, H = Ep * ir, gk = gm * ke;
+    f[0][0] = u[1];          f[0][1] = u[2];
+    f[1][0] = u[1] * vx + p; f[1][1] = u[1] * vy;
+    f[2][0] = u[2] * vx;     f[2][1] = u[2] * vy + p;
+    f[3][0] = Ep * vx;       f[3][1] = Ep * vy;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const double* n = t == 0 ? d0 : d1;
+      double (*A)[4] = t == 0 ? A0 : A1;
+      const double qn = vx * n[0] + vy * n[1];
+      A[0][0] = 0.0;                A[0][1] = n[0];                            A[0][2] = n[1];                            A[0][3] = 0.0;
+      A[1][0] = gk * n[0] - vx * qn; A[1][1] = qn + vx * n[0] - gm * vx * n[0]; A[1][2] = vx * n[1] - gm * vy * n[0];     A[1][3] = gm * n[0];
+      A[2][0] = gk * n[1] - vy * qn; A[2][1] = vy * n[0] - gm * vx * n[1];      A[2][2] = qn + vy * n[1] - gm * vy * n[1]; A[2][3] = gm * n[1];
+      A[3][0] = qn * (gk - H);       A[3][1] = H * n[0] - gm * vx * qn;         A[3][2] = H * n[1] - gm * vy * qn;         A[3][3] = g * qn;
+    }
+    const double qh = vx * nh[0] + vy * nh[1];
+    const double c = sqrt(g * p / r);
+    const double sg = qh > 0.0 ? 1.0 : (qh < 0.0 ? -1.0 : 0.0);
+    const double cf = g / (2.0 * c * r);
+    dwdu[0] = sg * (-qh * ir) + cf * (gm * ke - p * ir);
+    dwdu[1] = sg * nh[0] * ir - cf * gm * vx;
+    dwdu[2] = sg * nh[1] * ir - cf * gm * vy;
+    dwdu[3] = cf * gm;
+    dwdn[0] = sg * vx;
+    dwdn[1] = sg * vy;
+    return fabs(qh) + c;
+  }
   // ws = |v.nh| + c and its gradients wrt u and nh (sign(0) = 0)
   __device__ static double wavespeed_grad(const double* u, const double* nh, double* dwdu, double* dwdn, const LawArgs& a) {
     const double g = a.p[0], gm = g - 1.0;
