@@ -106,12 +106,24 @@ def freestream_field(rng, ne, nb, mach, gamma=1.4, jitter=0.05, per_component=Fa
 
 
 # -- config 1 -----------------------------------------------------------------------
-def strip_case(ncell=64, ku=4, kx=2, n_active=10, P=8, seed=1, quad_order=None):
+def strip_case(ncell=64, ku=4, kx=2, n_active=10, P=8, seed=1, quad_order=None, boundary_in_sample=True):
+    """Config 1.  The EQP sample always contains the two elements that touch the
+    prescribed left / right boundaries (``boundary_in_sample``): without them the
+    weighted residual at U = 0 vanishes identically and every solve is trivial."""
     mesh, maps = build_box_mesh(((0.0, 0.0), (1.0, 1.0 / ncell)), ncell, 1, degree_sol=2, n_comp=1)
     rng = np.random.default_rng(seed)
     phi = orthonormal(rng, maps.n_global_state, ku)
     psi = orthonormal(rng, maps.n_global_coord, kx)
     rho = eqp_weights(rng, mesh.num_elements, n_active, mesh.num_elements / n_active)
+    if boundary_in_sample:
+        _, _, _, tag = mesh.neighbor_tables()
+        ends = [int(np.flatnonzero(np.any(tag == mesh.boundary_tags[t], axis=1))[0]) for t in ("left", "right")]
+        for e in ends:
+            if rho[e] == 0.0:
+                drop = np.flatnonzero(rho > 0.0)
+                drop = [d for d in drop if d not in ends]
+                rho[rng.choice(drop)] = 0.0
+                rho[e] = rng.uniform(0.5, 2.0) * mesh.num_elements / n_active
     mus = rng.uniform(1.0, 3.0, size=(P, 1))
     return Case("cfg1-strip", L.burgers_strip(), mesh, maps, quad_order, phi, psi, mesh.nodes.ravel().copy(),
                 mus, np.zeros((P, ku)), np.zeros((P, kx)), rho)
