@@ -78,6 +78,7 @@ __global__ void __maxnreg__(200) derivs_mma_kernel(const __grid_constant__ Param
   extern __shared__ __align__(16) double smem[];
   __shared__ double s_w[KMAX], s_tau[KMAX];
   __shared__ double s_dphi[NQ * NB * 2];
+  __shared__ int s_tile[15];  // upper 8x8 tiles of the Gram (KP <= 40): (ti << 4) | tj
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int p = blockIdx.y;
   if (r.mask && !r.mask[p]) return;
@@ -91,6 +92,11 @@ __global__ void __maxnreg__(200) derivs_mma_kernel(const __grid_constant__ Param
   for (int i = threadIdx.x; i < kx; i += blockDim.x) s_tau[i] = r.tau[(size_t)p * kx + i];
   for (int i = threadIdx.x; i < NQ * NB * 2; i += blockDim.x) s_dphi[i] = (&T.dphi[0][0][0])[i];
   for (int i = lane; i < KP * KP; i += 32) HA[i] = 0.0;
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int ti = 0; ti < KP / 8; ++ti)
+      for (int tj = ti; tj < KP / 8; ++tj) s_tile[t++] = (ti << 4) | tj;
+  }
   LawArgs la;
 #pragma unroll
   for (int i = 0; i < 8; ++i) la.p[i] = r.lawp[i];
@@ -414,7 +420,7 @@ __global__ void __maxnreg__(200) derivs_mma_kernel(const __grid_constant__ Param
           for (int jp = 0; jp < NF; ++jp) {
             double v = 0.0;
 #pragma unroll
-            for (int s = 0; s < NS; ++s) v = fma(T.trace[0][s][j] * T.trace[0][s][jp], cs[s], v);
+            for (int s = 0; s < NS; ++s) v = fma(T.t2[j][jp][s], cs[s], v);
             if (side == 0) {
               RA[SH::LL + (fnode_of(PD, f, j) * M + c) * LDL + fnode_of(PD, f, jp) * M + cp] += v;
             } else {
@@ -577,9 +583,7 @@ __global__ void __maxnreg__(200) derivs_mma_kernel(const __grid_constant__ Param
     // ---- G: Gram and gradient, or per-element contributions --------------------------------
     if (r.mode == MODE_DERIVS) {
       for (int t = 0; t < ntri; ++t) {
-        int ti = 0, rem = t;
-        while (rem >= nt8 - ti) { rem -= nt8 - ti; ++ti; }
-        const int tj = ti + rem;
+        const int ti = s_tile[t] >> 4, tj = s_tile[t] & 15;
         double c0 = 0.0, c1 = 0.0;
         const double* ja = Jt + (lane & 3) * LDJ + ti * 8 + (lane >> 2);
         const double* jb = Jt + (lane & 3) * LDJ + tj * 8 + (lane >> 2);
@@ -605,11 +609,9 @@ __global__ void __maxnreg__(200) derivs_mma_kernel(const __grid_constant__ Param
           if (half == 0) gacc0 = fma(rho, v, gacc0); else gacc1 = fma(rho, v, gacc1);
         }
       }
-      if (lane == 0) {
-        double r2 = S[SH::MN] * S[SH::MN];
-#pragma unroll
-        for (int i = 0; i < NU; ++i) r2 = fma(S[SH::RT + i], S[SH::RT + i], r2);
-        jacc = fma(rho, r2, jacc);
+      {  // per-lane objective partials, reduced across lanes once at the end of the kernel
+        const double ri = lane < NU ? S[SH::RT + lane] : (lane == NU ? S[SH::MN] : 0.0);
+        jacc = fma(rho * ri, ri, jacc);
       }
     } else {
       const int extra = r.mode == MODE_CONTRIB_LPROWS ? 1 : 0;
@@ -642,6 +644,8 @@ __global__ void __maxnreg__(200) derivs_mma_kernel(const __grid_constant__ Param
     __syncwarp();
   }
   if (r.mode != MODE_DERIVS) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) jacc += __shfl_xor_sync(0xffffffffu, jacc, o);
   if (lane < K) GW[lane] = gacc0;
   if (lane + 32 < K) GW[lane + 32] = gacc1;
   if (lane == 0) GW[K] = jacc;

@@ -25,6 +25,7 @@ struct Tabs {
   double bary[NQ][3];
   double trace[3][NS][NF];
   double ws[NS];
+  double t2[NF][NF][NS];  // trace[0][s][j] * trace[0][s][j'] (face-block products)
   double wsum;
   int fnode[3][NF];
 };

@@ -22,6 +22,9 @@ static void fill_tabs(const strom_handle* h, Tabs<NB, NQ, NS, NF>& t) {
     for (int s = 0; s < NS; ++s)
       for (int j = 0; j < NF; ++j) t.trace[f][s][j] = h->trace[(f * NS + s) * NF + j];
   for (int s = 0; s < NS; ++s) t.ws[s] = h->ws[s];
+  for (int j = 0; j < NF; ++j)
+    for (int jp = 0; jp < NF; ++jp)
+      for (int s = 0; s < NS; ++s) t.t2[j][jp][s] = t.trace[0][s][j] * t.trace[0][s][jp];
   t.wsum = h->wsum;
   for (int f = 0; f < 3; ++f)
     for (int j = 0; j < NF; ++j) t.fnode[f][j] = fnode_of(NB == 3 ? 1 : 2, f, j);
