@@ -68,7 +68,7 @@ __device__ __forceinline__ int face_local(int f, int n) {
 }
 
 template <class LAW, int NQ>
-__global__ void __maxnreg__(200) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
+__global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
   using SH = MShape<NQ>;
   constexpr int M = 4, NB = 6, NU = 24, NF = 3, NS = 4, NFS = 12, PD = 2;
   constexpr int NQP = SH::NQP, NFSP = SH::NFSP, LDL = SH::LDL, LDO = SH::LDO, LDX = SH::LDX;
