@@ -184,13 +184,175 @@ __device__ __forceinline__ void face_normal(const double* x, int f, double* nu, 
   nh[0] = nu[0] / len; nh[1] = nu[1] / len;
 }
 
+// row . w for a basis row of length ku <= 32 with w in registers (compile-time
+// indexed, predicated), 16-byte loads of the row (broadcast when the warp shares it)
+__device__ __forceinline__ double row_dot(const double* __restrict__ row, const double* wr, int ku) {
+  double a0 = 0.0, a1 = 0.0;
+  if ((ku & 1) == 0) {
+    const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2)
+      if (2 * k2 < ku) {
+        const double2 t = __ldg(r2 + k2);
+        a0 = fma(t.x, wr[2 * k2], a0);
+        a1 = fma(t.y, wr[2 * k2 + 1], a1);
+      }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (k < ku) a0 = fma(__ldg(row + k), wr[k], a0);
+  }
+  return a0 + a1;
+}
+
 // ============================================================================
-// K2: value kernel — one thread per (element, mu)
+// K2: element residual (value path) for one (element, mu); w / tau through the
+// accessors WG(k) / TG(a) so one body serves both kernel layouts below
 // ============================================================================
+template <class LAW, int NB, int NQ, int NS, class TGet>
+__device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB, NQ, NS>::NF>& T, const Run& r,
+                                           const LawArgs& la, int e, int p, const double* wr, TGet TG,
+                                           double* R, double& Nd, bool& degenerate) {
+  using SH = Shape<LAW, NB, NQ, NS>;
+  constexpr int M = SH::M, NU = SH::NU, NF = SH::NF, PD = SH::P;
+  double x[6], X[6];
+#pragma unroll
+  for (int g = 0; g < 3; ++g) {
+    int n = r.elem_nodes[3 * e + g];
+    X[2 * g] = r.nodes[2 * n];
+    X[2 * g + 1] = r.nodes[2 * n + 1];
+#pragma unroll
+    for (int ic = 0; ic < 2; ++ic) {
+      int row = 2 * n + ic;
+      double v = r.xref[(size_t)p * r.x_stride + row];
+      const double* ps = r.psi + (size_t)row * r.kx;
+      for (int a = 0; a < r.kx; ++a) v = fma(__ldg(ps + a), TG(a), v);
+      x[2 * g + ic] = v;
+    }
+  }
+  double U[NU];
+  {
+    const double* ph = r.phi + (size_t)e * NU * r.ku;
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      const double v = r.u0 ? r.u0[(size_t)p * r.u0_stride + (size_t)e * NU + i] : 0.0;
+      U[i] = v + row_dot(ph + i * r.ku, wr, r.ku);
+    }
+  }
+  Geo o;
+  element_geo(x, X, o);
+  degenerate = o.g <= 0.0;
+#pragma unroll
+  for (int i = 0; i < NU; ++i) R[i] = 0.0;
+  // volume (dg.py:105-125)
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double uq[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      double v = 0.0;
+#pragma unroll
+      for (int n = 0; n < NB; ++n) v = fma(T.phi[q][n], U[n * M + c], v);
+      uq[c] = v;
+    }
+    double f[M][2];
+    LAW::flux(uq, f, la);
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      double F0 = T.wq[q] * (f[c][0] * o.adj[0][0] + f[c][1] * o.adj[0][1]);
+      double F1 = T.wq[q] * (f[c][0] * o.adj[1][0] + f[c][1] * o.adj[1][1]);
+#pragma unroll
+      for (int n = 0; n < NB; ++n) R[n * M + c] -= T.dphi[q][n][0] * F0 + T.dphi[q][n][1] * F1;
+    }
+    if (LAW::SRC != SRC_NONE) {
+      double pos[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) pos[i] = T.bary[q][0] * x[i] + T.bary[q][1] * x[2 + i] + T.bary[q][2] * x[4 + i];
+      double s[M];
+      LAW::source(pos, uq, s, la);
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        double sv = T.wq[q] * o.detJ * s[c];
+#pragma unroll
+        for (int n = 0; n < NB; ++n) R[n * M + c] -= T.phi[q][n] * sv;
+      }
+    }
+  }
+  // faces (dg.py:127-175)
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    double nu[2], len, nh[2];
+    face_normal(x, f, nu, len, nh);
+    const int nb = r.nbr[3 * e + f];
+    const int fi = r.finfo[3 * e + f];
+    const int bc = fi >> 3;
+    double Un[NF][M];
+    int flip = 0;
+    if (bc == 0) {
+      const int nf = fi & 3;
+      flip = (fi >> 2) & 1;
+      const double* ph = r.phi + (size_t)nb * NU * r.ku;
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        int node = j == 0 ? nf : (j == 1 ? (nf + 1) % 3 : 3 + nf * (PD - 1) + (j - 2));
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          int row = node * M + c;
+          const double v = r.u0 ? r.u0[(size_t)p * r.u0_stride + (size_t)nb * NU + row] : 0.0;
+          Un[j][c] = v + row_dot(ph + row * r.ku, wr, r.ku);
+        }
+      }
+    }
+    double ghost[M];
+    if (bc >= 2) LAW::ghost(bc - 2, la, ghost);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      double ui[M], uo[M];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < NF; ++j) v = fma(T.trace[f][s][j], U[fnode_of(PD, f, j) * M + c], v);
+        ui[c] = v;
+      }
+      if (bc == 0) {
+        const int sp = flip ? NS - 1 - s : s;
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j < NF; ++j) v = fma(T.trace[0][sp][j], Un[j][c], v);
+          uo[c] = v;
+        }
+      } else if (bc == 1) {
+#pragma unroll
+        for (int c = 0; c < M; ++c) uo[c] = ui[c];
+      } else {
+#pragma unroll
+        for (int c = 0; c < M; ++c) uo[c] = ghost[c];
+      }
+      double fi_[M][2], fo[M][2];
+      LAW::flux(ui, fi_, la);
+      LAW::flux(uo, fo, la);
+      double wi = LAW::wavespeed(ui, nh, la), wo = LAW::wavespeed(uo, nh, la);
+      double lam = wi >= wo ? wi : wo;
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        double fn = (fi_[c][0] * nu[0] + fi_[c][1] * nu[1]) + (fo[c][0] * nu[0] + fo[c][1] * nu[1]);
+        double H = T.ws[s] * (0.5 * fn - 0.5 * (lam * len) * (uo[c] - ui[c]));
+#pragma unroll
+        for (int j = 0; j < NF; ++j) R[fnode_of(PD, f, j) * M + c] = fma(T.trace[f][s][j], H, R[fnode_of(PD, f, j) * M + c]);
+      }
+    }
+  }
+  Nd = r.kappa * (distortion_eta(o, T.wsum, r.eps, nullptr, nullptr) - r.eta_ref[e]);
+}
+
+// one thread per (element, mu): grid (elements / 128, P)
 template <class LAW, int NB, int NQ, int NS>
 __global__ void __launch_bounds__(128) value_kernel(const __grid_constant__ Params<NB, NQ, NS, Shape<LAW, NB, NQ, NS>::NF> prm) {
   using SH = Shape<LAW, NB, NQ, NS>;
-  constexpr int M = SH::M, NU = SH::NU, NF = SH::NF, PD = SH::P;
+  constexpr int NU = SH::NU;
   const auto& T = prm.t;
   const Run& r = prm.r;
   const int p = blockIdx.y;
@@ -206,139 +368,13 @@ __global__ void __launch_bounds__(128) value_kernel(const __grid_constant__ Para
     for (int i = 0; i < NMU; ++i) la.mu[i] = i < r.nmu ? r.mu[p * r.nmu + i] : 0.0;
     const double* w = r.w + (size_t)p * r.ku;
     const double* tau = r.tau + (size_t)p * r.kx;
-    double x[6], X[6];
+    double wr[32];
 #pragma unroll
-    for (int g = 0; g < 3; ++g) {
-      int n = r.elem_nodes[3 * e + g];
-      X[2 * g] = r.nodes[2 * n];
-      X[2 * g + 1] = r.nodes[2 * n + 1];
-#pragma unroll
-      for (int ic = 0; ic < 2; ++ic) {
-        int row = 2 * n + ic;
-        double v = r.xref[(size_t)p * r.x_stride + row];
-        const double* ps = r.psi + (size_t)row * r.kx;
-        for (int a = 0; a < r.kx; ++a) v = fma(ps[a], tau[a], v);
-        x[2 * g + ic] = v;
-      }
-    }
-    double U[NU];
-    {
-      const double* ph = r.phi + (size_t)e * NU * r.ku;
-#pragma unroll
-      for (int i = 0; i < NU; ++i) {
-        double v = r.u0 ? r.u0[(size_t)p * r.u0_stride + (size_t)e * NU + i] : 0.0;
-        for (int k = 0; k < r.ku; ++k) v = fma(ph[i * r.ku + k], w[k], v);
-        U[i] = v;
-      }
-    }
-    Geo o;
-    element_geo(x, X, o);
-    if (o.g <= 0.0) flag_degenerate(r, p, e);
-    double R[NU];
-#pragma unroll
-    for (int i = 0; i < NU; ++i) R[i] = 0.0;
-    // volume (dg.py:105-125)
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      double uq[M];
-#pragma unroll
-      for (int c = 0; c < M; ++c) {
-        double v = 0.0;
-#pragma unroll
-        for (int n = 0; n < NB; ++n) v = fma(T.phi[q][n], U[n * M + c], v);
-        uq[c] = v;
-      }
-      double f[M][2];
-      LAW::flux(uq, f, la);
-#pragma unroll
-      for (int c = 0; c < M; ++c) {
-        double F0 = T.wq[q] * (f[c][0] * o.adj[0][0] + f[c][1] * o.adj[0][1]);
-        double F1 = T.wq[q] * (f[c][0] * o.adj[1][0] + f[c][1] * o.adj[1][1]);
-#pragma unroll
-        for (int n = 0; n < NB; ++n) R[n * M + c] -= T.dphi[q][n][0] * F0 + T.dphi[q][n][1] * F1;
-      }
-      if (LAW::SRC != SRC_NONE) {
-        double pos[2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) pos[i] = T.bary[q][0] * x[i] + T.bary[q][1] * x[2 + i] + T.bary[q][2] * x[4 + i];
-        double s[M];
-        LAW::source(pos, uq, s, la);
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-          double sv = T.wq[q] * o.detJ * s[c];
-#pragma unroll
-          for (int n = 0; n < NB; ++n) R[n * M + c] -= T.phi[q][n] * sv;
-        }
-      }
-    }
-    // faces (dg.py:127-175)
-#pragma unroll
-    for (int f = 0; f < 3; ++f) {
-      double nu[2], len, nh[2];
-      face_normal(x, f, nu, len, nh);
-      const int nb = r.nbr[3 * e + f];
-      const int fi = r.finfo[3 * e + f];
-      const int bc = fi >> 3;
-      double Un[NF][M];
-      int flip = 0;
-      if (bc == 0) {
-        const int nf = fi & 3;
-        flip = (fi >> 2) & 1;
-        const double* ph = r.phi + (size_t)nb * NU * r.ku;
-#pragma unroll
-        for (int j = 0; j < NF; ++j) {
-          int node = j == 0 ? nf : (j == 1 ? (nf + 1) % 3 : 3 + nf * (PD - 1) + (j - 2));
-#pragma unroll
-          for (int c = 0; c < M; ++c) {
-            int row = node * M + c;
-            double v = r.u0 ? r.u0[(size_t)p * r.u0_stride + (size_t)nb * NU + row] : 0.0;
-            for (int k = 0; k < r.ku; ++k) v = fma(ph[row * r.ku + k], w[k], v);
-            Un[j][c] = v;
-          }
-        }
-      }
-      double ghost[M];
-      if (bc >= 2) LAW::ghost(bc - 2, la, ghost);
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        double ui[M], uo[M];
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-          double v = 0.0;
-#pragma unroll
-          for (int j = 0; j < NF; ++j) v = fma(T.trace[f][s][j], U[fnode_of(PD, f, j) * M + c], v);
-          ui[c] = v;
-        }
-        if (bc == 0) {
-          const int sp = flip ? NS - 1 - s : s;
-#pragma unroll
-          for (int c = 0; c < M; ++c) {
-            double v = 0.0;
-#pragma unroll
-            for (int j = 0; j < NF; ++j) v = fma(T.trace[0][sp][j], Un[j][c], v);
-            uo[c] = v;
-          }
-        } else if (bc == 1) {
-#pragma unroll
-          for (int c = 0; c < M; ++c) uo[c] = ui[c];
-        } else {
-#pragma unroll
-          for (int c = 0; c < M; ++c) uo[c] = ghost[c];
-        }
-        double fi_[M][2], fo[M][2];
-        LAW::flux(ui, fi_, la);
-        LAW::flux(uo, fo, la);
-        double wi = LAW::wavespeed(ui, nh, la), wo = LAW::wavespeed(uo, nh, la);
-        double lam = wi >= wo ? wi : wo;
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-          double fn = (fi_[c][0] * nu[0] + fi_[c][1] * nu[1]) + (fo[c][0] * nu[0] + fo[c][1] * nu[1]);
-          double H = T.ws[s] * (0.5 * fn - 0.5 * (lam * len) * (uo[c] - ui[c]));
-#pragma unroll
-          for (int j = 0; j < NF; ++j) R[fnode_of(PD, f, j) * M + c] = fma(T.trace[f][s][j], H, R[fnode_of(PD, f, j) * M + c]);
-        }
-      }
-    }
+    for (int k = 0; k < 32; ++k) wr[k] = k < r.ku ? __ldg(w + k) : 0.0;
+    double R[NU], N;
+    bool deg;
+    value_unit<LAW, NB, NQ, NS>(T, r, la, e, p, wr, [&](int a) { return __ldg(tau + a); }, R, N, deg);
+    if (deg) flag_degenerate(r, p, e);
     if (r.mode == MODE_RESIDUAL) {
       double* o_ = r.out + ((size_t)p * r.ne + e) * NU;
 #pragma unroll
@@ -347,12 +383,7 @@ __global__ void __launch_bounds__(128) value_kernel(const __grid_constant__ Para
       double r2 = 0.0;
 #pragma unroll
       for (int i = 0; i < NU; ++i) r2 = fma(R[i], R[i], r2);
-      if (r.mode == MODE_OBJECTIVE) {
-        double N = r.kappa * (distortion_eta(o, T.wsum, r.eps, nullptr, nullptr) - r.eta_ref[e]);
-        contrib = 0.5 * rho * (r2 + N * N);
-      } else {
-        contrib = r2;
-      }
+      contrib = r.mode == MODE_OBJECTIVE ? 0.5 * rho * (r2 + N * N) : r2;
     }
   }
   if (r.mode != MODE_RESIDUAL) {
@@ -366,6 +397,62 @@ __global__ void __launch_bounds__(128) value_kernel(const __grid_constant__ Para
     }
     if (threadIdx.x == 0) r.part[(size_t)p * gridDim.x + blockIdx.x] = red[0];
   }
+}
+
+// one warp per element, lane = parameter point (32 mu per warp): every basis row is a
+// broadcast load shared by the 32 mu; grid (element chunks, ceil(P / 32)); per-mu
+// partials per block (fixed-order sums)
+template <class LAW, int NB, int NQ, int NS>
+__global__ void __launch_bounds__(128) value_mu_kernel(const __grid_constant__ Params<NB, NQ, NS, Shape<LAW, NB, NQ, NS>::NF> prm) {
+  using SH = Shape<LAW, NB, NQ, NS>;
+  constexpr int NU = SH::NU;
+  const auto& T = prm.t;
+  const Run& r = prm.r;
+  __shared__ double Ws[KMAX][32], Ts[KXMAX][32], red[4][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p = blockIdx.y * 32 + lane;
+  const bool pv = p < r.P && (!r.mask || r.mask[p]);
+  for (int t = threadIdx.x; t < KMAX * 32; t += blockDim.x) {
+    const int k = t / 32, l = t % 32, pp = blockIdx.y * 32 + l;
+    Ws[k][l] = (k < r.ku && pp < r.P) ? r.w[(size_t)pp * r.ku + k] : 0.0;
+  }
+  for (int t = threadIdx.x; t < KXMAX * 32; t += blockDim.x) {
+    const int a = t / 32, l = t % 32, pp = blockIdx.y * 32 + l;
+    Ts[a][l] = (a < r.kx && pp < r.P) ? r.tau[(size_t)pp * r.kx + a] : 0.0;
+  }
+  __syncthreads();
+  LawArgs la;
+  for (int i = 0; i < 8; ++i) la.p[i] = r.lawp[i];
+  for (int i = 0; i < NMU; ++i) la.mu[i] = (i < r.nmu && p < r.P) ? r.mu[p * r.nmu + i] : (i < r.nmu ? r.mu[i] : 0.0);
+  const int pp = pv ? p : blockIdx.y * 32;  // idle lanes shadow a valid point (no traps, results unused)
+  const int nunits = r.active ? r.A : r.ne;
+  double wr[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) wr[k] = k < KMAX ? Ws[k][lane] : 0.0;
+  double acc = 0.0;
+  for (int idx = blockIdx.x * 4 + warp; idx < nunits; idx += gridDim.x * 4) {
+    const int e = r.active ? r.active[idx] : idx;
+    const double rho = r.active ? r.rho[idx] : 1.0;
+    double R[NU], N;
+    bool deg;
+    value_unit<LAW, NB, NQ, NS>(T, r, la, e, pp, wr, [&](int a) { return Ts[a][lane]; }, R, N, deg);
+    if (!pv) continue;
+    if (deg) flag_degenerate(r, p, e);
+    if (r.mode == MODE_RESIDUAL) {
+      double* o_ = r.out + ((size_t)p * r.ne + e) * NU;
+#pragma unroll
+      for (int i = 0; i < NU; ++i) o_[i] = R[i];
+    } else {
+      double r2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < NU; ++i) r2 = fma(R[i], R[i], r2);
+      acc += r.mode == MODE_OBJECTIVE ? 0.5 * rho * (r2 + N * N) : r2;
+    }
+  }
+  if (r.mode == MODE_RESIDUAL) return;
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && pv) r.part[(size_t)p * gridDim.x + blockIdx.x] = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
 }
 
 static __global__ void sum_partials_kernel(const double* __restrict__ part, int nparts, int P, double* __restrict__ out,

@@ -149,13 +149,18 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
     return 0;
   }
   if (a.mode == MODE_OBJECTIVE || a.mode == MODE_RESNORM2 || a.mode == MODE_RESIDUAL) {
-    const int gx = (nunits + 127) / 128;
+    const bool multi = a.P >= 8;  // many parameter points: warp per element, lanes over mu
+    const int gy = multi ? (a.P + 31) / 32 : a.P;
+    const int gx = multi ? std::max(1, std::min((nunits + 3) / 4, (h->num_sms * 16 + gy - 1) / gy)) : (nunits + 127) / 128;
     if (a.mode != MODE_RESIDUAL) {
       if (ensure_part(h, (size_t)a.P * gx)) return -2;
       r.part = h->part;
     }
     prof_mark(h, a.stream, 0);
-    value_kernel<LAW, NB, NQ, NS><<<dim3(gx, a.P), 128, 0, a.stream>>>(prm);
+    if (multi)
+      value_mu_kernel<LAW, NB, NQ, NS><<<dim3(gx, gy), 128, 0, a.stream>>>(prm);
+    else
+      value_kernel<LAW, NB, NQ, NS><<<dim3(gx, a.P), 128, 0, a.stream>>>(prm);
     prof_mark(h, a.stream, 1);
     CK(cudaGetLastError());
     if (a.mode != MODE_RESIDUAL) {
