@@ -326,7 +326,7 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
               FXp[(2 * c) * NFSP] * dnu0 + FXp[(2 * c + 1) * NFSP] * dnu1 - FXp[(2 * M + c) * NFSP] * coef;
       }
     }
-    __syncwarp();
+    // (no barrier: the L stage reads only BQ / CF; TQ / FD / R rows are read after later barriers)
     // prefetch the projection's B fragments (basis rows of the element and of the
     // neighbors' face nodes) so their load latency overlaps the L stage
     double pfe[6][2], pfn[3][3][2];
