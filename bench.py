@@ -77,7 +77,7 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
 
@@ -311,7 +311,7 @@ def run_mine(args):
                    "elements": ne, "n_u": nu, "K": K, "l2": "inputs larger than L2 (Phi %.0f MB)" % (case.phi.nbytes / 1e6),
                    "parallelism": f"element-range x{world}" + (" + NCCL all_reduce of 1+K+K^2 sums" if world > 1 else "")},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "derivs_kernel<Euler,6,12,4>",
+                     "traffic": traffic, "kernel": "derivs_mma_kernel<Euler,12>",
                      "flops_per_element": F, "flops_per_launch": per_launch_flops,
                      "kernel_ms_avg": kern_avg_s * 1e3, "peak_source": peak_src,
                      "hbm_bytes_per_launch": bytes_per_pass(ne, case.mesh.num_nodes, nu, ku, kx)},
@@ -331,7 +331,7 @@ def run_mine(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--n", type=int, default=256, help="cells per side of the unit square (cfg2: 256)")

@@ -465,22 +465,27 @@ static __global__ void sum_partials_kernel(const double* __restrict__ part, int 
 }
 
 static __global__ void finalize_derivs_kernel(const double* __restrict__ part, int gx, int K, int KP, int P,
-                                       double* __restrict__ out, const int* __restrict__ mask) {
+                                              double* __restrict__ out, const int* __restrict__ mask) {
+  // one warp per output entry: lane-strided partial sums, then a fixed-order shuffle tree
+  // (deterministic: the same grid always sums in the same order)
   const int p = blockIdx.y;
   if (mask && !mask[p]) return;
   const int PSZ = 1 + K + KP * KP;
   const int OSZ = 1 + K + K * K;
-  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < OSZ; o += gridDim.x * blockDim.x) {
-    int src;
-    if (o < 1 + K) src = o;
-    else {
-      int k = (o - 1 - K) / K, l = (o - 1 - K) % K;
-      src = 1 + K + min(k, l) * KP + max(k, l);
-    }
-    double s = 0.0;
-    for (int b = 0; b < gx; ++b) s += part[((size_t)p * gx + b) * PSZ + src];
-    out[(size_t)p * OSZ + o] = o == 0 ? 0.5 * s : s;
+  const int lane = threadIdx.x & 31;
+  const int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (o >= OSZ) return;
+  int src;
+  if (o < 1 + K) src = o;
+  else {
+    const int k = (o - 1 - K) / K, l = (o - 1 - K) % K;
+    src = 1 + K + min(k, l) * KP + max(k, l);
   }
+  double s = 0.0;
+  for (int b = lane; b < gx; b += 32) s += part[((size_t)p * gx + b) * PSZ + src];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+  if (lane == 0) out[(size_t)p * OSZ + o] = o == 0 ? 0.5 * s : s;
 }
 
 }  // namespace strom

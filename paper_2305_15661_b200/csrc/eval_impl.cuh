@@ -67,7 +67,7 @@ static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WS
   CK(cudaGetLastError());
   if (a.mode == MODE_DERIVS) {
     const int OSZ = 1 + r.K + r.K * r.K;
-    finalize_derivs_kernel<<<dim3((OSZ + 127) / 128, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
+    finalize_derivs_kernel<<<dim3((OSZ + 3) / 4, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
     CK(cudaGetLastError());
   }
   return 0;
@@ -111,7 +111,7 @@ static int launch_mma(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& p
   CK(cudaGetLastError());
   if (a.mode == MODE_DERIVS) {
     const int OSZ = 1 + r.K + r.K * r.K;
-    finalize_derivs_kernel<<<dim3((OSZ + 127) / 128, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
+    finalize_derivs_kernel<<<dim3((OSZ + 3) / 4, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
     CK(cudaGetLastError());
   }
   return 0;
