@@ -111,3 +111,52 @@ def test_greedy_step_single_rank():
     ind = indicators(op, case.mus, np.stack([r.w for r in res]), np.stack([r.tau for r in res]))
     ind[1] = -np.inf
     assert i == int(np.argmax(ind)) and abs(v - ind[i]) <= 1e-12 * abs(ind[i])
+
+
+@pytest.mark.parametrize("ku,kx", [(20, 10), (24, 12), (32, 8), (5, 3)])
+def test_reduced_dimensions_match_oracle(ku, kx):
+    """Config 3 / 5 reduced dimensions (K = 30, 36) and odd / maximal k_u on the
+    DMMA kernel (n-tile padding, 10 and 15 Gram tiles) vs the oracle."""
+    from paper_2305_15661_b200 import configs
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.reduced import ReducedCoords
+
+    case = configs.sector_rom_case(n_radial=6, n_circ=8, ku=ku, kx=kx, frac_active=0.3, rho_scale=3.0, P=2, seed=31)
+    rng = np.random.default_rng(ku)
+    w = case.W[0] + 0.02 * rng.standard_normal(ku)
+    tau = 1e-3 * rng.standard_normal(kx)
+    op = gpu_op(case)
+    ref = OracleReducedOperator(case.law, OracleGeometry(case.mesh, case.maps, case.quad_order), case.phi, case.psi,
+                                case.ref_coords, case.kappa, case.eps)
+    for rho in (None, case.rho):
+        got = op.derivatives(ReducedCoords(w, tau), case.mus[0], None if rho is None else WeightVector(rho))
+        want = ref.derivatives(w, tau, case.mus[0], rho)
+        for a, b in zip(got, want):
+            assert rel_err(a, b) < 1e-10
+    for a, b in zip(op.elemental_contributions(ReducedCoords(w, tau), case.mus[0], split=True),
+                    ref.elemental_contributions(w, tau, case.mus[0], split=True)):
+        assert rel_err(a, b) < 1e-10
+
+
+def test_batched_derivatives_match_single():
+    """P parameter points in one launch equal P single calls (bit-exact)."""
+    from paper_2305_15661_b200 import _lib
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.reduced import ReducedCoords
+
+    case = small_sector()
+    op = gpu_op(case)
+    rho = WeightVector(case.rho)
+    rng = np.random.default_rng(9)
+    W = case.W + 0.01 * rng.standard_normal(case.W.shape)
+    Tau = 1e-3 * rng.standard_normal((3, 4))
+    K = 10
+    out, _ = op.eval_batched(_lib.DERIVS, torch.as_tensor(W).cuda(), torch.as_tensor(Tau).cuda(),
+                             torch.as_tensor(case.mus).cuda(), rho)
+    out = out.view(3, 1 + K + K * K).cpu().numpy()
+    for p in range(3):
+        J, S, T, Hww, Hwt, Htt = op.derivatives(ReducedCoords(W[p], Tau[p]), case.mus[p], rho)
+        assert out[p, 0] == J and np.array_equal(out[p, 1:7], S)
+        obj, _ = op.eval_batched(_lib.OBJECTIVE, torch.as_tensor(W).cuda(), torch.as_tensor(Tau).cuda(),
+                                 torch.as_tensor(case.mus).cuda(), rho)
+        assert abs(obj.cpu().numpy()[p] - op.objective(ReducedCoords(W[p], Tau[p]), case.mus[p], rho)) <= 1e-14 * abs(J)
