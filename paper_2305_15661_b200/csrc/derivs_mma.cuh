@@ -67,7 +67,7 @@ __device__ __forceinline__ int face_local(int f, int n) {
   return n == a ? 0 : (n == b ? 1 : (n == 3 + f ? 2 : -1));
 }
 
-template <class LAW, int NQ>
+template <class LAW, int NQ, int KUT = 0, int KXT = 0>  // KUT/KXT > 0: compile-time reduced dimensions
 __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
   using SH = MShape<NQ>;
   constexpr int M = 4, NB = 6, NU = 24, NF = 3, NS = 4, NFS = 12, PD = 2;
@@ -82,7 +82,10 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int p = blockIdx.y;
   if (r.mask && !r.mask[p]) return;
-  const int ku = r.ku, kx = r.kx, K = r.K, KP = r.KP, LDJ = r.LDJ;
+  constexpr bool CT = KUT > 0;
+  constexpr int KT = KUT + KXT, KPT = (KT + 7) / 8 * 8;
+  const int ku = CT ? KUT : r.ku, kx = CT ? KXT : r.kx, K = CT ? KT : r.K, KP = CT ? KPT : r.KP;
+  const int LDJ = CT ? KPT + 4 : r.LDJ;
   double* const S = smem + (size_t)warp * r.gx_warp_stride;
   double* const RA = S + SH::RA;
   double* const HA = S + r.gx_warp_stride - 4 - 48 - KP * KP;  // warp Gram accumulator (KP x KP)

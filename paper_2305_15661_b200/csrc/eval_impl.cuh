@@ -73,8 +73,8 @@ static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WS
   return 0;
 }
 
-template <class LAW, int NQ>
-static int launch_mma(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& prm, int nunits) {
+template <class LAW, int NQ, int KUT, int KXT>
+static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& prm, int nunits) {
   using SH = MShape<NQ>;
   Run& r = prm.r;
   r.LDJ = r.KP + 4;  // == 4 mod 8 doubles: conflict-free half-warp fragment loads
@@ -87,7 +87,7 @@ static int launch_mma(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& p
   if (const char* ev = getenv("STROM_MMA_WARPS")) nwarps = std::max(1, std::min(nwarps, atoi(ev)));
   if (nwarps < 1) return fail(-1, "element does not fit in shared memory");
   const size_t smem = nwarps * warp_bytes;
-  auto kern = derivs_mma_kernel<LAW, NQ>;
+  auto kern = derivs_mma_kernel<LAW, NQ, KUT, KXT>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nwarps * 32, smem));
@@ -115,6 +115,17 @@ static int launch_mma(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& p
     CK(cudaGetLastError());
   }
   return 0;
+}
+
+template <class LAW, int NQ>
+static int launch_mma(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& prm, int nunits) {
+  // compile-time reduced dimensions for the BASELINE configs (addressing folds to immediates)
+  if (!getenv("STROM_GENERIC_K")) {
+    if (h->ku == 16 && h->kx == 8) return launch_mma_t<LAW, NQ, 16, 8>(h, a, prm, nunits);
+    if (h->ku == 20 && h->kx == 10) return launch_mma_t<LAW, NQ, 20, 10>(h, a, prm, nunits);
+    if (h->ku == 24 && h->kx == 12) return launch_mma_t<LAW, NQ, 24, 12>(h, a, prm, nunits);
+  }
+  return launch_mma_t<LAW, NQ, 0, 0>(h, a, prm, nunits);
 }
 
 template <class LAW, int NB, int NQ, int NS>
