@@ -53,7 +53,8 @@ static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WS
   const int ngroups = (nunits + UPW - 1) / UPW;
   const int target = h->num_sms * per_sm;
   const int maxb = std::max(1, (ngroups + nwarps - 1) / nwarps);
-  int gx = std::max(1, std::min(maxb, (target + a.P - 1) / a.P));
+  const int live = a.live > 0 ? a.live : a.P;
+  int gx = std::max(1, std::min(maxb, (target + live - 1) / live));
   r.gx = gx;
   r.ntiles = ngroups;
   const int PSZ = 1 + r.K + r.KP * r.KP;
@@ -94,7 +95,8 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
   per_sm = std::max(per_sm, 1);
   const int target = h->num_sms * per_sm;
   const int maxb = std::max(1, (nunits + nwarps - 1) / nwarps);
-  int gx = std::max(1, std::min(maxb, (target + a.P - 1) / a.P));
+  const int live = a.live > 0 ? a.live : a.P;
+  int gx = std::max(1, std::min(maxb, (target + live - 1) / live));
   r.gx = gx;
   r.ntiles = nunits;
   if (getenv("STROM_DEBUG"))

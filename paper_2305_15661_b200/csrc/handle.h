@@ -46,6 +46,7 @@ struct EvalArgs {
   double* out;
   int* degen;
   cudaStream_t stream;
+  int live = 0;  // number of unmasked rows (0 = all): sizes the grid for sparse LM rounds
 };
 
 }  // namespace strom_host
