@@ -585,16 +585,37 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
     }
     // ---- G: Gram and gradient, or per-element contributions --------------------------------
     if (r.mode == MODE_DERIVS) {
-      for (int t = 0; t < ntri; ++t) {
-        const int ti = s_tile[t] >> 4, tj = s_tile[t] & 15;
-        double c0 = 0.0, c1 = 0.0;
-        const double* ja = Jt + (lane & 3) * LDJ + ti * 8 + (lane >> 2);
-        const double* jb = Jt + (lane & 3) * LDJ + tj * 8 + (lane >> 2);
+      if constexpr (CT) {
+        // fragments of J^T per (tile column, k-step), loaded once and shared by the tiles
+        constexpr int NT8C = KPT / 8;
+        double fr[NT8C][NU / 4];
 #pragma unroll
-        for (int rs = 0; rs < NU / 4; ++rs) dmma(c0, c1, ja[rs * 4 * LDJ], jb[rs * 4 * LDJ]);
-        double* Hp = HA + (ti * 8 + (lane >> 2)) * KP + tj * 8 + 2 * (lane & 3);
-        Hp[0] = fma(rho, c0, Hp[0]);
-        Hp[1] = fma(rho, c1, Hp[1]);
+        for (int cc = 0; cc < NT8C; ++cc)
+#pragma unroll
+          for (int rs = 0; rs < NU / 4; ++rs) fr[cc][rs] = Jt[(rs * 4 + (lane & 3)) * LDJ + cc * 8 + (lane >> 2)];
+#pragma unroll
+        for (int ti = 0; ti < NT8C; ++ti)
+#pragma unroll
+          for (int tj = ti; tj < NT8C; ++tj) {
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int rs = 0; rs < NU / 4; ++rs) dmma(c0, c1, fr[ti][rs], fr[tj][rs]);
+            double* Hp = HA + (ti * 8 + (lane >> 2)) * KP + tj * 8 + 2 * (lane & 3);
+            Hp[0] = fma(rho, c0, Hp[0]);
+            Hp[1] = fma(rho, c1, Hp[1]);
+          }
+      } else {
+        for (int t = 0; t < ntri; ++t) {
+          const int ti = s_tile[t] >> 4, tj = s_tile[t] & 15;
+          double c0 = 0.0, c1 = 0.0;
+          const double* ja = Jt + (lane & 3) * LDJ + ti * 8 + (lane >> 2);
+          const double* jb = Jt + (lane & 3) * LDJ + tj * 8 + (lane >> 2);
+  #pragma unroll
+          for (int rs = 0; rs < NU / 4; ++rs) dmma(c0, c1, ja[rs * 4 * LDJ], jb[rs * 4 * LDJ]);
+          double* Hp = HA + (ti * 8 + (lane >> 2)) * KP + tj * 8 + 2 * (lane & 3);
+          Hp[0] = fma(rho, c0, Hp[0]);
+          Hp[1] = fma(rho, c1, Hp[1]);
+        }
       }
       __syncwarp();
       for (int pi = lane; pi < kx * kx; pi += 32) {
