@@ -205,13 +205,31 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ row, const 
   return a0 + a1;
 }
 
+// same with w through an accessor (shared-memory column of the warp's parameter points)
+template <class WGet>
+__device__ __forceinline__ double row_dot_g(const double* __restrict__ row, WGet WG, int ku) {
+  double a0 = 0.0, a1 = 0.0;
+  if ((ku & 1) == 0) {
+    const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll 4
+    for (int k2 = 0; k2 < (ku >> 1); ++k2) {
+      const double2 t = __ldg(r2 + k2);
+      a0 = fma(t.x, WG(2 * k2), a0);
+      a1 = fma(t.y, WG(2 * k2 + 1), a1);
+    }
+  } else {
+    for (int k = 0; k < ku; ++k) a0 = fma(__ldg(row + k), WG(k), a0);
+  }
+  return a0 + a1;
+}
+
 // ============================================================================
 // K2: element residual (value path) for one (element, mu); w / tau through the
 // accessors WG(k) / TG(a) so one body serves both kernel layouts below
 // ============================================================================
-template <class LAW, int NB, int NQ, int NS, class TGet>
+template <class LAW, int NB, int NQ, int NS, class WGet, class TGet>
 __device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB, NQ, NS>::NF>& T, const Run& r,
-                                           const LawArgs& la, int e, int p, const double* wr, TGet TG,
+                                           const LawArgs& la, int e, int p, WGet WG, TGet TG,
                                            double* R, double& Nd, bool& degenerate) {
   using SH = Shape<LAW, NB, NQ, NS>;
   constexpr int M = SH::M, NU = SH::NU, NF = SH::NF, PD = SH::P;
@@ -236,7 +254,7 @@ __device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB,
 #pragma unroll
     for (int i = 0; i < NU; ++i) {
       const double v = r.u0 ? r.u0[(size_t)p * r.u0_stride + (size_t)e * NU + i] : 0.0;
-      U[i] = v + row_dot(ph + i * r.ku, wr, r.ku);
+      U[i] = v + row_dot_g(ph + i * r.ku, WG, r.ku);
     }
   }
   Geo o;
@@ -244,8 +262,8 @@ __device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB,
   degenerate = o.g <= 0.0;
 #pragma unroll
   for (int i = 0; i < NU; ++i) R[i] = 0.0;
-  // volume (dg.py:105-125)
-#pragma unroll
+  // volume (dg.py:105-125); rolled loop: keeps the kernel in the instruction cache
+#pragma unroll 1
   for (int q = 0; q < NQ; ++q) {
     double uq[M];
 #pragma unroll
@@ -299,7 +317,7 @@ __device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB,
         for (int c = 0; c < M; ++c) {
           int row = node * M + c;
           const double v = r.u0 ? r.u0[(size_t)p * r.u0_stride + (size_t)nb * NU + row] : 0.0;
-          Un[j][c] = v + row_dot(ph + row * r.ku, wr, r.ku);
+          Un[j][c] = v + row_dot_g(ph + row * r.ku, WG, r.ku);
         }
       }
     }
@@ -368,12 +386,9 @@ __global__ void __launch_bounds__(128) value_kernel(const __grid_constant__ Para
     for (int i = 0; i < NMU; ++i) la.mu[i] = i < r.nmu ? r.mu[p * r.nmu + i] : 0.0;
     const double* w = r.w + (size_t)p * r.ku;
     const double* tau = r.tau + (size_t)p * r.kx;
-    double wr[32];
-#pragma unroll
-    for (int k = 0; k < 32; ++k) wr[k] = k < r.ku ? __ldg(w + k) : 0.0;
     double R[NU], N;
     bool deg;
-    value_unit<LAW, NB, NQ, NS>(T, r, la, e, p, wr, [&](int a) { return __ldg(tau + a); }, R, N, deg);
+    value_unit<LAW, NB, NQ, NS>(T, r, la, e, p, [&](int k) { return __ldg(w + k); }, [&](int a) { return __ldg(tau + a); }, R, N, deg);
     if (deg) flag_degenerate(r, p, e);
     if (r.mode == MODE_RESIDUAL) {
       double* o_ = r.out + ((size_t)p * r.ne + e) * NU;
@@ -426,16 +441,13 @@ __global__ void __launch_bounds__(128) value_mu_kernel(const __grid_constant__ P
   for (int i = 0; i < NMU; ++i) la.mu[i] = (i < r.nmu && p < r.P) ? r.mu[p * r.nmu + i] : (i < r.nmu ? r.mu[i] : 0.0);
   const int pp = pv ? p : blockIdx.y * 32;  // idle lanes shadow a valid point (no traps, results unused)
   const int nunits = r.active ? r.A : r.ne;
-  double wr[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) wr[k] = k < KMAX ? Ws[k][lane] : 0.0;
   double acc = 0.0;
   for (int idx = blockIdx.x * 4 + warp; idx < nunits; idx += gridDim.x * 4) {
     const int e = r.active ? r.active[idx] : idx;
     const double rho = r.active ? r.rho[idx] : 1.0;
     double R[NU], N;
     bool deg;
-    value_unit<LAW, NB, NQ, NS>(T, r, la, e, pp, wr, [&](int a) { return Ts[a][lane]; }, R, N, deg);
+    value_unit<LAW, NB, NQ, NS>(T, r, la, e, pp, [&](int k) { return Ws[k][lane]; }, [&](int a) { return Ts[a][lane]; }, R, N, deg);
     if (!pv) continue;
     if (deg) flag_degenerate(r, p, e);
     if (r.mode == MODE_RESIDUAL) {
