@@ -119,15 +119,31 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
   const int nt8 = KP / 8, ntri = nt8 * (nt8 + 1) / 2;
   const int ntu = (ku + 7) / 8;
 
-  for (int idx = blockIdx.x * nwarps + warp; idx < nunits; idx += gridDim.x * nwarps) {
-    const int e = r.active ? r.active[idx] : idx;
+  // element index block carried in smem: [0] e, [1..3] nodes, [4..6] neighbors, [7..9] face info.
+  // Each iteration loads the next unit's block mid-way and stores it after the Jx
+  // stage, so the gather's address chain starts from shared memory.
+  int* const EI = reinterpret_cast<int*>(S + SH::MINT);
+  const int ustride = gridDim.x * nwarps;
+  auto index_word = [&](int ue, int l) -> int {
+    return l == 0 ? ue : (l < 4 ? __ldg(r.elem_nodes + 3 * ue + l - 1)
+                               : (l < 7 ? __ldg(r.nbr + 3 * ue + l - 4) : __ldg(r.finfo + 3 * ue + l - 7)));
+  };
+  {
+    const int idx0 = blockIdx.x * nwarps + warp;
+    if (idx0 < nunits && lane < 10) EI[lane] = index_word(r.active ? __ldg(r.active + idx0) : idx0, lane);
+    __syncwarp();
+  }
+  for (int idx = blockIdx.x * nwarps + warp; idx < nunits; idx += ustride) {
+    const int e = EI[0];
     const double rho = r.active ? r.rho[idx] : 1.0;
+    const int nidx = idx + ustride;
+    const int nact = (r.active && nidx < nunits) ? __ldg(r.active + nidx) : nidx;
     int nbr[3], fin[3];
 #pragma unroll
-    for (int f = 0; f < 3; ++f) { nbr[f] = r.nbr[3 * e + f]; fin[f] = r.finfo[3 * e + f]; }
+    for (int f = 0; f < 3; ++f) { nbr[f] = EI[4 + f]; fin[f] = EI[7 + f]; }
     // ---- G: coordinates and gathers (lane k = basis column k) --------------------
     if (lane < 6) {
-      const int n = r.elem_nodes[3 * e + (lane >> 1)];
+      const int n = EI[1 + (lane >> 1)];
       const int row = 2 * n + (lane & 1);
       double v = r.xref[(size_t)p * r.x_stride + row];
       const double* ps = r.psi + (size_t)row * kx;
@@ -173,7 +189,7 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
       double X[6];
 #pragma unroll
       for (int g = 0; g < 3; ++g) {
-        const int n = r.elem_nodes[3 * e + g];
+        const int n = EI[1 + g];
         X[2 * g] = r.nodes[2 * n];
         X[2 * g + 1] = r.nodes[2 * n + 1];
       }
@@ -192,68 +208,104 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
       }
     }
     __syncwarp();
-    // ---- P: pointwise physics (lanes = face points, then volume points) -----------
-    if (lane < NFS) {
-      const int fs = lane, f = fs / NS, s = fs % NS;
+    // ---- P: pointwise physics on 24 lanes, one code path: lane = side * 12 + fs evaluates
+    // face point fs on side `side` (0 in, 1 out) fused with volume point q = fs along the
+    // adj(Jx) row `side`; the two sides of a face point meet through shuffles.
+    {
+      static_assert(NQ >= NFS, "fused P stage needs n_q >= 12");
+      const int l24 = lane < 2 * NFS ? lane : lane - 2 * NFS;  // lanes 24..31 shadow 0..7 (no writes)
+      const int side = l24 >= NFS ? 1 : 0, fs = l24 - side * NFS, f = fs / NS, s = fs % NS;
       const int fi = fin[f], bc = fi >> 3;
+      const bool nside = side && bc == 0;
+      const int sp = (nside && ((fi >> 2) & 1)) ? NS - 1 - s : s;
       const double* nu = S + SH::MNU + 2 * f;
       const double len = S[SH::MNLEN + f];
       const double* nh = S + SH::MNHAT + 2 * f;
-      double ui[M], uo[M];
+      double us[M];
 #pragma unroll
       for (int c = 0; c < M; ++c) {
         double v = 0.0;
 #pragma unroll
-        for (int j = 0; j < NF; ++j) v = fma(T.trace[0][s][j], S[SH::UE + fnode_of(PD, f, j) * M + c], v);
-        ui[c] = v;
+        for (int j = 0; j < NF; ++j)
+          v = fma(T.trace[0][sp][j], S[(nside ? SH::UNF + (f * NF + j) * M : SH::UE + fnode_of(PD, f, j) * M) + c], v);
+        us[c] = v;
       }
-      if (bc == 0) {
-        const int sp = ((fi >> 2) & 1) ? NS - 1 - s : s;
-#pragma unroll
-        for (int c = 0; c < M; ++c) {
-          double v = 0.0;
-#pragma unroll
-          for (int j = 0; j < NF; ++j) v = fma(T.trace[0][sp][j], S[SH::UNF + (f * NF + j) * M + c], v);
-          uo[c] = v;
-        }
-      } else if (bc == 1) {
-#pragma unroll
-        for (int c = 0; c < M; ++c) uo[c] = ui[c];
-      } else {
-        LAW::ghost(bc - 2, la, uo);
-      }
-      double fi2[M][2], fo2[M][2], Ai[M][M], Ao[M][M], gi[M], go[M], gni[2], gno[2];
-      const double wsi = PointOps<LAW>::face_side(ui, nu, nh, fi2, Ai, gi, gni, la);
-      const double wso = PointOps<LAW>::face_side(uo, nu, nh, fo2, Ao, go, gno, la);
-      const bool in_wins = wsi >= wso;  // dual.maximum tie -> first argument (dual.py:171)
-      const double lam = in_wins ? wsi : wso;
-      const double ws = T.ws[s];
-      double* FXp = S + SH::FX;
+      if (side && bc >= 2) LAW::ghost(bc - 2, la, us);
+      double f2[M][2], A[M][M], g[M], gn[2];
+      const double ws = PointOps<LAW>::face_side(us, nu, nh, f2, A, g, gn, la);
+      const int q = fs;
+      double uq[M];
 #pragma unroll
       for (int c = 0; c < M; ++c) {
-        const double du = uo[c] - ui[c];
-        const double fni = fi2[c][0] * nu[0] + fi2[c][1] * nu[1], fno = fo2[c][0] * nu[0] + fo2[c][1] * nu[1];
-        S[SH::HS + c * NFSP + fs] = ws * (0.5 * (fni + fno) - 0.5 * (lam * len) * du);
-        FXp[(2 * c + 0) * NFSP + fs] = 0.5 * ws * (fi2[c][0] + fo2[c][0]);
-        FXp[(2 * c + 1) * NFSP + fs] = 0.5 * ws * (fi2[c][1] + fo2[c][1]);
-        FXp[(2 * M + c) * NFSP + fs] = 0.5 * ws * du;
+        double v = 0.0;
 #pragma unroll
-        for (int cp = 0; cp < M; ++cp) {
-          const double dl_in = in_wins ? gi[cp] : 0.0;
-          const double dl_out = in_wins ? 0.0 : go[cp];
-          double cin = 0.5 * Ai[c][cp] + (c == cp ? 0.5 * lam * len : 0.0) - 0.5 * len * du * dl_in;
-          double cout = 0.5 * Ao[c][cp] - (c == cp ? 0.5 * lam * len : 0.0) - 0.5 * len * du * dl_out;
-          if (bc == 1) { cin += cout; cout = 0.0; }
-          if (bc >= 2) cout = 0.0;
-          RA[SH::CF + ((0 * M + c) * M + cp) * NFSP + fs] = ws * cin;
-          RA[SH::CF + ((1 * M + c) * M + cp) * NFSP + fs] = ws * cout;
+        for (int n = 0; n < NB; ++n) v = fma(T.phi[q][n], S[SH::UE + n * M + c], v);
+        uq[c] = v;
+      }
+      const double dv[2] = {S[SH::MADJ + 2 * side], S[SH::MADJ + 2 * side + 1]};
+      double fq[M][2], Aq[M][M];
+      PointOps<LAW>::vol_dir(uq, dv, fq, Aq, la);
+      const int partner = side ? lane - NFS : (lane + NFS) & 31;
+      const double wsp = __shfl_sync(0xffffffffu, ws, partner);
+      double up[M], fp[M][2];
+#pragma unroll
+      for (int c = 0; c < M; ++c) {
+        up[c] = __shfl_sync(0xffffffffu, us[c], partner);
+        fp[c][0] = __shfl_sync(0xffffffffu, f2[c][0], partner);
+        fp[c][1] = __shfl_sync(0xffffffffu, f2[c][1], partner);
+      }
+      if (lane < 2 * NFS) {
+        const double wsi = side ? wsp : ws, wso = side ? ws : wsp;
+        const bool in_wins = wsi >= wso;  // dual.maximum tie -> first argument (dual.py:171)
+        const bool mine = (side == 0) == in_wins;
+        const double lam = in_wins ? wsi : wso;
+        const double wsq = T.ws[s];
+        double* FXp = S + SH::FX;
+        double du[M];
+#pragma unroll
+        for (int c = 0; c < M; ++c) du[c] = side ? us[c] - up[c] : up[c] - us[c];
+        if (side == 0) {
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            const double fni = f2[c][0] * nu[0] + f2[c][1] * nu[1], fno = fp[c][0] * nu[0] + fp[c][1] * nu[1];
+            S[SH::HS + c * NFSP + fs] = wsq * (0.5 * (fni + fno) - 0.5 * (lam * len) * du[c]);
+            FXp[(2 * c + 0) * NFSP + fs] = 0.5 * wsq * (f2[c][0] + fp[c][0]);
+            FXp[(2 * c + 1) * NFSP + fs] = 0.5 * wsq * (f2[c][1] + fp[c][1]);
+            FXp[(2 * M + c) * NFSP + fs] = 0.5 * wsq * du[c];
+          }
+          FXp[(3 * M + 0) * NFSP + fs] = lam;
+        }
+        if (mine) {
+          FXp[(3 * M + 1) * NFSP + fs] = gn[0];
+          FXp[(3 * M + 2) * NFSP + fs] = gn[1];
+        }
+        const double hl = 0.5 * lam * len;
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+#pragma unroll
+          for (int cp = 0; cp < M; ++cp) {
+            const double dl = mine ? g[cp] : 0.0;
+            double cv = 0.5 * A[c][cp] + (c == cp ? (side ? -hl : hl) : 0.0) - 0.5 * len * du[c] * dl;
+            if (side == 0 && bc == 1) {  // extrapolated exterior state: C_in += C_out (uo == ui, so Ao == Ai)
+              const double dlo = in_wins ? 0.0 : g[cp];
+              cv += 0.5 * A[c][cp] - (c == cp ? hl : 0.0) - 0.5 * len * du[c] * dlo;
+            }
+            if (side == 1 && bc >= 1) cv = 0.0;
+            RA[SH::CF + ((side * M + c) * M + cp) * NFSP + fs] = wsq * cv;
+          }
+        const double wq = T.wq[q];
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          if (side == 0) {
+            S[SH::FQ + (c * 2 + 0) * NQP + q] = wq * fq[c][0];
+            S[SH::FQ + (c * 2 + 1) * NQP + q] = wq * fq[c][1];
+          }
+#pragma unroll
+          for (int cp = 0; cp < M; ++cp) RA[SH::BQ + ((side * M + cp) * M + c) * SH::NQC + q] = wq * Aq[c][cp];
         }
       }
-      FXp[(3 * M + 0) * NFSP + fs] = lam;
-      FXp[(3 * M + 1) * NFSP + fs] = in_wins ? gni[0] : gno[0];
-      FXp[(3 * M + 2) * NFSP + fs] = in_wins ? gni[1] : gno[1];
     }
-    for (int q = lane; q < NQ; q += 32) {
+    for (int q = NFS + lane; q < NQ; q += 32) {  // remaining volume points (n_q > 12)
       double uq[M];
 #pragma unroll
       for (int c = 0; c < M; ++c) {
@@ -362,6 +414,8 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
         }
       }
     }
+    // next unit's index block: loaded here, stored to smem after the Jx stage
+    const int wv = (nidx < nunits && lane < 10) ? index_word(nact, lane) : 0;
     // ---- L: volume local Jacobian on DMMA; X = Dq^T B_q fused into the A fragments ------
     {
       double lv[4][3][2];
@@ -540,7 +594,7 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
         double af[3];
 #pragma unroll
         for (int mt = 0; mt < 3; ++mt) af[mt] = RA[SH::DRX + (mt * 8 + (lane >> 2)) * LDX + d];
-        const int node = d < 6 ? r.elem_nodes[3 * e + (d >> 1)] : 0;
+        const int node = d < 6 ? EI[1 + (d >> 1)] : 0;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           if (nt < ntx) {
@@ -568,18 +622,19 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
         double dn = 0.0;
 #pragma unroll
         for (int d = 0; d < 6; ++d) {
-          const int node = r.elem_nodes[3 * e + (d >> 1)];
+          const int node = EI[1 + (d >> 1)];
           dn = fma(S[SH::DNX + d], __ldg(r.psi + (size_t)(2 * node + (d & 1)) * kx + lane), dn);
         }
         S[SH::DNP + lane] = dn;
       }
     }
     __syncwarp();
-    {  // L2 prefetch of the next element's basis block (3 KB at k_u = 16)
-      const int nidx = idx + gridDim.x * nwarps;
+    {  // next unit: index block into smem, L2 prefetch of its basis block (3 KB at k_u = 16).
+      // (prefetching the neighbor rows, U0, Psi and coordinates too measured 4-9% slower)
+      __syncwarp();
       if (nidx < nunits) {
-        const int ne_ = r.active ? r.active[nidx] : nidx;
-        const char* base = reinterpret_cast<const char*>(r.phi + (size_t)ne_ * NU * ku);
+        if (lane < 10) EI[lane] = wv;
+        const char* base = reinterpret_cast<const char*>(r.phi + (size_t)nact * NU * ku);
         for (int off = lane * 128; off < NU * ku * 8; off += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
       }
     }

@@ -242,6 +242,23 @@ struct Euler {
       A[3][0] = qn * (gk - H);       A[3][1] = H * n[0] - gm * vx * qn;         A[3][2] = H * n[1] - gm * vy * qn;         A[3][3] = g * qn;
     }
   }
+  // volume point along one direction: flux components f and A(n) = d(f.n)/du
+  __device__ static void vol_dir(const double* u, const double* n, double (*f)[2], double (*A)[4], const LawArgs& a) {
+    const double g = a.p[0], gm = g - 1.0;
+    const double r = u[0], ir = 1.0 / r, vx = u[1] * ir, vy = u[2] * ir;
+    const double p = gm * (u[3] - 0.5 * (u[1] * vx + u[2] * vy));
+    const double ke = 0.5 * (vx * vx + vy * vy);
+    const double Ep = u[3] + p, H = Ep * ir, gk = gm * ke;
+    f[0][0] = u[1];          f[0][1] = u[2];
+    f[1][0] = u[1] * vx + p; f[1][1] = u[1] * vy;
+    f[2][0] = u[2] * vx;     f[2][1] = u[2] * vy + p;
+    f[3][0] = Ep * vx;       f[3][1] = Ep * vy;
+    const double qn = vx * n[0] + vy * n[1];
+    A[0][0] = 0.0;                A[0][1] = n[0];                            A[0][2] = n[1];                            A[0][3] = 0.0;
+    A[1][0] = gk * n[0] - vx * qn; A[1][1] = qn + vx * n[0] - gm * vx * n[0]; A[1][2] = vx * n[1] - gm * vy * n[0];     A[1][3] = gm * n[0];
+    A[2][0] = gk * n[1] - vy * qn; A[2][1] = vy * n[0] - gm * vx * n[1];      A[2][2] = qn + vy * n[1] - gm * vy * n[1]; A[2][3] = gm * n[1];
+    A[3][0] = qn * (gk - H);       A[3][1] = H * n[0] - gm * vx * qn;         A[3][2] = H * n[1] - gm * vy * qn;         A[3][3] = g * qn;
+  }
   // everything a quadrature point needs, one code path for volume and face points:
   // flux components, A(d0), A(d1), ws(u, nh) with its gradients
   __device__ static double point_full(const double* u, const double* d0, const double* d1, const double* nh,
@@ -340,6 +357,9 @@ struct PointOps<LAW, true> {
   __device__ static void flux_dir(const double* u, const double* n, double* fn, double (*Am)[LAW::M], const LawArgs& a) {
     LAW::flux_dir(u, n, fn, Am, a);
   }
+  __device__ static void vol_dir(const double* u, const double* n, double (*f)[2], double (*Am)[LAW::M], const LawArgs& a) {
+    LAW::vol_dir(u, n, f, Am, a);
+  }
   __device__ static double wavespeed_grad(const double* u, const double* nh, double* dwdu, double* dwdn, const LawArgs& a) {
     return LAW::wavespeed_grad(u, nh, dwdu, dwdn, a);
   }
@@ -352,6 +372,11 @@ struct PointOps<LAW, false> {
                                      double (*Am)[M], double* dwdu, double* dwdn, const LawArgs& a);
   __device__ static void vol_point(const double* u, const double* d0, const double* d1, double (*f)[2],
                                    double (*A0)[M], double (*A1)[M], const LawArgs& a);
+  __device__ static void vol_dir(const double* u, const double* n, double (*f)[2], double (*Am)[M], const LawArgs& a) {
+    double fn[M];
+    LAW::flux(u, f, a);
+    flux_dir(u, n, fn, Am, a);
+  }
   __device__ static void flux_dir(const double* u, const double* n, double* fn, double (*Am)[M], const LawArgs& a) {
     Dn<M> ud[M];
 #pragma unroll
