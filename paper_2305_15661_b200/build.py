@@ -40,6 +40,7 @@ def build(force=False, verbose=False):
     nvcc = os.environ.get("NVCC", "nvcc")
     tmp = tempfile.mkdtemp(prefix="strom_build_")
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
+    flags += os.environ.get("STROM_NVCC_EXTRA", "").split()  # experiment knobs (-D...)
     if verbose:
         flags += ["-Xptxas", "-v"]
 

@@ -18,6 +18,9 @@
 namespace strom {
 
 constexpr int MTHREADS = 256;
+#ifndef STROM_MMA_MAXNREG
+#define STROM_MMA_MAXNREG 255
+#endif
 
 template <int NQ>
 struct MShape {
@@ -68,7 +71,7 @@ __device__ __forceinline__ int face_local(int f, int n) {
 }
 
 template <class LAW, int NQ, int KUT = 0, int KXT = 0>  // KUT/KXT > 0: compile-time reduced dimensions
-__global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
+__global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
   using SH = MShape<NQ>;
   constexpr int M = 4, NB = 6, NU = 24, NF = 3, NS = 4, NFS = 12, PD = 2;
   constexpr int NQP = SH::NQP, NFSP = SH::NFSP, LDL = SH::LDL, LDO = SH::LDO, LDX = SH::LDX;
@@ -142,27 +145,16 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
 #pragma unroll
     for (int f = 0; f < 3; ++f) { nbr[f] = EI[4 + f]; fin[f] = EI[7 + f]; }
     // ---- G: coordinates and gathers (lane k = basis column k) --------------------
-    if (lane < 6) {
-      const int n = EI[1 + (lane >> 1)];
-      const int row = 2 * n + (lane & 1);
-      double v = r.xref[(size_t)p * r.x_stride + row];
-      const double* ps = r.psi + (size_t)row * kx;
-      for (int a = 0; a < kx; ++a) v = fma(ps[a], s_tau[a], v);
-      S[SH::MX + lane] = v;
-    }
-    // element rows (0..23) and neighbor face-node rows (24..59): one dot product
-    // U = U0 + Phi_row . w per lane, vectorised 16-byte loads of the 8*k_u-byte rows
-    for (int rr = lane; rr < NU + SH::NNB; rr += 32) {
-      const double* src = nullptr;
-      double v = 0.0;
-      int dst;
+    // element rows (0..23) and neighbor face-node rows (24..59) land at S[UE + row]:
+    // U = U0 + Phi_row . w, one row per lane and round, 16-byte loads of the 8*k_u-byte rows
+    auto row_src = [&](int rr, const double*& src, double& v) {
+      src = nullptr;
+      v = 0.0;
       if (rr < NU) {
         src = r.phi + ((size_t)e * NU + rr) * ku;
         if (r.u0) v = r.u0[(size_t)p * r.u0_stride + (size_t)e * NU + rr];
-        dst = SH::UE + rr;
-      } else {
+      } else if (rr < NU + SH::NNB) {
         const int i = rr - NU, f = i / (NF * M), jj = (i / M) % NF, c = i % M;
-        dst = SH::UNF + i;
         if ((fin[f] >> 3) == 0) {
           const int nf = fin[f] & 3;
           const int node = jj == 0 ? nf : (jj == 1 ? (nf + 1) % 3 : 3 + nf);
@@ -170,19 +162,65 @@ __global__ void __maxnreg__(255) derivs_mma_kernel(const __grid_constant__ Param
           if (r.u0) v = r.u0[(size_t)p * r.u0_stride + (size_t)nbr[f] * NU + node * M + c];
         }
       }
-      if (src) {
-        if ((ku & 1) == 0) {
-          const double2* s2 = reinterpret_cast<const double2*>(src);
-          for (int k2 = 0; k2 < (ku >> 1); ++k2) {
-            const double2 t2 = __ldg(s2 + k2);
-            v = fma(t2.x, s_w[2 * k2], v);
-            v = fma(t2.y, s_w[2 * k2 + 1], v);
-          }
-        } else {
-          for (int k = 0; k < ku; ++k) v = fma(__ldg(src + k), s_w[k], v);
-        }
+    };
+    if constexpr (CT && KUT % 2 == 0) {
+      // both rounds' loads (and the coordinate rows) issued before any use: one memory
+      // round trip for the whole gather
+      constexpr int H = KUT / 2;
+      const double *src0, *src1;
+      double v0, v1;
+      row_src(lane, src0, v0);
+      row_src(lane + 32, src1, v1);
+      double2 b0[H], b1[H];
+#pragma unroll
+      for (int k2 = 0; k2 < H; ++k2) b0[k2] = src0 ? __ldg(reinterpret_cast<const double2*>(src0) + k2) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k2 = 0; k2 < H; ++k2) b1[k2] = src1 ? __ldg(reinterpret_cast<const double2*>(src1) + k2) : make_double2(0.0, 0.0);
+      const int lx = lane < 6 ? lane : 0;
+      const int xrow = 2 * EI[1 + (lx >> 1)] + (lx & 1);
+      double xv = r.xref[(size_t)p * r.x_stride + xrow];
+      double pv[KXT];
+#pragma unroll
+      for (int a2 = 0; a2 < KXT; ++a2) pv[a2] = __ldg(r.psi + (size_t)xrow * KXT + a2);
+#pragma unroll
+      for (int k2 = 0; k2 < H; ++k2) {
+        v0 = fma(b0[k2].x, s_w[2 * k2], v0);
+        v0 = fma(b0[k2].y, s_w[2 * k2 + 1], v0);
+        v1 = fma(b1[k2].x, s_w[2 * k2], v1);
+        v1 = fma(b1[k2].y, s_w[2 * k2 + 1], v1);
       }
-      S[dst] = v;
+#pragma unroll
+      for (int a2 = 0; a2 < KXT; ++a2) xv = fma(pv[a2], s_tau[a2], xv);
+      S[SH::UE + lane] = v0;
+      if (lane + 32 < NU + SH::NNB) S[SH::UE + lane + 32] = v1;
+      if (lane < 6) S[SH::MX + lane] = xv;
+    } else {
+      if (lane < 6) {
+        const int n = EI[1 + (lane >> 1)];
+        const int row = 2 * n + (lane & 1);
+        double v = r.xref[(size_t)p * r.x_stride + row];
+        const double* ps = r.psi + (size_t)row * kx;
+        for (int a2 = 0; a2 < kx; ++a2) v = fma(ps[a2], s_tau[a2], v);
+        S[SH::MX + lane] = v;
+      }
+      for (int rr = lane; rr < NU + SH::NNB; rr += 32) {
+        const double* src;
+        double v;
+        row_src(rr, src, v);
+        if (src) {
+          if ((ku & 1) == 0) {
+            const double2* s2 = reinterpret_cast<const double2*>(src);
+            for (int k2 = 0; k2 < (ku >> 1); ++k2) {
+              const double2 t2 = __ldg(s2 + k2);
+              v = fma(t2.x, s_w[2 * k2], v);
+              v = fma(t2.y, s_w[2 * k2 + 1], v);
+            }
+          } else {
+            for (int k = 0; k < ku; ++k) v = fma(__ldg(src + k), s_w[k], v);
+          }
+        }
+        S[SH::UE + rr] = v;
+      }
     }
     __syncwarp();
     {  // element geometry (all lanes), distortion gradient (lanes 0-5), face normals (lanes 0-2)

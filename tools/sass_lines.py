@@ -19,7 +19,8 @@ tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
 dis = ""
 for cub in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
-    d = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
+    kfile = os.environ.get("KFILE")  # attribute inlined code to its call site in this file
+    d = subprocess.run(["nvdisasm", "-gi" if kfile else "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
     if kname in d:
         dis = d
         break
@@ -33,6 +34,11 @@ for ln in dis.splitlines():
     m = re.search(r'//## File ".*?/([^/"]+)", line (\d+)', ln)
     if m:
         cur_line = f"{m.group(1)}:{m.group(2)}"
+        if kfile:
+            for fn, li in re.findall(r'"[^"]*?/([^/"]+)", line (\d+)', ln):
+                if fn == kfile:
+                    cur_line = f"{fn}:{li}"
+                    break
         continue
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
     if m and cur_line:
