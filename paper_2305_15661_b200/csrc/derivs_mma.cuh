@@ -40,26 +40,27 @@ struct MShape {
   static constexpr int RF = RV + NU;
   static constexpr int TQ = RF + NU;            // [4][NU]
   static constexpr int FX = TQ + 4 * NU;        // [field][NFSP]
-  static constexpr int FQ = FX + FXS * NFSP;    // [c][i][NQP]
-  static constexpr int HS = FQ + 2 * M * NQP;   // [c][NFSP]
-  static constexpr int FD = HS + M * NFSP;      // face mesh-response [f][s][c][2]
+  static constexpr int FD = FX + FXS * NFSP;    // face mesh-response [f][s][c][2]
   static constexpr int RA = FD + 2 * M * NFSP;
   static constexpr int LDX = 12;
   // region A (offsets from RA), by phase:
-  //   P/L : BQ [q][c][kk][c'] at 0           -> L [NU][LDL] at 0 once the L GEMM has read BQ
+  //   P/R : BQ [q][c][kk][c'] at 0, FQ [c][i][NQP] and HS [c][NFSP] right after it
+  //   L   : L [NU][LDL] at 0 once the L GEMM has read BQ (FQ / HS dead after R)
   //   P/F : CF [fs][side][c][c'] at LA       (read by the face blocks)
   //   F/J : one face's Lout [12][LDO] at LO  (projected right away)
-  //   X/G : DRX [NU][LDX] at LO (LOUT dead), Jt [NU][LDJ] at 0 (L, CF dead)
+  //   X/G : DRX [NU][LDX] at max(LA, NU LDJ) (CF, LOUT dead), Jt [NU][LDJ] at 0 (L dead)
   static constexpr int LDL = 28, LDO = 20;
   static constexpr int BQ = 0, LL = 0;
-  static constexpr int LA = (32 * NQC > NU * LDL ? 32 * NQC : NU * LDL);
+  static constexpr int FQ = 32 * NQC;
+  static constexpr int HS = FQ + 2 * M * NQP;
+  static constexpr int LA = (HS + M * NFSP > NU * LDL ? HS + M * NFSP : NU * LDL);
   static constexpr int CF = LA;
   static constexpr int LO = LA + 32 * NFSP;
-  static constexpr int DRX = LO;
-  static constexpr int RAEND = LO + (12 * LDO > NU * LDX ? 12 * LDO : NU * LDX);
+  __host__ __device__ static int drx(int LDJ) { return LA > NU * LDJ ? LA : NU * LDJ; }
+  __host__ __device__ static int gtail(int KP) { return KP + 8; }  // gradient (K) + residual norm
   __host__ __device__ static int warp_stride(int LDJ, int KP) {
-    int ra = RAEND > NU * LDJ ? RAEND : NU * LDJ;
-    int s = RA + ra + KP * KP + 48;
+    const int a = LO + 12 * LDO, b = drx(LDJ) + NU * LDX;
+    const int s = RA + (a > b ? a : b) + KP * KP + gtail(KP);
     return (s + 15) / 16 * 16 + 4;
   }
 };
@@ -91,7 +92,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
   const int LDJ = CT ? KPT + 4 : r.LDJ;
   double* const S = smem + (size_t)warp * r.gx_warp_stride;
   double* const RA = S + SH::RA;
-  double* const HA = S + r.gx_warp_stride - 4 - 48 - KP * KP;  // warp Gram accumulator (KP x KP)
+  const int DRXo = SH::drx(LDJ);
+  double* const HA = S + r.gx_warp_stride - 4 - SH::gtail(KP) - KP * KP;  // warp Gram accumulator (KP x KP)
   double* const GW = HA + KP * KP;
 
   for (int i = threadIdx.x; i < ku; i += blockDim.x) s_w[i] = r.w[(size_t)p * ku + i];
@@ -306,7 +308,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
 #pragma unroll
           for (int c = 0; c < M; ++c) {
             const double fni = f2[c][0] * nu[0] + f2[c][1] * nu[1], fno = fp[c][0] * nu[0] + fp[c][1] * nu[1];
-            S[SH::HS + c * NFSP + fs] = wsq * (0.5 * (fni + fno) - 0.5 * (lam * len) * du[c]);
+            RA[SH::HS + c * NFSP + fs] = wsq * (0.5 * (fni + fno) - 0.5 * (lam * len) * du[c]);
             FXp[(2 * c + 0) * NFSP + fs] = 0.5 * wsq * (f2[c][0] + fp[c][0]);
             FXp[(2 * c + 1) * NFSP + fs] = 0.5 * wsq * (f2[c][1] + fp[c][1]);
             FXp[(2 * M + c) * NFSP + fs] = 0.5 * wsq * du[c];
@@ -335,8 +337,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           if (side == 0) {
-            S[SH::FQ + (c * 2 + 0) * NQP + q] = wq * fq[c][0];
-            S[SH::FQ + (c * 2 + 1) * NQP + q] = wq * fq[c][1];
+            RA[SH::FQ + (c * 2 + 0) * NQP + q] = wq * fq[c][0];
+            RA[SH::FQ + (c * 2 + 1) * NQP + q] = wq * fq[c][1];
           }
 #pragma unroll
           for (int cp = 0; cp < M; ++cp) RA[SH::BQ + ((side * M + cp) * M + c) * SH::NQC + q] = wq * Aq[c][cp];
@@ -358,8 +360,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       PointOps<LAW>::vol_point(uq, d0, d1, f2, A0, A1, la);
 #pragma unroll
       for (int c = 0; c < M; ++c) {
-        S[SH::FQ + (c * 2 + 0) * NQP + q] = wq * f2[c][0];
-        S[SH::FQ + (c * 2 + 1) * NQP + q] = wq * f2[c][1];
+        RA[SH::FQ + (c * 2 + 0) * NQP + q] = wq * f2[c][0];
+        RA[SH::FQ + (c * 2 + 1) * NQP + q] = wq * f2[c][1];
 #pragma unroll
         for (int cp = 0; cp < M; ++cp) {
           RA[SH::BQ + ((0 * M + cp) * M + c) * SH::NQC + q] = wq * A0[c][cp];
@@ -374,7 +376,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       double tq[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const double f0 = S[SH::FQ + (c * 2 + 0) * NQP + q], f1 = S[SH::FQ + (c * 2 + 1) * NQP + q];
+        const double f0 = RA[SH::FQ + (c * 2 + 0) * NQP + q], f1 = RA[SH::FQ + (c * 2 + 1) * NQP + q];
         const double d0 = s_dphi[(q * NB + n) * 2 + 0], d1 = s_dphi[(q * NB + n) * 2 + 1];
         tq[0][0] = fma(d0, f0, tq[0][0]);
         tq[0][1] = fma(d0, f1, tq[0][1]);
@@ -389,7 +391,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         const int j = face_local(f, n);
         if (j >= 0)
 #pragma unroll
-          for (int s = 0; s < NS; ++s) rf = fma(T.trace[0][s][j], S[SH::HS + c * NFSP + f * NS + s], rf);
+          for (int s = 0; s < NS; ++s) rf = fma(T.trace[0][s][j], RA[SH::HS + c * NFSP + f * NS + s], rf);
       }
       S[SH::TQ + 0 * NU + i] = tq[0][0];
       S[SH::TQ + 1 * NU + i] = tq[0][1];
@@ -603,9 +605,9 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         dr[2 * b + 0] -= ry;  dr[2 * a + 0] += ry;
       }
 #pragma unroll
-      for (int d = 0; d < 6; ++d) RA[SH::DRX + i * LDX + d] = dr[d];
+      for (int d = 0; d < 6; ++d) RA[DRXo + i * LDX + d] = dr[d];
 #pragma unroll
-      for (int d = 6; d < 8; ++d) RA[SH::DRX + i * LDX + d] = 0.0;
+      for (int d = 6; d < 8; ++d) RA[DRXo + i * LDX + d] = 0.0;
     }
     __syncwarp();
     // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
@@ -631,7 +633,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         const int d = 4 * ks + (lane & 3);
         double af[3];
 #pragma unroll
-        for (int mt = 0; mt < 3; ++mt) af[mt] = RA[SH::DRX + (mt * 8 + (lane >> 2)) * LDX + d];
+        for (int mt = 0; mt < 3; ++mt) af[mt] = RA[DRXo + (mt * 8 + (lane >> 2)) * LDX + d];
         const int node = d < 6 ? EI[1 + (d >> 1)] : 0;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
@@ -773,7 +775,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     double v = 0.0;
     for (int w = 0; w < nwarps; ++w) {
       const double* Sw = smem + (size_t)w * r.gx_warp_stride;
-      const double* Hw = Sw + r.gx_warp_stride - 4 - 48 - KP * KP;
+      const double* Hw = Sw + r.gx_warp_stride - 4 - SH::gtail(KP) - KP * KP;
       const double* Gw = Hw + KP * KP;
       v += i == 0 ? Gw[K] : (i <= K ? Gw[i - 1] : Hw[i - 1 - K]);
     }

@@ -49,6 +49,12 @@ static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WS
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nwarps * 32, smem));
+  if (getenv("STROM_DEBUG")) {
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, kern));
+    fprintf(stderr, "[strom] mma kernel attrs: %d regs, %zu B static smem, max dyn %d\n", fa.numRegs, fa.sharedSizeBytes,
+            fa.maxDynamicSharedSizeBytes);
+  }
   per_sm = std::max(per_sm, 1);
   const int ngroups = (nunits + UPW - 1) / UPW;
   const int target = h->num_sms * per_sm;
@@ -92,6 +98,12 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nwarps * 32, smem));
+  if (getenv("STROM_DEBUG")) {
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, kern));
+    fprintf(stderr, "[strom] mma kernel attrs: %d regs, %zu B static smem, max dyn %d\n", fa.numRegs, fa.sharedSizeBytes,
+            fa.maxDynamicSharedSizeBytes);
+  }
   per_sm = std::max(per_sm, 1);
   const int target = h->num_sms * per_sm;
   const int maxb = std::max(1, (nunits + nwarps - 1) / nwarps);
