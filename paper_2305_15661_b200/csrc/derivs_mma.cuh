@@ -19,7 +19,7 @@ namespace strom {
 
 constexpr int MTHREADS = 256;
 #ifndef STROM_MMA_MAXNREG
-#define STROM_MMA_MAXNREG 255
+#define STROM_MMA_MAXNREG 168  // 3 warps per SMSP (12 per SM with 17 KB of smem per warp)
 #endif
 
 template <int NQ>
@@ -39,14 +39,14 @@ struct MShape {
   static constexpr int RV = RT + NU;
   static constexpr int RF = RV + NU;
   static constexpr int TQ = RF + NU;            // [4][NU]
-  static constexpr int FX = TQ + 4 * NU;        // [field][NFSP]
-  static constexpr int FD = FX + FXS * NFSP;    // face mesh-response [f][s][c][2]
+  static constexpr int FD = TQ + 4 * NU;        // face mesh-response [f][s][c][2]
   static constexpr int RA = FD + 2 * M * NFSP;
   static constexpr int LDX = 12;
   // region A (offsets from RA), by phase:
   //   P/R : BQ [q][c][kk][c'] at 0, FQ [c][i][NQP] and HS [c][NFSP] right after it
   //   L   : L [NU][LDL] at 0 once the L GEMM has read BQ (FQ / HS dead after R)
   //   P/F : CF [fs][side][c][c'] at LA       (read by the face blocks)
+  //   P/R : FX [field][NFSP] at LO           (face flux fields, read by the FD stage)
   //   F/J : one face's Lout [12][LDO] at LO  (projected right away)
   //   X/G : DRX [NU][LDX] at max(LA, NU LDJ) (CF, LOUT dead), Jt [NU][LDJ] at 0 (L dead)
   static constexpr int LDL = 28, LDO = 20;
@@ -56,11 +56,16 @@ struct MShape {
   static constexpr int LA = (HS + M * NFSP > NU * LDL ? HS + M * NFSP : NU * LDL);
   static constexpr int CF = LA;
   static constexpr int LO = LA + 32 * NFSP;
+  static constexpr int FX = LO;
+  static_assert(FXS * NFSP <= 12 * LDO, "FX overlays the one-face Lout buffer");
   __host__ __device__ static int drx(int LDJ) { return LA > NU * LDJ ? LA : NU * LDJ; }
   __host__ __device__ static int gtail(int KP) { return KP + 8; }  // gradient (K) + residual norm
+  // Gram accumulator: upper 8x8 tiles only, tile (ti <= tj) at tri_tile(ti, tj) * 64
+  __host__ __device__ static int hsize(int KP) { return (KP / 8) * (KP / 8 + 1) / 2 * 64; }
+  __host__ __device__ static constexpr int tri_tile(int ti, int tj, int nt8) { return ti * nt8 - ti * (ti - 1) / 2 + (tj - ti); }
   __host__ __device__ static int warp_stride(int LDJ, int KP) {
     const int a = LO + 12 * LDO, b = drx(LDJ) + NU * LDX;
-    const int s = RA + (a > b ? a : b) + KP * KP + gtail(KP);
+    const int s = RA + (a > b ? a : b) + hsize(KP) + gtail(KP);
     return (s + 15) / 16 * 16 + 4;
   }
 };
@@ -93,13 +98,13 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
   double* const S = smem + (size_t)warp * r.gx_warp_stride;
   double* const RA = S + SH::RA;
   const int DRXo = SH::drx(LDJ);
-  double* const HA = S + r.gx_warp_stride - 4 - SH::gtail(KP) - KP * KP;  // warp Gram accumulator (KP x KP)
-  double* const GW = HA + KP * KP;
+  double* const HA = S + r.gx_warp_stride - 4 - SH::gtail(KP) - SH::hsize(KP);  // warp Gram accumulator (upper tiles)
+  double* const GW = HA + SH::hsize(KP);
 
   for (int i = threadIdx.x; i < ku; i += blockDim.x) s_w[i] = r.w[(size_t)p * ku + i];
   for (int i = threadIdx.x; i < kx; i += blockDim.x) s_tau[i] = r.tau[(size_t)p * kx + i];
   for (int i = threadIdx.x; i < NQ * NB * 2; i += blockDim.x) s_dphi[i] = (&T.dphi[0][0][0])[i];
-  for (int i = lane; i < KP * KP; i += 32) HA[i] = 0.0;
+  for (int i = lane; i < SH::hsize(KP); i += 32) HA[i] = 0.0;
   if (threadIdx.x == 0) {
     int t = 0;
     for (int ti = 0; ti < KP / 8; ++ti)
@@ -300,7 +305,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         const bool mine = (side == 0) == in_wins;
         const double lam = in_wins ? wsi : wso;
         const double wsq = T.ws[s];
-        double* FXp = S + SH::FX;
+        double* FXp = RA + SH::FX;
         double du[M];
 #pragma unroll
         for (int c = 0; c < M; ++c) du[c] = side ? us[c] - up[c] : up[c] - us[c];
@@ -406,7 +411,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       const int fs = lane, f = fs / NS;
       const double* nh = S + SH::MNHAT + 2 * f;
       const double len = S[SH::MNLEN + f];
-      const double* FXp = S + SH::FX + fs;
+      const double* FXp = RA + SH::FX + fs;
       const double lam = FXp[(3 * M) * NFSP];
 #pragma unroll
       for (int dir = 0; dir < 2; ++dir) {  // dnu = e_x or e_y
@@ -695,7 +700,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
             for (int rs = 0; rs < NU / 4; ++rs) dmma(c0, c1, fr[ti][rs], fr[tj][rs]);
-            double* Hp = HA + (ti * 8 + (lane >> 2)) * KP + tj * 8 + 2 * (lane & 3);
+            double* Hp = HA + SH::tri_tile(ti, tj, NT8C) * 64 + (lane >> 2) * 8 + 2 * (lane & 3);
             Hp[0] = fma(rho, c0, Hp[0]);
             Hp[1] = fma(rho, c1, Hp[1]);
           }
@@ -707,7 +712,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
           const double* jb = Jt + (lane & 3) * LDJ + tj * 8 + (lane >> 2);
   #pragma unroll
           for (int rs = 0; rs < NU / 4; ++rs) dmma(c0, c1, ja[rs * 4 * LDJ], jb[rs * 4 * LDJ]);
-          double* Hp = HA + (ti * 8 + (lane >> 2)) * KP + tj * 8 + 2 * (lane & 3);
+          double* Hp = HA + t * 64 + (lane >> 2) * 8 + 2 * (lane & 3);
           Hp[0] = fma(rho, c0, Hp[0]);
           Hp[1] = fma(rho, c1, Hp[1]);
         }
@@ -715,7 +720,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       __syncwarp();
       for (int pi = lane; pi < kx * kx; pi += 32) {
         const int a = pi / kx, b = pi % kx;
-        if (a <= b) HA[(ku + a) * KP + ku + b] += rho * S[SH::DNP + a] * S[SH::DNP + b];
+        const int row = ku + a, col = ku + b;
+        if (a <= b) HA[SH::tri_tile(row >> 3, col >> 3, nt8) * 64 + (row & 7) * 8 + (col & 7)] += rho * S[SH::DNP + a] * S[SH::DNP + b];
       }
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -775,9 +781,14 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     double v = 0.0;
     for (int w = 0; w < nwarps; ++w) {
       const double* Sw = smem + (size_t)w * r.gx_warp_stride;
-      const double* Hw = Sw + r.gx_warp_stride - 4 - SH::gtail(KP) - KP * KP;
-      const double* Gw = Hw + KP * KP;
-      v += i == 0 ? Gw[K] : (i <= K ? Gw[i - 1] : Hw[i - 1 - K]);
+      const double* Hw = Sw + r.gx_warp_stride - 4 - SH::gtail(KP) - SH::hsize(KP);
+      const double* Gw = Hw + SH::hsize(KP);
+      if (i == 0) v += Gw[K];
+      else if (i <= K) v += Gw[i - 1];
+      else {
+        const int d = i - 1 - K, row = d / KP, col = d % KP;
+        if ((row >> 3) <= (col >> 3)) v += Hw[SH::tri_tile(row >> 3, col >> 3, nt8) * 64 + (row & 7) * 8 + (col & 7)];
+      }
     }
     dst[i] = v;
   }
