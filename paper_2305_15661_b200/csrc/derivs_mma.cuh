@@ -76,6 +76,15 @@ __device__ __forceinline__ int face_local(int f, int n) {
   return n == a ? 0 : (n == b ? 1 : (n == 3 + f ? 2 : -1));
 }
 
+// Row tiles of the J_U projection GEMMs pair the element nodes as {1,3}, {2,4}, {0,5}:
+// every face (nodes {f, f+1, 3+f}) then touches only two of the three 8-row tiles, and
+// tile (f+1)%3 holds none of its nodes, so the neighbor projection skips it.
+__device__ __forceinline__ int prow(int mt, int lane) {
+  const int slot = 2 * mt + (lane >> 4);
+  const int node = slot == 0 ? 1 : (slot == 1 ? 3 : (slot == 2 ? 2 : (slot == 3 ? 4 : (slot == 4 ? 0 : 5))));
+  return node * 4 + ((lane >> 2) & 3);
+}
+
 template <class LAW, int NQ, int KUT = 0, int KXT = 0>  // KUT/KXT > 0: compile-time reduced dimensions
 __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
   using SH = MShape<NQ>;
@@ -413,11 +422,12 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       const double len = S[SH::MNLEN + f];
       const double* FXp = RA + SH::FX + fs;
       const double lam = FXp[(3 * M) * NFSP];
+      const double il = 1.0 / len;
 #pragma unroll
       for (int dir = 0; dir < 2; ++dir) {  // dnu = e_x or e_y
         const double dnu0 = dir == 0 ? 1.0 : 0.0, dnu1 = dir == 0 ? 0.0 : 1.0;
         const double dlen = nh[0] * dnu0 + nh[1] * dnu1;
-        const double dnh0 = (dnu0 - nh[0] * dlen) / len, dnh1 = (dnu1 - nh[1] * dlen) / len;
+        const double dnh0 = (dnu0 - nh[0] * dlen) * il, dnh1 = (dnu1 - nh[1] * dlen) * il;
         const double dlam = FXp[(3 * M + 1) * NFSP] * dnh0 + FXp[(3 * M + 2) * NFSP] * dnh1;
         const double coef = dlam * len + lam * dlen;
 #pragma unroll
@@ -519,14 +529,16 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
 #pragma unroll
         for (int j = 0; j < NF; ++j)
 #pragma unroll
-          for (int jp = 0; jp < NF; ++jp) {
+          for (int jp = j; jp < NF; ++jp) {  // t2 is symmetric in (j, j'): one sum per pair
             double v = 0.0;
 #pragma unroll
             for (int s = 0; s < NS; ++s) v = fma(T.t2[j][jp][s], cs[s], v);
             if (side == 0) {
               RA[SH::LL + (fnode_of(PD, f, j) * M + c) * LDL + fnode_of(PD, f, jp) * M + cp] += v;
+              if (jp != j) RA[SH::LL + (fnode_of(PD, f, jp) * M + c) * LDL + fnode_of(PD, f, j) * M + cp] += v;
             } else {
               Lo[(j * M + c) * LDO + jp * M + cp] = v;
+              if (jp != j) Lo[(jp * M + c) * LDO + j * M + cp] = v;
             }
           }
       }
@@ -544,9 +556,9 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
           double af[3];
 #pragma unroll
           for (int mt = 0; mt < 3; ++mt) {
-            const int row = mt * 8 + (lane >> 2), n = row >> 2, c = row & 3;
+            const int row = prow(mt, lane), n = row >> 2, c = row & 3;
             const int j = face_local(f, n);
-            af[mt] = j >= 0 ? Lo[(j * M + c) * LDO + 4 * ks + (lane & 3)] : 0.0;
+            af[mt] = (mt != (f + 1) % 3 && j >= 0) ? Lo[(j * M + c) * LDO + 4 * ks + (lane & 3)] : 0.0;
           }
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) {
@@ -554,7 +566,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
               const int col = nt * 8 + (lane >> 2);
               const double b = pref ? pfn[f][ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phn + (size_t)brow * ku + col) : 0.0);
 #pragma unroll
-              for (int mt = 0; mt < 3; ++mt) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
+              for (int mt = 0; mt < 3; ++mt)
+                if (mt != (f + 1) % 3) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
             }
           }
         }
@@ -568,7 +581,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       for (int ks = 0; ks < 6; ++ks) {
         double af[3];
 #pragma unroll
-        for (int mt = 0; mt < 3; ++mt) af[mt] = L[(mt * 8 + (lane >> 2)) * LDL + 4 * ks + (lane & 3)];
+        for (int mt = 0; mt < 3; ++mt) af[mt] = L[prow(mt, lane) * LDL + 4 * ks + (lane & 3)];
         const int brow = 4 * ks + (lane & 3);
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
@@ -624,7 +637,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
           const int col = nt * 8 + 2 * (lane & 3) + h2;
-          if (nt < ntu && col < ku) Jt[(mt * 8 + (lane >> 2)) * LDJ + col] = ju[nt][mt][h2];
+          if (nt < ntu && col < ku) Jt[prow(mt, lane) * LDJ + col] = ju[nt][mt][h2];
         }
     {
       double jx[2][3][2];
