@@ -275,28 +275,34 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       const double* nu = S + SH::MNU + 2 * f;
       const double len = S[SH::MNLEN + f];
       const double* nh = S + SH::MNHAT + 2 * f;
-      double us[M];
+      double us[M] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int c = 0; c < M; ++c) {
-        double v = 0.0;
-#pragma unroll
-        for (int j = 0; j < NF; ++j)
-          v = fma(T.trace[0][sp][j], S[(nside ? SH::UNF + (f * NF + j) * M : SH::UE + fnode_of(PD, f, j) * M) + c], v);
-        us[c] = v;
+      for (int j = 0; j < NF; ++j) {  // node values as two 16-byte loads
+        const double2* u2 = reinterpret_cast<const double2*>(S + (nside ? SH::UNF + (f * NF + j) * M : SH::UE + fnode_of(PD, f, j) * M));
+        const double2 a = u2[0], b = u2[1];
+        const double t = T.trace[0][sp][j];
+        us[0] = fma(t, a.x, us[0]); us[1] = fma(t, a.y, us[1]); us[2] = fma(t, b.x, us[2]); us[3] = fma(t, b.y, us[3]);
       }
       if (side && bc >= 2) LAW::ghost(bc - 2, la, us);
+      // A(n) is linear in n: evaluated along sc * nu it comes out already scaled by the face
+      // weight and the LLF 1/2 (weight 1 on an extrapolated exterior, whose C_out folds into
+      // C_in since u_out == u_in there; 0 for exterior sides, which carry no state tangent)
+      const double wsq = T.ws[s];
+      const double sc = (side == 1 && bc >= 1) ? 0.0 : ((side == 0 && bc == 1) ? wsq : 0.5 * wsq);
+      const double nus[2] = {sc * nu[0], sc * nu[1]};
       double f2[M][2], A[M][M], g[M], gn[2];
-      const double ws = PointOps<LAW>::face_side(us, nu, nh, f2, A, g, gn, la);
+      const double ws = PointOps<LAW>::face_side(us, nus, nh, f2, A, g, gn, la);
       const int q = fs;
-      double uq[M];
+      double uq[M] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int c = 0; c < M; ++c) {
-        double v = 0.0;
-#pragma unroll
-        for (int n = 0; n < NB; ++n) v = fma(T.phi[q][n], S[SH::UE + n * M + c], v);
-        uq[c] = v;
+      for (int n = 0; n < NB; ++n) {
+        const double2* u2 = reinterpret_cast<const double2*>(S + SH::UE + n * M);
+        const double2 a = u2[0], b = u2[1];
+        const double t = T.phi[q][n];
+        uq[0] = fma(t, a.x, uq[0]); uq[1] = fma(t, a.y, uq[1]); uq[2] = fma(t, b.x, uq[2]); uq[3] = fma(t, b.y, uq[3]);
       }
-      const double dv[2] = {S[SH::MADJ + 2 * side], S[SH::MADJ + 2 * side + 1]};
+      const double wq = T.wq[q];  // folded into the direction: Aq comes out weighted
+      const double dv[2] = {wq * S[SH::MADJ + 2 * side], wq * S[SH::MADJ + 2 * side + 1]};
       double fq[M][2], Aq[M][M];
       PointOps<LAW>::vol_dir(uq, dv, fq, Aq, la);
       const int partner = side ? lane - NFS : (lane + NFS) & 31;
@@ -313,7 +319,6 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         const bool in_wins = wsi >= wso;  // dual.maximum tie -> first argument (dual.py:171)
         const bool mine = (side == 0) == in_wins;
         const double lam = in_wins ? wsi : wso;
-        const double wsq = T.ws[s];
         double* FXp = RA + SH::FX;
         double du[M];
 #pragma unroll
@@ -333,21 +338,21 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
           FXp[(3 * M + 1) * NFSP + fs] = gn[0];
           FXp[(3 * M + 2) * NFSP + fs] = gn[1];
         }
-        const double hl = 0.5 * lam * len;
+        // C_side = wsq (A/2 -+ lam len/2 I - len/2 du (d lam/du_side)^T); the extrapolated
+        // exterior (du = 0) adds its C_out = A/2 - lam len/2 I into C_in, exterior sides are 0
+        const bool ext0 = side == 1 && bc >= 1;
+        const double dgn = (bc == 1 || ext0) ? 0.0 : (side ? -0.5 : 0.5) * lam * len * wsq;
+        const double dsc = ext0 ? 0.0 : -0.5 * len * wsq;
+        double gm[M];
 #pragma unroll
-        for (int c = 0; c < M; ++c)
+        for (int cp = 0; cp < M; ++cp) gm[cp] = mine ? g[cp] : 0.0;
 #pragma unroll
-          for (int cp = 0; cp < M; ++cp) {
-            const double dl = mine ? g[cp] : 0.0;
-            double cv = 0.5 * A[c][cp] + (c == cp ? (side ? -hl : hl) : 0.0) - 0.5 * len * du[c] * dl;
-            if (side == 0 && bc == 1) {  // extrapolated exterior state: C_in += C_out (uo == ui, so Ao == Ai)
-              const double dlo = in_wins ? 0.0 : g[cp];
-              cv += 0.5 * A[c][cp] - (c == cp ? hl : 0.0) - 0.5 * len * du[c] * dlo;
-            }
-            if (side == 1 && bc >= 1) cv = 0.0;
-            RA[SH::CF + ((side * M + c) * M + cp) * NFSP + fs] = wsq * cv;
-          }
-        const double wq = T.wq[q];
+        for (int c = 0; c < M; ++c) {
+          const double dd = dsc * du[c];
+#pragma unroll
+          for (int cp = 0; cp < M; ++cp)
+            RA[SH::CF + ((side * M + c) * M + cp) * NFSP + fs] = fma(dd, gm[cp], A[c][cp]) + (c == cp ? dgn : 0.0);
+        }
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           if (side == 0) {
@@ -355,7 +360,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
             RA[SH::FQ + (c * 2 + 1) * NQP + q] = wq * fq[c][1];
           }
 #pragma unroll
-          for (int cp = 0; cp < M; ++cp) RA[SH::BQ + ((side * M + cp) * M + c) * SH::NQC + q] = wq * Aq[c][cp];
+          for (int cp = 0; cp < M; ++cp) RA[SH::BQ + ((side * M + cp) * M + c) * SH::NQC + q] = Aq[c][cp];
         }
       }
     }

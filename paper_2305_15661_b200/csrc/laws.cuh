@@ -208,9 +208,9 @@ struct Euler {
     A[2][0] = gk * nu[1] - vy * qn; A[2][1] = vy * nu[0] - gm * vx * nu[1];       A[2][2] = qn + vy * nu[1] - gm * vy * nu[1]; A[2][3] = gm * nu[1];
     A[3][0] = qn * (gk - H);        A[3][1] = H * nu[0] - gm * vx * qn;           A[3][2] = H * nu[1] - gm * vy * qn;           A[3][3] = g * qn;
     const double qh = vx * nh[0] + vy * nh[1];
-    const double c = sqrt(g * p / r);
+    const double c2 = g * p * ir, rc = rsqrt(c2), c = c2 * rc;  // c = sqrt(g p / r), 1/c from one rsqrt
     const double sg = qh > 0.0 ? 1.0 : (qh < 0.0 ? -1.0 : 0.0);
-    const double cf = g / (2.0 * c * r);
+    const double cf = 0.5 * g * ir * rc;  // g / (2 c r)
     dwdu[0] = sg * (-qh * ir) + cf * (gm * ke - p * ir);
     dwdu[1] = sg * nh[0] * ir - cf * gm * vx;
     dwdu[2] = sg * nh[1] * ir - cf * gm * vy;
