@@ -18,6 +18,12 @@
 namespace strom {
 
 constexpr int MTHREADS = 256;
+#ifndef STROM_RESID_MMA
+#define STROM_RESID_MMA 1  // R stage volume contraction on DMMA
+#endif
+#ifndef STROM_GFRAG
+#define STROM_GFRAG 1  // CT path: gradient partials from the J accumulators
+#endif
 #ifndef STROM_MMA_MAXNREG
 #define STROM_MMA_MAXNREG 168  // 3 warps per SMSP (12 per SM with 17 KB of smem per warp)
 #endif
@@ -43,7 +49,7 @@ struct MShape {
   static constexpr int RA = FD + 2 * M * NFSP;
   static constexpr int LDX = 12;
   // region A (offsets from RA), by phase:
-  //   P/R : BQ [q][c][kk][c'] at 0, FQ [c][i][NQP] and HS [c][NFSP] right after it
+  //   P/R : BQ [q][c][kk][c'] at 0, FQ [c][i][NQC] and HS [c][NFSP] right after it
   //   L   : L [NU][LDL] at 0 once the L GEMM has read BQ (FQ / HS dead after R)
   //   P/F : CF [fs][side][c][c'] at LA       (read by the face blocks)
   //   P/R : FX [field][NFSP] at LO           (face flux fields, read by the FD stage)
@@ -52,7 +58,7 @@ struct MShape {
   static constexpr int LDL = 28, LDO = 20;
   static constexpr int BQ = 0, LL = 0;
   static constexpr int FQ = 32 * NQC;
-  static constexpr int HS = FQ + 2 * M * NQP;
+  static constexpr int HS = FQ + 2 * M * NQC;
   static constexpr int LA = (HS + M * NFSP > NU * LDL ? HS + M * NFSP : NU * LDL);
   static constexpr int CF = LA;
   static constexpr int LO = LA + 32 * NFSP;
@@ -95,7 +101,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
   const Run& r = prm.r;
   extern __shared__ __align__(16) double smem[];
   __shared__ double s_w[KMAX], s_tau[KMAX];
-  __shared__ double s_dphi[NQ * NB * 2];
+  __shared__ __align__(16) double s_dphi[NQ * NB * 2];
   __shared__ int s_tile[15];  // upper 8x8 tiles of the Gram (KP <= 40): (ti << 4) | tj
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int p = blockIdx.y;
@@ -134,6 +140,9 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
   __syncthreads();
 
   double gacc0 = 0.0, gacc1 = 0.0, jacc = 0.0;
+  // CT path: gradient partials straight from the J accumulators (column layout of the C
+  // fragments, reduced over the lane>>2 groups once at the end), distortion part per lane
+  double gj[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}}, gx[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, gd = 0.0;
   const int nunits = r.active ? r.A : r.ne;
   const int nt8 = KP / 8, ntri = nt8 * (nt8 + 1) / 2;
   const int ntu = (ku + 7) / 8;
@@ -356,8 +365,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
 #pragma unroll
         for (int c = 0; c < M; ++c) {
           if (side == 0) {
-            RA[SH::FQ + (c * 2 + 0) * NQP + q] = wq * fq[c][0];
-            RA[SH::FQ + (c * 2 + 1) * NQP + q] = wq * fq[c][1];
+            RA[SH::FQ + (c * 2 + 0) * SH::NQC + q] = wq * fq[c][0];
+            RA[SH::FQ + (c * 2 + 1) * SH::NQC + q] = wq * fq[c][1];
           }
 #pragma unroll
           for (int cp = 0; cp < M; ++cp) RA[SH::BQ + ((side * M + cp) * M + c) * SH::NQC + q] = Aq[c][cp];
@@ -379,8 +388,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       PointOps<LAW>::vol_point(uq, d0, d1, f2, A0, A1, la);
 #pragma unroll
       for (int c = 0; c < M; ++c) {
-        RA[SH::FQ + (c * 2 + 0) * NQP + q] = wq * f2[c][0];
-        RA[SH::FQ + (c * 2 + 1) * NQP + q] = wq * f2[c][1];
+        RA[SH::FQ + (c * 2 + 0) * SH::NQC + q] = wq * f2[c][0];
+        RA[SH::FQ + (c * 2 + 1) * SH::NQC + q] = wq * f2[c][1];
 #pragma unroll
         for (int cp = 0; cp < M; ++cp) {
           RA[SH::BQ + ((0 * M + cp) * M + c) * SH::NQC + q] = wq * A0[c][cp];
@@ -390,17 +399,18 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     }
     __syncwarp();
     // ---- R: residual rows (volume / face split) and Tq ------------------------------
+#if !STROM_RESID_MMA
     if (lane < NU) {
       const int i = lane, n = i / M, c = i % M;
       double tq[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const double f0 = RA[SH::FQ + (c * 2 + 0) * NQP + q], f1 = RA[SH::FQ + (c * 2 + 1) * NQP + q];
-        const double d0 = s_dphi[(q * NB + n) * 2 + 0], d1 = s_dphi[(q * NB + n) * 2 + 1];
-        tq[0][0] = fma(d0, f0, tq[0][0]);
-        tq[0][1] = fma(d0, f1, tq[0][1]);
-        tq[1][0] = fma(d1, f0, tq[1][0]);
-        tq[1][1] = fma(d1, f1, tq[1][1]);
+        const double f0 = RA[SH::FQ + (c * 2 + 0) * SH::NQC + q], f1 = RA[SH::FQ + (c * 2 + 1) * SH::NQC + q];
+        const double2 dd = *reinterpret_cast<const double2*>(s_dphi + (q * NB + n) * 2);
+        tq[0][0] = fma(dd.x, f0, tq[0][0]);
+        tq[0][1] = fma(dd.x, f1, tq[0][1]);
+        tq[1][0] = fma(dd.y, f0, tq[1][0]);
+        tq[1][1] = fma(dd.y, f1, tq[1][1]);
       }
       const double* adj = S + SH::MADJ;
       const double rv = -(adj[0] * tq[0][0] + adj[1] * tq[0][1] + adj[2] * tq[1][0] + adj[3] * tq[1][1]);
@@ -420,6 +430,56 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       S[SH::RF + i] = rf;
       S[SH::RT + i] = rv + rf;
     }
+#else
+    // Tq[(n,j)][(c,k)] = sum_q dphi[q][n][j] FQ[(c,k)][q] on DMMA: rows (n,j) in two 8-row
+    // tiles, columns (c,k); the lane of row (n,j) holds c = lane&3, k = 0,1
+    {
+      double tc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int ks = 0; ks < SH::NQ4 / 4; ++ks) {
+        const int q = 4 * ks + (lane & 3);
+        const bool qv = q < NQ;
+        const double b = qv ? RA[SH::FQ + (lane >> 2) * SH::NQC + q] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int rw = mt * 8 + (lane >> 2);
+          const double a = (qv && rw < 2 * NB) ? s_dphi[q * 2 * NB + rw] : 0.0;
+          dmma(tc[mt][0], tc[mt][1], a, b);
+        }
+      }
+      const double* adj = S + SH::MADJ;
+      const int j = (lane >> 2) & 1, c = lane & 3;
+      double rvm[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int rw = mt * 8 + (lane >> 2), n = rw >> 1;
+        const double pj = adj[2 * j] * tc[mt][0] + adj[2 * j + 1] * tc[mt][1];
+        rvm[mt] = -(pj + __shfl_xor_sync(0xffffffffu, pj, 4));  // rows (n,0) + (n,1)
+        if (rw < 2 * NB) {
+          S[SH::TQ + (2 * j + 0) * NU + n * M + c] = tc[mt][0];
+          S[SH::TQ + (2 * j + 1) * NU + n * M + c] = tc[mt][1];
+          if (j == 0) S[SH::RV + n * M + c] = rvm[mt];
+        }
+      }
+      // row i = (n, c) of the residual: rv from the lane of row (n, 0)
+      const int src = (8 * (lane >> 2) + (lane & 3)) & 31;
+      const double rv0 = __shfl_sync(0xffffffffu, rvm[0], src), rv1 = __shfl_sync(0xffffffffu, rvm[1], src);
+      if (lane < NU) {
+        const int i = lane, n = i / M;
+        const double rv = n < 4 ? rv0 : rv1;
+        double rf = 0.0;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          const int jf = face_local(f, n);
+          if (jf >= 0)
+#pragma unroll
+            for (int s = 0; s < NS; ++s) rf = fma(T.trace[0][s][jf], RA[SH::HS + c * NFSP + f * NS + s], rf);
+        }
+        S[SH::RF + i] = rf;
+        S[SH::RT + i] = rv + rf;
+      }
+    }
+#endif
     // face responses to unit normal-vector perturbations (for the mesh tangents)
     if (lane < NFS) {
       const int fs = lane, f = fs / NS;
@@ -635,6 +695,11 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     __syncwarp();
     // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
     double* Jt = RA;
+    constexpr bool GFRAG = CT && STROM_GFRAG;  // gradient from the fragments
+    const bool gfrag = GFRAG && r.mode == MODE_DERIVS;
+    double rr[3];  // rho * R at the lane's three projection rows
+#pragma unroll
+    for (int mt = 0; mt < 3; ++mt) rr[mt] = gfrag ? rho * S[SH::RT + prow(mt, lane)] : 0.0;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -643,6 +708,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         for (int h2 = 0; h2 < 2; ++h2) {
           const int col = nt * 8 + 2 * (lane & 3) + h2;
           if (nt < ntu && col < ku) Jt[prow(mt, lane) * LDJ + col] = ju[nt][mt][h2];
+          if (GFRAG && nt < ntu) gj[nt][h2] = fma(ju[nt][mt][h2], rr[mt], gj[nt][h2]);
         }
     {
       double jx[2][3][2];
@@ -656,7 +722,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         const int d = 4 * ks + (lane & 3);
         double af[3];
 #pragma unroll
-        for (int mt = 0; mt < 3; ++mt) af[mt] = RA[DRXo + (mt * 8 + (lane >> 2)) * LDX + d];
+        for (int mt = 0; mt < 3; ++mt) af[mt] = RA[DRXo + prow(mt, lane) * LDX + d];
         const int node = d < 6 ? EI[1 + (d >> 1)] : 0;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
@@ -675,7 +741,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
             const int col = nt * 8 + 2 * (lane & 3) + h2;
-            if (col < kx) Jt[(mt * 8 + (lane >> 2)) * LDJ + ku + col] = jx[nt][mt][h2];
+            if (col < kx) Jt[prow(mt, lane) * LDJ + ku + col] = jx[nt][mt][h2];
+            if (GFRAG && nt < ntx) gx[nt][h2] = fma(jx[nt][mt][h2], rr[mt], gx[nt][h2]);
           }
       // Gram padding columns
       for (int col = K + lane; col < KP; col += 32)
@@ -689,6 +756,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
           dn = fma(S[SH::DNX + d], __ldg(r.psi + (size_t)(2 * node + (d & 1)) * kx + lane), dn);
         }
         S[SH::DNP + lane] = dn;
+        if (gfrag) gd = fma(rho * dn, S[SH::MN], gd);
       }
     }
     __syncwarp();
@@ -744,7 +812,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         const int j = lane + 32 * half;
-        if (j < K) {
+        if (!GFRAG && j < K) {
           double v = 0.0;
 #pragma unroll
           for (int i = 0; i < NU; ++i) v = fma(Jt[i * LDJ + j], S[SH::RT + i], v);
@@ -789,8 +857,32 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
   if (r.mode != MODE_DERIVS) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) jacc += __shfl_xor_sync(0xffffffffu, jacc, o);
-  if (lane < K) GW[lane] = gacc0;
-  if (lane + 32 < K) GW[lane + 32] = gacc1;
+  if constexpr (CT && STROM_GFRAG) {
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) gj[nt][h2] += __shfl_xor_sync(0xffffffffu, gj[nt][h2], o);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) gx[nt][h2] += __shfl_xor_sync(0xffffffffu, gx[nt][h2], o);
+      }
+    if (lane < 4)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          if (nt * 8 + 2 * lane + h2 < ku) GW[nt * 8 + 2 * lane + h2] = gj[nt][h2];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+          if (nt * 8 + 2 * lane + h2 < kx) GW[ku + nt * 8 + 2 * lane + h2] = gx[nt][h2];
+      }
+    __syncwarp();
+    if (lane < kx) GW[ku + lane] += gd;
+  } else {
+    if (lane < K) GW[lane] = gacc0;
+    if (lane + 32 < K) GW[lane + 32] = gacc1;
+  }
   if (lane == 0) GW[K] = jacc;
   __syncthreads();
   const int PSZ = 1 + K + KP * KP;
