@@ -44,8 +44,9 @@ struct MShape {
   static constexpr int RT = UNF + NNB;
   static constexpr int RV = RT + NU;
   static constexpr int RF = RV + NU;
-  static constexpr int TQ = RF + NU;            // [4][NU]
-  static constexpr int FD = TQ + 4 * NU;        // face mesh-response [f][s][c][2]
+  static constexpr int TQS = NU + 4;            // Tq row stride (== 12 mod 16: conflict-free fragment stores)
+  static constexpr int TQ = RF + NU;            // [4][TQS]
+  static constexpr int FD = TQ + 4 * TQS;       // face mesh-response [f][s][c][2]
   static constexpr int RA = FD + 2 * M * NFSP;
   static constexpr int LDX = 12;
   // region A (offsets from RA), by phase:
@@ -56,12 +57,15 @@ struct MShape {
   //   F/J : one face's Lout [12][LDO] at LO  (projected right away)
   //   X/G : DRX [NU][LDX] at max(LA, NU LDJ) (CF, LOUT dead), Jt [NU][LDJ] at 0 (L dead)
   static constexpr int LDL = 28, LDO = 20;
+  // the two sides of BQ / CF sit 12 mod 16 doubles apart, so the 24 point lanes (12 per
+  // side) of one store instruction hit 24 distinct banks
+  static constexpr int BQS = 16 * NQC + 12, CFS = 16 * NFSP + 12;
   static constexpr int BQ = 0, LL = 0;
-  static constexpr int FQ = 32 * NQC;
+  static constexpr int FQ = BQS + 16 * NQC;
   static constexpr int HS = FQ + 2 * M * NQC;
   static constexpr int LA = (HS + M * NFSP > NU * LDL ? HS + M * NFSP : NU * LDL);
   static constexpr int CF = LA;
-  static constexpr int LO = LA + 32 * NFSP;
+  static constexpr int LO = LA + CFS + 16 * NFSP;
   static constexpr int FX = LO;
   static_assert(FXS * NFSP <= 12 * LDO, "FX overlays the one-face Lout buffer");
   __host__ __device__ static int drx(int LDJ) { return LA > NU * LDJ ? LA : NU * LDJ; }
@@ -360,7 +364,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
           const double dd = dsc * du[c];
 #pragma unroll
           for (int cp = 0; cp < M; ++cp)
-            RA[SH::CF + ((side * M + c) * M + cp) * NFSP + fs] = fma(dd, gm[cp], A[c][cp]) + (c == cp ? dgn : 0.0);
+            RA[SH::CF + side * SH::CFS + (c * M + cp) * NFSP + fs] = fma(dd, gm[cp], A[c][cp]) + (c == cp ? dgn : 0.0);
         }
 #pragma unroll
         for (int c = 0; c < M; ++c) {
@@ -369,7 +373,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
             RA[SH::FQ + (c * 2 + 1) * SH::NQC + q] = wq * fq[c][1];
           }
 #pragma unroll
-          for (int cp = 0; cp < M; ++cp) RA[SH::BQ + ((side * M + cp) * M + c) * SH::NQC + q] = Aq[c][cp];
+          for (int cp = 0; cp < M; ++cp) RA[SH::BQ + side * SH::BQS + (cp * M + c) * SH::NQC + q] = Aq[c][cp];
         }
       }
     }
@@ -392,8 +396,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         RA[SH::FQ + (c * 2 + 1) * SH::NQC + q] = wq * f2[c][1];
 #pragma unroll
         for (int cp = 0; cp < M; ++cp) {
-          RA[SH::BQ + ((0 * M + cp) * M + c) * SH::NQC + q] = wq * A0[c][cp];
-          RA[SH::BQ + ((1 * M + cp) * M + c) * SH::NQC + q] = wq * A1[c][cp];
+          RA[SH::BQ + (cp * M + c) * SH::NQC + q] = wq * A0[c][cp];
+          RA[SH::BQ + SH::BQS + (cp * M + c) * SH::NQC + q] = wq * A1[c][cp];
         }
       }
     }
@@ -422,10 +426,10 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
 #pragma unroll
           for (int s = 0; s < NS; ++s) rf = fma(T.trace[0][s][j], RA[SH::HS + c * NFSP + f * NS + s], rf);
       }
-      S[SH::TQ + 0 * NU + i] = tq[0][0];
-      S[SH::TQ + 1 * NU + i] = tq[0][1];
-      S[SH::TQ + 2 * NU + i] = tq[1][0];
-      S[SH::TQ + 3 * NU + i] = tq[1][1];
+      S[SH::TQ + 0 * SH::TQS + i] = tq[0][0];
+      S[SH::TQ + 1 * SH::TQS + i] = tq[0][1];
+      S[SH::TQ + 2 * SH::TQS + i] = tq[1][0];
+      S[SH::TQ + 3 * SH::TQS + i] = tq[1][1];
       S[SH::RV + i] = rv;
       S[SH::RF + i] = rf;
       S[SH::RT + i] = rv + rf;
@@ -456,8 +460,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         const double pj = adj[2 * j] * tc[mt][0] + adj[2 * j + 1] * tc[mt][1];
         rvm[mt] = -(pj + __shfl_xor_sync(0xffffffffu, pj, 4));  // rows (n,0) + (n,1)
         if (rw < 2 * NB) {
-          S[SH::TQ + (2 * j + 0) * NU + n * M + c] = tc[mt][0];
-          S[SH::TQ + (2 * j + 1) * NU + n * M + c] = tc[mt][1];
+          S[SH::TQ + (2 * j + 0) * SH::TQS + n * M + c] = tc[mt][0];
+          S[SH::TQ + (2 * j + 1) * SH::TQS + n * M + c] = tc[mt][1];
           if (j == 0) S[SH::RV + n * M + c] = rvm[mt];
         }
       }
@@ -556,22 +560,30 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
           const double* B = RA + SH::BQ + c * SH::NQC + qq;
 #pragma unroll
           for (int cp = 0; cp < 4; ++cp) {
-            const double a = fma(d0, B[(0 * M + cp) * M * SH::NQC], d1 * B[(1 * M + cp) * M * SH::NQC]);
+            const double a = fma(d0, B[cp * M * SH::NQC], d1 * B[SH::BQS + cp * M * SH::NQC]);
             dmma(lv[cp][mt][0], lv[cp][mt][1], a, phib[ks]);
           }
         }
       }
       __syncwarp();  // BQ / CF reads of other lanes finished before L overwrites region A? (L lives after CF)
-      // write -L into L[(n,c)][(n',c')], n' = 2(lane&3) + {0,1}
+      // write -L into L[(n,c)][(n',c')], n' = 2(lane&3) + {0,1}: the lane's 8 values are
+      // contiguous (columns 8(lane&3) .. +7), written as four 16-byte pieces in an order
+      // rotated by (lane&3)>>1 so every quarter-warp store hits 8 distinct bank groups
+      if ((lane & 3) < 3) {
+        const bool rot = (lane & 2) != 0;
 #pragma unroll
-      for (int cp = 0; cp < 4; ++cp)
+        for (int mt = 0; mt < 3; ++mt) {
+          double2* dst = reinterpret_cast<double2*>(RA + SH::LL + (mt * 8 + (lane >> 2)) * LDL + 8 * (lane & 3));
 #pragma unroll
-        for (int mt = 0; mt < 3; ++mt)
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int np_ = 2 * (lane & 3) + h2;
-            if (np_ < NB) RA[SH::LL + (mt * 8 + (lane >> 2)) * LDL + np_ * M + cp] = -lv[cp][mt][h2];
+          for (int t = 0; t < 4; ++t) {
+            // piece pc = (t + rot) & 3 holds (h2 = pc >> 1, cp = 2 (pc & 1) + {0, 1})
+            const int pa = t, pb = (t + 1) & 3;
+            const double xa = -lv[2 * (pa & 1)][mt][pa >> 1], ya = -lv[2 * (pa & 1) + 1][mt][pa >> 1];
+            const double xb = -lv[2 * (pb & 1)][mt][pb >> 1], yb = -lv[2 * (pb & 1) + 1][mt][pb >> 1];
+            dst[rot ? pb : pa] = make_double2(rot ? xb : xa, rot ? yb : ya);
           }
+        }
+      }
     }
     __syncwarp();
     // face blocks, one face at a time: lanes 0-15 add the in-side block into L, lanes
@@ -590,7 +602,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         const int c = (lane & 15) >> 2, cp = lane & 3, side = lane >> 4;
         double cs[NS];
 #pragma unroll
-        for (int s = 0; s < NS; ++s) cs[s] = RA[SH::CF + ((side * M + c) * M + cp) * NFSP + f * NS + s];
+        for (int s = 0; s < NS; ++s) cs[s] = RA[SH::CF + side * SH::CFS + (c * M + cp) * NFSP + f * NS + s];
 #pragma unroll
         for (int j = 0; j < NF; ++j)
 #pragma unroll
@@ -663,7 +675,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     // ---- X: local mesh Jacobian dR/dx (24 x 6) -------------------------------------------
     if (lane < NU) {
       const int i = lane, n = i / M, c = i % M;
-      const double t00 = S[SH::TQ + i], t01 = S[SH::TQ + NU + i], t10 = S[SH::TQ + 2 * NU + i], t11 = S[SH::TQ + 3 * NU + i];
+      const double t00 = S[SH::TQ + i], t01 = S[SH::TQ + SH::TQS + i], t10 = S[SH::TQ + 2 * SH::TQS + i], t11 = S[SH::TQ + 3 * SH::TQS + i];
       double dr[6];
 #pragma unroll
       for (int d = 0; d < 6; ++d) {
@@ -687,10 +699,14 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         dr[2 * b + 1] += rx;  dr[2 * a + 1] -= rx;
         dr[2 * b + 0] -= ry;  dr[2 * a + 0] += ry;
       }
+      {  // 16-byte pieces, order rotated by (i>>2)&1: conflict-free quarter-warp stores
+        double2* dst = reinterpret_cast<double2*>(RA + DRXo + i * LDX);
+        const bool rot = (i & 4) != 0;
+        const double2 pc[4] = {make_double2(dr[0], dr[1]), make_double2(dr[2], dr[3]), make_double2(dr[4], dr[5]),
+                               make_double2(0.0, 0.0)};
 #pragma unroll
-      for (int d = 0; d < 6; ++d) RA[DRXo + i * LDX + d] = dr[d];
-#pragma unroll
-      for (int d = 6; d < 8; ++d) RA[DRXo + i * LDX + d] = 0.0;
+        for (int t = 0; t < 4; ++t) dst[rot ? (t + 1) & 3 : t] = rot ? pc[(t + 1) & 3] : pc[t];
+      }
     }
     __syncwarp();
     // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
@@ -700,15 +716,21 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     double rr[3];  // rho * R at the lane's three projection rows
 #pragma unroll
     for (int mt = 0; mt < 3; ++mt) rr[mt] = gfrag ? rho * S[SH::RT + prow(mt, lane)] : 0.0;
+    // fragment stores: the lane's two columns in an order flipped by jflip so the 16 lanes
+    // of a half-warp (rows c = 0..3 x column pairs k = 0..3, LDJ == 12 mod 16) never collide
+    const int jc = (lane >> 2) & 3, jk = lane & 3;
+    const int jflip = jc == 3 ? 1 : ((jc == 1 || jc == 2) ? (jk >> 1) : 0);
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int mt = 0; mt < 3; ++mt)
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
+        for (int t = 0; t < 2; ++t) {
+          const int h2 = t ^ jflip;
           const int col = nt * 8 + 2 * (lane & 3) + h2;
-          if (nt < ntu && col < ku) Jt[prow(mt, lane) * LDJ + col] = ju[nt][mt][h2];
-          if (GFRAG && nt < ntu) gj[nt][h2] = fma(ju[nt][mt][h2], rr[mt], gj[nt][h2]);
+          const double v = h2 ? ju[nt][mt][1] : ju[nt][mt][0];
+          if (nt < ntu && col < ku) Jt[prow(mt, lane) * LDJ + col] = v;
+          if (GFRAG && nt < ntu) gj[nt][t] = fma(ju[nt][mt][t], rr[mt], gj[nt][t]);
         }
     {
       double jx[2][3][2];
@@ -739,10 +761,12 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
 #pragma unroll
         for (int mt = 0; mt < 3; ++mt)
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
+          for (int t = 0; t < 2; ++t) {
+            const int h2 = t ^ jflip;
             const int col = nt * 8 + 2 * (lane & 3) + h2;
-            if (col < kx) Jt[prow(mt, lane) * LDJ + ku + col] = jx[nt][mt][h2];
-            if (GFRAG && nt < ntx) gx[nt][h2] = fma(jx[nt][mt][h2], rr[mt], gx[nt][h2]);
+            const double v = h2 ? jx[nt][mt][1] : jx[nt][mt][0];
+            if (col < kx) Jt[prow(mt, lane) * LDJ + ku + col] = v;
+            if (GFRAG && nt < ntx) gx[nt][t] = fma(jx[nt][mt][t], rr[mt], gx[nt][t]);
           }
       // Gram padding columns
       for (int col = K + lane; col < KP; col += 32)
@@ -786,9 +810,9 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
             for (int rs = 0; rs < NU / 4; ++rs) dmma(c0, c1, fr[ti][rs], fr[tj][rs]);
-            double* Hp = HA + SH::tri_tile(ti, tj, NT8C) * 64 + (lane >> 2) * 8 + 2 * (lane & 3);
-            Hp[0] = fma(rho, c0, Hp[0]);
-            Hp[1] = fma(rho, c1, Hp[1]);
+            double2* Hp = reinterpret_cast<double2*>(HA + SH::tri_tile(ti, tj, NT8C) * 64 + (lane >> 2) * 8 + 2 * (lane & 3));
+            const double2 h = *Hp;
+            *Hp = make_double2(fma(rho, c0, h.x), fma(rho, c1, h.y));
           }
       } else {
         for (int t = 0; t < ntri; ++t) {
