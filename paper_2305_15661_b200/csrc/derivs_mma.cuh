@@ -165,6 +165,10 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     if (idx0 < nunits && lane < 10) EI[lane] = index_word(r.active ? __ldg(r.active + idx0) : idx0, lane);
     __syncwarp();
   }
+  // per-lane gather roles (CT path): row lane (own row, or neighbor face 0 rows 0..7 for
+  // lanes 24..31) and row lane + 32 (neighbor rows 8..35 for lanes 0..27)
+  const int g0j = (lane - NU) >> 2;                       // lanes >= NU: face-node slot on face 0
+  const int g1i = lane + 32 - NU, g1f = g1i / (NF * M), g1j = (g1i / M) % NF;
   for (int idx = blockIdx.x * nwarps + warp; idx < nunits; idx += ustride) {
     const int e = EI[0];
     const double rho = r.active ? r.rho[idx] : 1.0;
@@ -192,25 +196,46 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         }
       }
     };
+    double Xr[6], eref = 0.0;
     if constexpr (CT && KUT % 2 == 0) {
       // both rounds' loads (and the coordinate rows) issued before any use: one memory
       // round trip for the whole gather
       constexpr int H = KUT / 2;
-      const double *src0, *src1;
-      double v0, v1;
-      row_src(lane, src0, v0);
-      row_src(lane + 32, src1, v1);
+      auto nrow = [&](int f, int jj, int c, int& ok) -> int {  // neighbor face-node row (element-major)
+        const int fi = EI[7 + f];
+        ok = (fi >> 3) == 0;
+        const int nf = fi & 3;
+        const int node = jj == 0 ? nf : (jj == 1 ? (nf == 2 ? 0 : nf + 1) : 3 + nf);
+        return EI[4 + f] * NU + node * M + c;
+      };
+      int ok0 = 1, ok1 = 0;
+      const int row0 = lane < NU ? e * NU + lane : nrow(0, g0j, lane & 3, ok0);
+      const int row1 = lane < NU + SH::NNB - 32 ? nrow(g1f, g1j, lane & 3, ok1) : 0;
+      const double* src0 = r.phi + (size_t)row0 * KUT;
+      const double* src1 = r.phi + (size_t)row1 * KUT;
+      double v0 = 0.0, v1 = 0.0;
+      if (r.u0) {
+        if (ok0) v0 = r.u0[(size_t)p * r.u0_stride + row0];
+        if (ok1) v1 = r.u0[(size_t)p * r.u0_stride + row1];
+      }
       double2 b0[H], b1[H];
 #pragma unroll
-      for (int k2 = 0; k2 < H; ++k2) b0[k2] = src0 ? __ldg(reinterpret_cast<const double2*>(src0) + k2) : make_double2(0.0, 0.0);
+      for (int k2 = 0; k2 < H; ++k2) b0[k2] = ok0 ? __ldg(reinterpret_cast<const double2*>(src0) + k2) : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int k2 = 0; k2 < H; ++k2) b1[k2] = src1 ? __ldg(reinterpret_cast<const double2*>(src1) + k2) : make_double2(0.0, 0.0);
+      for (int k2 = 0; k2 < H; ++k2) b1[k2] = ok1 ? __ldg(reinterpret_cast<const double2*>(src1) + k2) : make_double2(0.0, 0.0);
       const int lx = lane < 6 ? lane : 0;
       const int xrow = 2 * EI[1 + (lx >> 1)] + (lx & 1);
       double xv = r.xref[(size_t)p * r.x_stride + xrow];
       double pv[KXT];
 #pragma unroll
       for (int a2 = 0; a2 < KXT; ++a2) pv[a2] = __ldg(r.psi + (size_t)xrow * KXT + a2);
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {  // reference vertices, loaded with the gather (one round trip)
+        const int n = EI[1 + g];
+        Xr[2 * g] = r.nodes[2 * n];
+        Xr[2 * g + 1] = r.nodes[2 * n + 1];
+      }
+      eref = lane == 0 ? r.eta_ref[e] : 0.0;
 #pragma unroll
       for (int k2 = 0; k2 < H; ++k2) {
         v0 = fma(b0[k2].x, s_w[2 * k2], v0);
@@ -250,18 +275,18 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         }
         S[SH::UE + rr] = v;
       }
-    }
-    __syncwarp();
-    {  // element geometry (all lanes), distortion gradient (lanes 0-5), face normals (lanes 0-2)
-      double X[6];
 #pragma unroll
       for (int g = 0; g < 3; ++g) {
         const int n = EI[1 + g];
-        X[2 * g] = r.nodes[2 * n];
-        X[2 * g + 1] = r.nodes[2 * n + 1];
+        Xr[2 * g] = r.nodes[2 * n];
+        Xr[2 * g + 1] = r.nodes[2 * n + 1];
       }
+      eref = lane == 0 ? r.eta_ref[e] : 0.0;
+    }
+    __syncwarp();
+    {  // element geometry (all lanes), distortion gradient (lanes 0-5), face normals (lanes 0-2)
       Geo o;
-      element_geo(S + SH::MX, X, o);
+      element_geo(S + SH::MX, Xr, o);
       if (lane < 6) S[SH::DNX + lane] = distortion_grad_dir(o, T.wsum, r.eps, r.kappa, lane);
       if (lane < 3) face_normal(S + SH::MX, lane, S + SH::MNU + 2 * lane, S[SH::MNLEN + lane], S + SH::MNHAT + 2 * lane);
       if (lane == 0) {
@@ -271,7 +296,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         S[SH::MDET] = o.detJ;
         S[SH::MDETR] = o.detr;
         S[SH::MRHO] = rho;
-        S[SH::MN] = r.kappa * (distortion_eta(o, T.wsum, r.eps, nullptr, nullptr) - r.eta_ref[e]);
+        S[SH::MN] = r.kappa * (distortion_eta(o, T.wsum, r.eps, nullptr, nullptr) - eref);
       }
     }
     __syncwarp();
