@@ -73,9 +73,13 @@ struct MShape {
   // Gram accumulator: upper 8x8 tiles only, tile (ti <= tj) at tri_tile(ti, tj) * 64
   __host__ __device__ static int hsize(int KP) { return (KP / 8) * (KP / 8 + 1) / 2 * 64; }
   __host__ __device__ static constexpr int tri_tile(int ti, int tj, int nt8) { return ti * nt8 - ti * (ti - 1) / 2 + (tj - ti); }
-  __host__ __device__ static int warp_stride(int LDJ, int KP) {
+  // the element's six Psi rows (gathered once, read by the Jx and distortion stages),
+  // row stride == 4 mod 8 (conflict-free B fragments), just below the Gram accumulator
+  __host__ __device__ static int prs(int kx) { return (kx + 3) / 8 * 8 + 4; }
+  __host__ __device__ static int psr(int kx) { return 6 * prs(kx); }
+  __host__ __device__ static int warp_stride(int LDJ, int KP, int kx) {
     const int a = LO + 12 * LDO, b = drx(LDJ) + NU * LDX;
-    const int s = RA + (a > b ? a : b) + hsize(KP) + gtail(KP);
+    const int s = RA + (a > b ? a : b) + hsize(KP) + gtail(KP) + psr(kx);
     return (s + 15) / 16 * 16 + 4;
   }
 };
@@ -119,6 +123,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
   const int DRXo = SH::drx(LDJ);
   double* const HA = S + r.gx_warp_stride - 4 - SH::gtail(KP) - SH::hsize(KP);  // warp Gram accumulator (upper tiles)
   double* const GW = HA + SH::hsize(KP);
+  const int PRS = SH::prs(kx);
+  double* const PR = HA - SH::psr(kx);  // Psi rows of the element's vertex coordinates
 
   for (int i = threadIdx.x; i < ku; i += blockDim.x) s_w[i] = r.w[(size_t)p * ku + i];
   for (int i = threadIdx.x; i < kx; i += blockDim.x) s_tau[i] = r.tau[(size_t)p * kx + i];
@@ -229,6 +235,9 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       double pv[KXT];
 #pragma unroll
       for (int a2 = 0; a2 < KXT; ++a2) pv[a2] = __ldg(r.psi + (size_t)xrow * KXT + a2);
+      if (lane < 6)
+#pragma unroll
+        for (int a2 = 0; a2 < KXT; ++a2) PR[lane * PRS + a2] = pv[a2];
 #pragma unroll
       for (int g = 0; g < 3; ++g) {  // reference vertices, loaded with the gather (one round trip)
         const int n = EI[1 + g];
@@ -254,7 +263,11 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         const int row = 2 * n + (lane & 1);
         double v = r.xref[(size_t)p * r.x_stride + row];
         const double* ps = r.psi + (size_t)row * kx;
-        for (int a2 = 0; a2 < kx; ++a2) v = fma(ps[a2], s_tau[a2], v);
+        for (int a2 = 0; a2 < kx; ++a2) {
+          const double t = ps[a2];
+          PR[lane * PRS + a2] = t;
+          v = fma(t, s_tau[a2], v);
+        }
         S[SH::MX + lane] = v;
       }
       for (int rr = lane; rr < NU + SH::NNB; rr += 32) {
@@ -770,12 +783,11 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         double af[3];
 #pragma unroll
         for (int mt = 0; mt < 3; ++mt) af[mt] = RA[DRXo + prow(mt, lane) * LDX + d];
-        const int node = d < 6 ? EI[1 + (d >> 1)] : 0;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           if (nt < ntx) {
             const int col = nt * 8 + (lane >> 2);
-            const double b = (d < 6 && col < kx) ? __ldg(r.psi + (size_t)(2 * node + (d & 1)) * kx + col) : 0.0;
+            const double b = (d < 6 && col < kx) ? PR[d * PRS + col] : 0.0;
 #pragma unroll
             for (int mt = 0; mt < 3; ++mt) dmma(jx[nt][mt][0], jx[nt][mt][1], af[mt], b);
           }
@@ -800,10 +812,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       if (lane < kx) {
         double dn = 0.0;
 #pragma unroll
-        for (int d = 0; d < 6; ++d) {
-          const int node = EI[1 + (d >> 1)];
-          dn = fma(S[SH::DNX + d], __ldg(r.psi + (size_t)(2 * node + (d & 1)) * kx + lane), dn);
-        }
+        for (int d = 0; d < 6; ++d) dn = fma(S[SH::DNX + d], PR[d * PRS + lane], dn);
         S[SH::DNP + lane] = dn;
         if (gfrag) gd = fma(rho * dn, S[SH::MN], gd);
       }
