@@ -61,6 +61,8 @@ struct Run {
   int* __restrict__ degen_fill;
   int mode;
   const int* __restrict__ mask;  // per-row enable (batched LM), or null
+  const int* __restrict__ list;  // value_mu_kernel: compacted enabled rows (nlist of them), or null
+  int nlist;
   int U;          // units per tile (derivs kernel)
   int ntiles;     // tiles per parameter
   int gx;         // blocks per parameter

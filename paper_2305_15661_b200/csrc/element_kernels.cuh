@@ -425,21 +425,28 @@ __global__ void __launch_bounds__(128) value_mu_kernel(const __grid_constant__ P
   const Run& r = prm.r;
   __shared__ double Ws[KMAX][32], Ts[KXMAX][32], red[4][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int p = blockIdx.y * 32 + lane;
-  const bool pv = p < r.P && (!r.mask || r.mask[p]);
+  // lane -> parameter row: consecutive rows, or the compacted list of enabled rows
+  auto row_of = [&](int l) -> int {
+    const int s = blockIdx.y * 32 + l;
+    return r.list ? (s < r.nlist ? r.list[s] : r.P) : s;
+  };
+  const int p0 = row_of(0);
+  const int pr = row_of(lane);
+  const bool pv = pr < r.P && (!r.mask || r.mask[pr]);
+  const int p = pv ? pr : p0;  // idle lanes shadow a valid point (no traps, results unused)
   for (int t = threadIdx.x; t < KMAX * 32; t += blockDim.x) {
-    const int k = t / 32, l = t % 32, pp = blockIdx.y * 32 + l;
+    const int k = t / 32, l = t % 32, pp = row_of(l);
     Ws[k][l] = (k < r.ku && pp < r.P) ? r.w[(size_t)pp * r.ku + k] : 0.0;
   }
   for (int t = threadIdx.x; t < KXMAX * 32; t += blockDim.x) {
-    const int a = t / 32, l = t % 32, pp = blockIdx.y * 32 + l;
+    const int a = t / 32, l = t % 32, pp = row_of(l);
     Ts[a][l] = (a < r.kx && pp < r.P) ? r.tau[(size_t)pp * r.kx + a] : 0.0;
   }
   __syncthreads();
   LawArgs la;
   for (int i = 0; i < 8; ++i) la.p[i] = r.lawp[i];
   for (int i = 0; i < NMU; ++i) la.mu[i] = (i < r.nmu && p < r.P) ? r.mu[p * r.nmu + i] : (i < r.nmu ? r.mu[i] : 0.0);
-  const int pp = pv ? p : blockIdx.y * 32;  // idle lanes shadow a valid point (no traps, results unused)
+  const int pp = p < r.P ? p : 0;
   const int nunits = r.active ? r.A : r.ne;
   double acc = 0.0;
   for (int idx = blockIdx.x * 4 + warp; idx < nunits; idx += gridDim.x * 4) {

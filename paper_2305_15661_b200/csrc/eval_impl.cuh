@@ -175,7 +175,9 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
   }
   if (a.mode == MODE_OBJECTIVE || a.mode == MODE_RESNORM2 || a.mode == MODE_RESIDUAL) {
     const bool multi = a.P >= 8;  // many parameter points: warp per element, lanes over mu
-    const int gy = multi ? (a.P + 31) / 32 : a.P;
+    const bool listed = multi && a.list != nullptr && a.live > 0;  // lanes over the compacted enabled rows
+    if (listed) { r.list = a.list; r.nlist = a.live; }
+    const int gy = multi ? ((listed ? a.live : a.P) + 31) / 32 : a.P;
     const int gx = multi ? std::max(1, std::min((nunits + 3) / 4, (h->num_sms * 16 + gy - 1) / gy)) : (nunits + 127) / 128;
     if (a.mode != MODE_RESIDUAL) {
       if (ensure_part(h, (size_t)a.P * gx)) return -2;

@@ -47,6 +47,7 @@ struct EvalArgs {
   int* degen;
   cudaStream_t stream;
   int live = 0;  // number of unmasked rows (0 = all): sizes the grid for sparse LM rounds
+  const int* list = nullptr;  // value modes: ascending unmasked rows (compacted), `live` of them
 };
 
 }  // namespace strom_host

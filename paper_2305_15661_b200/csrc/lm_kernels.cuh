@@ -60,7 +60,8 @@ struct LmRun {
   double* tw;          // (P*LM_B, ku) trial points
   double* ttau;        // (P*LM_B, kx)
   double* tmu;         // (P*LM_B, nmu)
-  int* counters;       // [n_active, n_derivs, n_obj]
+  int* counters;       // [n_active, n_derivs, n_obj, n_obj_rows]
+  int* olist;          // (P*LM_B) compacted objective rows requested (ascending)
   double* hist;        // (P, max_iters+1, 6) or null
   double* status;      // (P, 8)
 };
@@ -150,14 +151,9 @@ static __device__ void hist_row(const LmRun& R, int p, int it, double J, double 
 
 enum LmAction { ACT_ADVANCE = 0, ACT_SOLVE_SI = 1, ACT_SOLVE_MAIN = 2, ACT_WAIT = 3 };
 
-__device__ __forceinline__ void lm_fill_main(const LmRun& R, int p, const LmState& s, double* A, double* rhs) {
-  const int K = R.K, ku = R.ku, kx = R.kx;
-  const double* Hm = R.H + (size_t)p * K * K;
-  const double* Sv = R.S + p * K;
-  for (int i = 0; i < K * K; ++i) A[i] = Hm[i];
-  for (int i = 0; i < kx; ++i) A[(ku + i) * K + ku + i] += s.lam;
-  for (int i = 0; i < K; ++i) rhs[i] = -Sv[i];
-}
+// the solve's system is filled by all threads of the block right before the solve
+// (lm_control_kernel); the state machine only decides which one (ACT_SOLVE_SI / _MAIN)
+__device__ __forceinline__ void lm_fill_main(const LmRun&, int, const LmState&, double*, double*) {}
 
 __device__ __forceinline__ void lm_request_derivs(const LmRun& R, int p, LmState& s, int phase) {
   s.phase = phase;
@@ -203,8 +199,7 @@ static __device__ int lm_advance(const LmRun& R, int p, LmState& s, double* A, d
         s.phase = PH_DONE;
         return ACT_WAIT;
       }
-      for (int i = 0; i < K; ++i) Sv[i] = d[1 + i];
-      for (int i = 0; i < K * K; ++i) Hm[i] = d[1 + K + i];
+      // (S, H) were copied from the derivatives output by the whole block
       const double Jd = d[0];
       if (s.phase == PH_SI_DERIV) {  // lm.py:134-141
         const double nSw = nrm2(Sv, ku);
@@ -213,9 +208,6 @@ static __device__ int lm_advance(const LmRun& R, int p, LmState& s, double* A, d
           lm_request_derivs(R, p, s, PH_MAIN_DERIV);
           return ACT_WAIT;
         }
-        for (int i = 0; i < ku; ++i)
-          for (int k2 = 0; k2 < ku; ++k2) A[i * ku + k2] = Hm[i * K + k2];
-        for (int i = 0; i < ku; ++i) rhs[i] = -Sv[i];
         return ACT_SOLVE_SI;
       }
       if (s.phase == PH_MAIN_DERIV) {  // lm.py:185
@@ -395,6 +387,14 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
     s_act = ACT_ADVANCE;
   }
   __syncthreads();
+  double* Sv = R.S + p * K;
+  double* Hm = R.H + (size_t)p * K * K;
+  if ((s.phase == PH_SI_DERIV || s.phase == PH_MAIN_DERIV || s.phase == PH_MAIN_ACCEPT_DERIV) && R.ddeg[p] == 0) {
+    const double* d = R.dout + (size_t)p * (1 + K + K * K);  // a finished derivatives pass -> (S, H)
+    for (int i = threadIdx.x; i < K; i += blockDim.x) Sv[i] = d[1 + i];
+    for (int i = threadIdx.x; i < K * K; i += blockDim.x) Hm[i] = d[1 + K + i];
+  }
+  __syncthreads();
   for (int guard = 0; guard < 100000; ++guard) {
     if (threadIdx.x == 0 && s_act == ACT_ADVANCE) s_act = lm_advance(R, p, s, A, rhs);
     __syncthreads();
@@ -402,6 +402,14 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
     if (act == ACT_WAIT) break;
     if (act == ACT_ADVANCE) continue;
     const int n = act == ACT_SOLVE_SI ? R.ku : K;
+    // the system: H_ww (state init, lm.py:141) or [[H_ww, H_wt], [H_wt^T, H_tt + lam I]] (lm.py:116-122)
+    const double lam = s.lam;
+    for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+      const int row = i / n, col = i % n;
+      A[i] = Hm[row * K + col] + ((act == ACT_SOLVE_MAIN && row == col && row >= R.ku) ? lam : 0.0);
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) rhs[i] = -Sv[i];
+    __syncthreads();
     const bool ok = ldlt_solve(A, n, rhs, x, &s_flag);
     if (threadIdx.x == 0) s_act = lm_after_solve(R, p, s, act, ok, x, A, rhs);
     __syncthreads();
@@ -412,6 +420,35 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
     if (R.req_d[p]) atomicAdd(&R.counters[1], 1);
     if (R.req_o[p * LM_B]) atomicAdd(&R.counters[2], 1);
   }
+}
+
+// compact the objective requests into an ascending row list (one block, deterministic)
+static __global__ void __launch_bounds__(1024) lm_compact_kernel(LmRun R) {
+  __shared__ int wsum[32];
+  const int n = R.P * LM_B, t = threadIdx.x, lane = t & 31, wp = t >> 5;
+  const int per = (n + blockDim.x - 1) / blockDim.x, lo = t * per;
+  int c = 0;
+  for (int i = lo; i < lo + per && i < n; ++i) c += R.req_o[i] != 0;
+  int x = c;  // inclusive warp scan
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wp] = x;
+  __syncthreads();
+  if (wp == 0) {
+    int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    wsum[lane] = v;
+  }
+  __syncthreads();
+  int pos = x - c + (wp > 0 ? wsum[wp - 1] : 0);
+  for (int i = lo; i < lo + per && i < n; ++i)
+    if (R.req_o[i]) R.olist[pos++] = i;
+  if (t == blockDim.x - 1) R.counters[3] = pos;
 }
 
 // results: best-iterate fallback (lm.py:266-270) and status rows
