@@ -3,6 +3,7 @@
 #include "handle.h"
 #include "derivs_warp.cuh"
 #include "derivs_mma.cuh"
+#include "value_mma.cuh"
 #include <cstdlib>
 #include <cstdio>
 
@@ -184,7 +185,12 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
       r.part = h->part;
     }
     prof_mark(h, a.stream, 0);
-    if (multi)
+    static const bool old_value = getenv("STROM_VALUE_OLD") != nullptr;
+    if (multi && h->ku <= 32 && !old_value) {
+      using VS = VShape<LAW, NB>;
+      value_mma_kernel<LAW, NB, NQ, NS><<<dim3(gy, gx), VM_THREADS, (VM_THREADS / 32) * VS::TILE * sizeof(double),
+                                           a.stream>>>(prm);
+    } else if (multi)
       value_mu_kernel<LAW, NB, NQ, NS><<<dim3(gx, gy), 128, 0, a.stream>>>(prm);
     else
       value_kernel<LAW, NB, NQ, NS><<<dim3(gx, a.P), 128, 0, a.stream>>>(prm);

@@ -160,3 +160,34 @@ def test_batched_derivatives_match_single():
         obj, _ = op.eval_batched(_lib.OBJECTIVE, torch.as_tensor(W).cuda(), torch.as_tensor(Tau).cuda(),
                                  torch.as_tensor(case.mus).cuda(), rho)
         assert abs(obj.cpu().numpy()[p] - op.objective(ReducedCoords(W[p], Tau[p]), case.mus[p], rho)) <= 1e-14 * abs(J)
+
+
+def test_value_many_points_matches_oracle_and_single_point_path():
+    """P >= 8 runs the DMMA-reconstruction value kernel (lanes over parameter points):
+    indicator vs the oracle residual norm, objectives vs the one-point kernel."""
+    from paper_2305_15661_b200 import _lib
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.greedy import indicators
+    from paper_2305_15661_b200.reduced import ReducedCoords
+
+    case = small_sector()
+    P = 40  # two point groups, the second one partial
+    rng = np.random.default_rng(11)
+    mus = rng.uniform(2.0, 4.0, (P, 1))
+    W = case.W[0] + 0.01 * rng.standard_normal((P, case.W.shape[1]))
+    Tau = 1e-3 * rng.standard_normal((P, 4))
+    op = gpu_op(case)
+    got = indicators(op, mus, W, Tau)
+    geom = OracleGeometry(case.mesh, case.maps, case.quad_order)
+    for p in (0, 17, 39):
+        U = case.phi @ W[p]
+        x = case.ref_coords + case.psi @ Tau[p]
+        ref = np.linalg.norm(assemble_residual(case.law, geom, U, x, mus[p]))
+        assert abs(got[p] - ref) <= 1e-10 * ref
+    rho = WeightVector(case.rho)
+    obj, _ = op.eval_batched(_lib.OBJECTIVE, torch.as_tensor(W).cuda(), torch.as_tensor(Tau).cuda(),
+                             torch.as_tensor(mus).cuda(), rho)
+    obj = obj.cpu().numpy()
+    for p in range(P):
+        one = op.objective(ReducedCoords(W[p], Tau[p]), mus[p], rho)
+        assert abs(obj[p] - one) <= 1e-12 * abs(one)

@@ -1,0 +1,28 @@
+"""Where the time of a batched LM solve goes (cfg3): wall vs device kernel time per kernel."""
+import os, sys, time
+import numpy as np
+import torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2305_15661_b200 import configs
+from paper_2305_15661_b200.eqp import WeightVector
+from paper_2305_15661_b200.lm import LmConfig, lm_solve_batched
+from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases
+
+which = sys.argv[1] if len(sys.argv) > 1 else "3"
+case = configs.cfg3() if which == "3" else configs.strip_case()
+op = GpuReducedOperator(case.law, case.geom, ReducedBases(case.phi, case.psi, case.ref_coords), case.dist)
+rho = WeightVector(case.rho)
+W0 = case.W[0] if which == "3" else None
+cfg = LmConfig(max_iters=30)
+lm_solve_batched(op, case.mus, W0, None, rho, cfg)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+res = lm_solve_batched(op, case.mus, W0, None, rho, cfg)
+dt = time.perf_counter() - t0
+print(f"wall {dt*1e3:.2f} ms, iters {np.mean([r.n_iters for r in res]):.1f}")
+from torch.profiler import profile, ProfilerActivity
+with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+    lm_solve_batched(op, case.mus, W0, None, rho, cfg)
+    torch.cuda.synchronize()
+print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25))
