@@ -88,19 +88,29 @@ static __device__ bool ldlt_solve(double* A, int n, double* b, double* x, int* f
     if (*flag == 0) return false;
     for (int i = j + 1 + t; i < n; i += nt) A[i * n + j] = A[i * n + j] / d;  // L[i][j]
     __syncthreads();
-    for (int i = j + 1 + t; i < n; i += nt) {
-      const double lij = A[i * n + j] * d;
-      for (int k = j + 1; k <= i; ++k) A[i * n + k] -= lij * A[k * n + j];
+    // trailing update A[i][k] -= L[i][j] d L[k][j], j < k <= i: one (i, k) entry per thread
+    // (per entry the same j-ascending update sequence as the row-wise loop)
+    const int m = n - j - 1, cnt = m * (m + 1) / 2;
+    for (int q = t; q < cnt; q += nt) {
+      // q -> (ii, kk) with 0 <= kk <= ii < m, row-major over the lower triangle
+      int ii = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+      while (ii * (ii + 1) / 2 > q) --ii;
+      while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
+      const int kk = q - ii * (ii + 1) / 2;
+      const int i = j + 1 + ii, k = j + 1 + kk;
+      A[i * n + k] -= (A[i * n + j] * d) * A[k * n + j];
     }
     __syncthreads();
   }
+  // L y = b: column sweep (per entry the same k-ascending subtraction order as the row form)
+  for (int i = 0; i < n; ++i) {
+    const double yi = b[i];
+    for (int k = i + 1 + t; k < n; k += nt) b[k] -= A[k * n + i] * yi;
+    __syncthreads();
+  }
+  for (int i = t; i < n; i += nt) x[i] = b[i] / A[i * n + i];
+  __syncthreads();
   if (t == 0) {
-    for (int i = 0; i < n; ++i) {  // L y = b
-      double v = b[i];
-      for (int k = 0; k < i; ++k) v -= A[i * n + k] * x[k];
-      x[i] = v;
-    }
-    for (int i = 0; i < n; ++i) x[i] /= A[i * n + i];
     for (int i = n - 1; i >= 0; --i) {  // L^T x = z
       double v = x[i];
       for (int k = i + 1; k < n; ++k) v -= A[k * n + i] * x[k];
@@ -387,34 +397,63 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
     s_act = ACT_ADVANCE;
   }
   __syncthreads();
-  double* Sv = R.S + p * K;
+  // the mu's vectors live in shared memory for the round: the state machine (thread 0)
+  // then works on shared copies; loads / stores of the global arrays are block-parallel
+  __shared__ double c_w[32], c_tau[KXMAX], c_dw[KMAX], c_S[KMAX], c_best[KMAX];
+  __shared__ double c_tw[LM_B * 32], c_ttau[LM_B * KXMAX], c_tmu[LM_B * NMU];
+  const int ku = R.ku, kx = R.kx, nmu = R.nmu, t = threadIdx.x, nt = blockDim.x;
   double* Hm = R.H + (size_t)p * K * K;
-  if ((s.phase == PH_SI_DERIV || s.phase == PH_MAIN_DERIV || s.phase == PH_MAIN_ACCEPT_DERIV) && R.ddeg[p] == 0) {
+  const bool dphase = (s.phase == PH_SI_DERIV || s.phase == PH_MAIN_DERIV || s.phase == PH_MAIN_ACCEPT_DERIV) && R.ddeg[p] == 0;
+  if (dphase) {
     const double* d = R.dout + (size_t)p * (1 + K + K * K);  // a finished derivatives pass -> (S, H)
-    for (int i = threadIdx.x; i < K; i += blockDim.x) Sv[i] = d[1 + i];
-    for (int i = threadIdx.x; i < K * K; i += blockDim.x) Hm[i] = d[1 + K + i];
+    for (int i = t; i < K; i += nt) c_S[i] = d[1 + i];
+    for (int i = t; i < K * K; i += nt) Hm[i] = d[1 + K + i];
+  } else {
+    for (int i = t; i < K; i += nt) c_S[i] = R.S[p * K + i];
   }
+  for (int i = t; i < ku; i += nt) c_w[i] = R.w[p * ku + i];
+  for (int i = t; i < kx; i += nt) c_tau[i] = R.tau[p * kx + i];
+  for (int i = t; i < K; i += nt) { c_dw[i] = R.dw[p * K + i]; c_best[i] = R.best_w[p * K + i]; }
+  LmRun Rl = R;  // per-mu arrays redirected to the shared copies (same indexing)
+  Rl.w = c_w - (size_t)p * ku;
+  Rl.tau = c_tau - (size_t)p * kx;
+  Rl.dw = c_dw - (size_t)p * K;
+  Rl.S = c_S - (size_t)p * K;
+  Rl.best_w = c_best - (size_t)p * K;
+  Rl.tw = c_tw - (size_t)p * LM_B * ku;
+  Rl.ttau = c_ttau - (size_t)p * LM_B * kx;
+  Rl.tmu = c_tmu - (size_t)p * LM_B * nmu;
   __syncthreads();
   for (int guard = 0; guard < 100000; ++guard) {
-    if (threadIdx.x == 0 && s_act == ACT_ADVANCE) s_act = lm_advance(R, p, s, A, rhs);
+    if (t == 0 && s_act == ACT_ADVANCE) s_act = lm_advance(Rl, p, s, A, rhs);
     __syncthreads();
     const int act = s_act;
     if (act == ACT_WAIT) break;
     if (act == ACT_ADVANCE) continue;
-    const int n = act == ACT_SOLVE_SI ? R.ku : K;
+    const int n = act == ACT_SOLVE_SI ? ku : K;
     // the system: H_ww (state init, lm.py:141) or [[H_ww, H_wt], [H_wt^T, H_tt + lam I]] (lm.py:116-122)
     const double lam = s.lam;
-    for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+    for (int i = t; i < n * n; i += nt) {
       const int row = i / n, col = i % n;
-      A[i] = Hm[row * K + col] + ((act == ACT_SOLVE_MAIN && row == col && row >= R.ku) ? lam : 0.0);
+      A[i] = Hm[row * K + col] + ((act == ACT_SOLVE_MAIN && row == col && row >= ku) ? lam : 0.0);
     }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) rhs[i] = -Sv[i];
+    for (int i = t; i < n; i += nt) rhs[i] = -c_S[i];
     __syncthreads();
     const bool ok = ldlt_solve(A, n, rhs, x, &s_flag);
-    if (threadIdx.x == 0) s_act = lm_after_solve(R, p, s, act, ok, x, A, rhs);
+    if (t == 0) s_act = lm_after_solve(Rl, p, s, act, ok, x, A, rhs);
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
+  for (int i = t; i < ku; i += nt) R.w[p * ku + i] = c_w[i];
+  for (int i = t; i < kx; i += nt) R.tau[p * kx + i] = c_tau[i];
+  for (int i = t; i < K; i += nt) { R.dw[p * K + i] = c_dw[i]; R.S[p * K + i] = c_S[i]; R.best_w[p * K + i] = c_best[i]; }
+  for (int j = 0; j < LM_B; ++j) {
+    const int row = p * LM_B + j;
+    if (!R.req_o[row]) continue;
+    for (int i = t; i < ku; i += nt) R.tw[(size_t)row * ku + i] = c_tw[j * ku + i];
+    for (int i = t; i < kx; i += nt) R.ttau[(size_t)row * kx + i] = c_ttau[j * kx + i];
+    for (int i = t; i < nmu; i += nt) R.tmu[(size_t)row * nmu + i] = c_tmu[j * nmu + i];
+  }
+  if (t == 0) {
     R.st[p] = s;
     if (s.phase != PH_DONE) atomicAdd(&R.counters[0], 1);
     if (R.req_d[p]) atomicAdd(&R.counters[1], 1);
