@@ -47,9 +47,15 @@ static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WS
   if (nwarps < 1) return fail(-1, "element group does not fit in shared memory");
   const size_t smem = nwarps * warp_bytes;
   auto kern = derivs_warp_kernel<LAW, NB, NQ, NS, TPU>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nwarps * 32, smem));
+  static size_t c_smem = 0;
+  static int c_dev = -1, c_per_sm = 0;
+  if (c_smem != smem || c_dev != h->device) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per_sm, kern, nwarps * 32, smem));
+    c_smem = smem;
+    c_dev = h->device;
+  }
+  int per_sm = c_per_sm;
   if (getenv("STROM_DEBUG")) {
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, kern));
@@ -96,9 +102,17 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
   if (nwarps < 1) return fail(-1, "element does not fit in shared memory");
   const size_t smem = nwarps * warp_bytes;
   auto kern = derivs_mma_kernel<LAW, NQ, KUT, KXT>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nwarps * 32, smem));
+  // attribute + occupancy query once per (kernel, shared-memory size, device): host API
+  // calls on every launch dominate the small LM rounds
+  static size_t c_smem = 0;
+  static int c_dev = -1, c_per_sm = 0;
+  if (c_smem != smem || c_dev != h->device) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per_sm, kern, nwarps * 32, smem));
+    c_smem = smem;
+    c_dev = h->device;
+  }
+  int per_sm = c_per_sm;
   if (getenv("STROM_DEBUG")) {
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, kern));
@@ -106,10 +120,19 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
             fa.maxDynamicSharedSizeBytes);
   }
   per_sm = std::max(per_sm, 1);
+  // k_u > 16: the larger per-warp footprint leaves too little L1 for the basis rows above
+  // 8 warps/SM (measured: cfg3/4/5 fastest at 4 two-warp CTAs per SM; cfg2 at 6)
+  if (r.ku > 16) per_sm = std::min(per_sm, 4);
+  if (const char* ev = getenv("STROM_MMA_BPS")) per_sm = std::max(1, std::min(per_sm, atoi(ev)));  // blocks/SM cap
   const int target = h->num_sms * per_sm;
   const int maxb = std::max(1, (nunits + nwarps - 1) / nwarps);
   const int live = a.live > 0 ? a.live : a.P;
-  int gx = std::max(1, std::min(maxb, (target + live - 1) / live));
+  // one wave: at most `target` co-resident CTAs (a partial second wave doubles the pass time)
+  int gx = std::max(1, std::min(maxb, target / live));
+  if (const char* ev = getenv("STROM_MMA_UPW")) {  // experiment knob: at least this many units per warp
+    const int upw = std::max(1, atoi(ev));
+    gx = std::max(1, std::min(gx, (nunits + nwarps * upw - 1) / (nwarps * upw)));
+  }
   r.gx = gx;
   r.ntiles = nunits;
   if (getenv("STROM_DEBUG"))
