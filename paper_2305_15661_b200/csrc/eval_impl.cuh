@@ -211,8 +211,13 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
     static const bool old_value = getenv("STROM_VALUE_OLD") != nullptr;
     if (multi && h->ku <= 32 && !old_value) {
       using VS = VShape<LAW, NB>;
-      value_mma_kernel<LAW, NB, NQ, NS><<<dim3(gy, gx), VM_THREADS, (VM_THREADS / 32) * VS::TILE * sizeof(double),
-                                           a.stream>>>(prm);
+      constexpr int vsmem = (VM_THREADS / 32) * VS::TILE * sizeof(double);
+      static int c_dev = -1;
+      if (c_dev != h->device) {
+        CK(cudaFuncSetAttribute(value_mma_kernel<LAW, NB, NQ, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, vsmem));
+        c_dev = h->device;
+      }
+      value_mma_kernel<LAW, NB, NQ, NS><<<dim3(gy, gx), VM_THREADS, vsmem, a.stream>>>(prm);
     } else if (multi)
       value_mu_kernel<LAW, NB, NQ, NS><<<dim3(gx, gy), 128, 0, a.stream>>>(prm);
     else

@@ -20,10 +20,13 @@ constexpr int VM_THREADS = 128;
 #define VM_NTB_OWN 4
 #endif
 #ifndef VM_NTB_F
-#define VM_NTB_F 1
+#define VM_NTB_F 4
+#endif
+#ifndef VM_USMEM
+#define VM_USMEM 1  // U and the neighbor face values read from the warp tile (no register copies)
 #endif
 #ifndef VM_MINB
-#define VM_MINB 2
+#define VM_MINB (VM_USMEM ? 3 : 2)
 #endif
 constexpr int VM_LDU = 40;  // tile row stride: == 8 mod 16 -> conflict-free double2 C-fragment stores
 constexpr int VM_LDW = 36;  // W row stride: == 4 mod 16 -> conflict-free B-fragment loads
@@ -34,7 +37,8 @@ struct VShape {
   static constexpr int NFR = NF * M;                      // one face's neighbor rows
   static constexpr int MT_OWN = (NU + 7) / 8, MT_F = (NFR + 7) / 8;
   static constexpr int MTB = MT_OWN > MT_F ? MT_OWN : MT_F;
-  static constexpr int TILE = MTB * 8 * VM_LDU;           // doubles per warp
+  static constexpr int FROW = VM_USMEM ? MT_OWN * 8 : 0;   // first face row of the tile
+  static constexpr int TILE = (VM_USMEM ? MT_OWN * 8 + MT_F * 8 : MTB * 8) * VM_LDU;  // doubles per warp
 };
 
 // rows r < nrows of the warp tile <- U0 + Phi[row(r)] . W  for the CTA's 32 points,
@@ -127,13 +131,20 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
   for (int idx = blockIdx.y * (VM_THREADS / 32) + warp; idx < nunits; idx += gridDim.y * (VM_THREADS / 32)) {
     const int e = r.active ? r.active[idx] : idx;
     const double rho = r.active ? r.rho[idx] : 1.0;
+    __syncwarp();  // the previous element's tile reads are done
     // ---- own rows
     vm_recon<VS::MT_OWN, VM_NTB_OWN>(r, Ws, tile, NU, [&](int rr) { return e * NU + rr; }, s_prow, lane);
     __syncwarp();
+#if VM_USMEM
+    const double* U = tile + lane;  // U[i * VM_LDU]
+#define VM_U(i) U[(i) * VM_LDU]
+#else
     double U[NU];
 #pragma unroll
     for (int i = 0; i < NU; ++i) U[i] = tile[i * VM_LDU + lane];
     __syncwarp();
+#define VM_U(i) U[i]
+#endif
     // ---- geometry (value_unit, element_kernels.cuh)
     double x[6], X[6];
 #pragma unroll
@@ -166,7 +177,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
       for (int c = 0; c < M; ++c) {
         double v = 0.0;
 #pragma unroll
-        for (int n = 0; n < NB; ++n) v = fma(T.phi[q][n], U[n * M + c], v);
+        for (int n = 0; n < NB; ++n) v = fma(T.phi[q][n], VM_U(n * M + c), v);
         uq[c] = v;
       }
       double f[M][2];
@@ -205,7 +216,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
       if (bc == 0) {  // warp-uniform (one element per warp)
         const int nf = fi & 3;
         flip = (fi >> 2) & 1;
-        vm_recon<VS::MT_F, VM_NTB_F>(r, Ws, tile, NFR, [&](int rr) {
+        vm_recon<VS::MT_F, VM_NTB_F>(r, Ws, tile + VS::FROW * VM_LDU, NFR, [&](int rr) {
           const int j = rr / M, c = rr % M;
           const int node = j == 0 ? nf : (j == 1 ? (nf + 1) % 3 : 3 + nf * (PD - 1) + (j - 2));
           return nb * NU + node * M + c;
@@ -214,7 +225,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
 #pragma unroll
         for (int j = 0; j < NF; ++j)
 #pragma unroll
-          for (int c = 0; c < M; ++c) Un[j][c] = tile[(j * M + c) * VM_LDU + lane];
+          for (int c = 0; c < M; ++c) Un[j][c] = tile[(VS::FROW + j * M + c) * VM_LDU + lane];
         __syncwarp();
       }
       double ghost[M];
@@ -226,7 +237,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
         for (int c = 0; c < M; ++c) {
           double v = 0.0;
 #pragma unroll
-          for (int j = 0; j < NF; ++j) v = fma(T.trace[f][s][j], U[fnode_of(PD, f, j) * M + c], v);
+          for (int j = 0; j < NF; ++j) v = fma(T.trace[f][s][j], VM_U(fnode_of(PD, f, j) * M + c), v);
           ui[c] = v;
         }
         if (bc == 0) {

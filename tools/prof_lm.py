@@ -10,11 +10,11 @@ from paper_2305_15661_b200.lm import LmConfig, lm_solve_batched
 from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases
 
 which = sys.argv[1] if len(sys.argv) > 1 else "3"
-case = configs.cfg3() if which == "3" else configs.strip_case()
+case = configs.cfg3() if which == "3" else (configs.cfg5_rom(256) if which == "5" else configs.strip_case())
 op = GpuReducedOperator(case.law, case.geom, ReducedBases(case.phi, case.psi, case.ref_coords), case.dist)
 rho = WeightVector(case.rho)
-W0 = case.W[0] if which == "3" else None
-cfg = LmConfig(max_iters=30)
+W0 = case.W[0] if which in ("3", "5") else None
+cfg = LmConfig(max_iters=10 if which == "5" else 30)
 lm_solve_batched(op, case.mus, W0, None, rho, cfg)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
