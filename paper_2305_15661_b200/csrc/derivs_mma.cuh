@@ -837,16 +837,27 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         for (int cc = 0; cc < NT8C; ++cc)
 #pragma unroll
           for (int rs = 0; rs < NU / 4; ++rs) fr[cc][rs] = Jt[(rs * 4 + (lane & 3)) * LDJ + cc * 8 + (lane >> 2)];
+        constexpr int NTRI = NT8C * (NT8C + 1) / 2;
+        double gc[NTRI][2];  // all upper tiles in flight: k-step outer, independent chains inner
+#pragma unroll
+        for (int t = 0; t < NTRI; ++t) gc[t][0] = gc[t][1] = 0.0;
+#pragma unroll
+        for (int rs = 0; rs < NU / 4; ++rs)
+#pragma unroll
+          for (int ti = 0; ti < NT8C; ++ti)
+#pragma unroll
+            for (int tj = ti; tj < NT8C; ++tj) {
+              const int t = SH::tri_tile(ti, tj, NT8C);
+              dmma(gc[t][0], gc[t][1], fr[ti][rs], fr[tj][rs]);
+            }
 #pragma unroll
         for (int ti = 0; ti < NT8C; ++ti)
 #pragma unroll
           for (int tj = ti; tj < NT8C; ++tj) {
-            double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-            for (int rs = 0; rs < NU / 4; ++rs) dmma(c0, c1, fr[ti][rs], fr[tj][rs]);
-            double2* Hp = reinterpret_cast<double2*>(HA + SH::tri_tile(ti, tj, NT8C) * 64 + (lane >> 2) * 8 + 2 * (lane & 3));
+            const int t = SH::tri_tile(ti, tj, NT8C);
+            double2* Hp = reinterpret_cast<double2*>(HA + t * 64 + (lane >> 2) * 8 + 2 * (lane & 3));
             const double2 h = *Hp;
-            *Hp = make_double2(fma(rho, c0, h.x), fma(rho, c1, h.y));
+            *Hp = make_double2(fma(rho, gc[t][0], h.x), fma(rho, gc[t][1], h.y));
           }
       } else {
         for (int t = 0; t < ntri; ++t) {

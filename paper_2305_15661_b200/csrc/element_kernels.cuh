@@ -79,7 +79,7 @@ enum { MX = 0, MJ = 6, MADJ = 10, MDET = 14, MNU = 15, MNLEN = 21, MNHAT = 24, M
 struct UnitInts { int e, nbr[3], fi[3], valid; };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
