@@ -311,7 +311,7 @@ def run_mine(args):
                    "elements": ne, "n_u": nu, "K": K, "l2": "inputs larger than L2 (Phi %.0f MB)" % (case.phi.nbytes / 1e6),
                    "parallelism": f"element-range x{world}" + (" + NCCL all_reduce of 1+K+K^2 sums" if world > 1 else "")},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "derivs_mma_kernel<Euler,12>",
+                     "traffic": traffic, "kernel": "derivs_mma_kernel<Euler,12,16,8>",
                      "flops_per_element": F, "flops_per_launch": per_launch_flops,
                      "kernel_ms_avg": kern_avg_s * 1e3, "peak_source": peak_src,
                      "hbm_bytes_per_launch": bytes_per_pass(ne, case.mesh.num_nodes, nu, ku, kx)},
