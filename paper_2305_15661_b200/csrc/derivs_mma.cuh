@@ -21,6 +21,12 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_RESID_MMA
 #define STROM_RESID_MMA 1  // R stage volume contraction on DMMA
 #endif
+#ifndef STROM_HREG
+#define STROM_HREG 1  // CT path, K <= 24: Gram accumulator in registers (fragment layout), to region A once
+#endif
+#ifndef STROM_PREF
+#define STROM_PREF 0  // prefetch the projection B fragments into registers during the L stage (measured slower)
+#endif
 #ifndef STROM_GFRAG
 #define STROM_GFRAG 1  // CT path: gradient partials from the J accumulators
 #endif
@@ -77,9 +83,13 @@ struct MShape {
   // row stride == 4 mod 8 (conflict-free B fragments), just below the Gram accumulator
   __host__ __device__ static int prs(int kx) { return (kx + 3) / 8 * 8 + 4; }
   __host__ __device__ static int psr(int kx) { return 6 * prs(kx); }
-  __host__ __device__ static int warp_stride(int LDJ, int KP, int kx) {
+  // Gram accumulator in registers: compile-time K <= 24 (six upper tiles, 12 doubles per lane)
+  __host__ __device__ static constexpr bool hreg(int KUT, int KXT) {
+    return STROM_HREG && KUT > 0 && (KUT + KXT + 7) / 8 * ((KUT + KXT + 7) / 8 + 1) / 2 <= 6;
+  }
+  __host__ __device__ static int warp_stride(int LDJ, int KP, int kx, bool hreg) {
     const int a = LO + 12 * LDO, b = drx(LDJ) + NU * LDX;
-    const int s = RA + (a > b ? a : b) + hsize(KP) + gtail(KP) + psr(kx);
+    const int s = RA + (a > b ? a : b) + (hreg ? 0 : hsize(KP)) + gtail(KP) + psr(kx);
     return (s + 15) / 16 * 16 + 4;
   }
 };
@@ -121,15 +131,22 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
   double* const S = smem + (size_t)warp * r.gx_warp_stride;
   double* const RA = S + SH::RA;
   const int DRXo = SH::drx(LDJ);
-  double* const HA = S + r.gx_warp_stride - 4 - SH::gtail(KP) - SH::hsize(KP);  // warp Gram accumulator (upper tiles)
-  double* const GW = HA + SH::hsize(KP);
+  constexpr bool HREG = SH::hreg(KUT, KXT);
+  double* const GW = S + r.gx_warp_stride - 4 - SH::gtail(KP);  // gradient + objective tail
+  // warp Gram accumulator (upper 8x8 tiles): registers + region A at the end (HREG), or smem
+  double* const HA = HREG ? S + SH::RA : GW - SH::hsize(KP);
   const int PRS = SH::prs(kx);
-  double* const PR = HA - SH::psr(kx);  // Psi rows of the element's vertex coordinates
+  double* const PR = (HREG ? GW : HA) - SH::psr(kx);  // Psi rows of the element's vertex coordinates
+  constexpr int NT8T = CT ? (KUT + KXT + 7) / 8 : 1, NTRIT = NT8T * (NT8T + 1) / 2;
+  double hacc[NTRIT][2];
+#pragma unroll
+  for (int t = 0; t < NTRIT; ++t) hacc[t][0] = hacc[t][1] = 0.0;
 
   for (int i = threadIdx.x; i < ku; i += blockDim.x) s_w[i] = r.w[(size_t)p * ku + i];
   for (int i = threadIdx.x; i < kx; i += blockDim.x) s_tau[i] = r.tau[(size_t)p * kx + i];
   for (int i = threadIdx.x; i < NQ * NB * 2; i += blockDim.x) s_dphi[i] = (&T.dphi[0][0][0])[i];
-  for (int i = lane; i < SH::hsize(KP); i += 32) HA[i] = 0.0;
+  if (!HREG)
+    for (int i = lane; i < SH::hsize(KP); i += 32) HA[i] = 0.0;
   if (threadIdx.x == 0) {
     int t = 0;
     for (int ti = 0; ti < KP / 8; ++ti)
@@ -547,7 +564,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     // prefetch the projection's B fragments (basis rows of the element and of the
     // neighbors' face nodes) so their load latency overlaps the L stage
     double pfe[6][2], pfn[3][3][2];
-    const bool pref = ntu <= 2;
+    const bool pref = STROM_PREF && ntu <= 2;
     if (pref) {
       const double* phe = r.phi + (size_t)e * NU * ku;
 #pragma unroll
@@ -855,10 +872,29 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
 #pragma unroll
           for (int tj = ti; tj < NT8C; ++tj) {
             const int t = SH::tri_tile(ti, tj, NT8C);
-            double2* Hp = reinterpret_cast<double2*>(HA + t * 64 + (lane >> 2) * 8 + 2 * (lane & 3));
-            const double2 h = *Hp;
-            *Hp = make_double2(fma(rho, gc[t][0], h.x), fma(rho, gc[t][1], h.y));
+            if constexpr (HREG) {
+              hacc[t][0] = fma(rho, gc[t][0], hacc[t][0]);
+              hacc[t][1] = fma(rho, gc[t][1], hacc[t][1]);
+            } else {
+              double2* Hp = reinterpret_cast<double2*>(HA + t * 64 + (lane >> 2) * 8 + 2 * (lane & 3));
+              const double2 h = *Hp;
+              *Hp = make_double2(fma(rho, gc[t][0], h.x), fma(rho, gc[t][1], h.y));
+            }
           }
+        if constexpr (HREG) {  // distortion term dN dN^T in the tau-tau block, row <= col
+#pragma unroll
+          for (int ti = 0; ti < NT8C; ++ti)
+#pragma unroll
+            for (int tj = ti; tj < NT8C; ++tj)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int row = ti * 8 + (lane >> 2), col = tj * 8 + 2 * (lane & 3) + h;
+                if (tj * 8 + 7 >= KUT && row >= KUT && col >= KUT && row < KT && col < KT && row <= col) {
+                  const int t = SH::tri_tile(ti, tj, NT8C);
+                  hacc[t][h] = fma(rho * S[SH::DNP + row - KUT], S[SH::DNP + col - KUT], hacc[t][h]);
+                }
+              }
+        }
       } else {
         for (int t = 0; t < ntri; ++t) {
           const int ti = s_tile[t] >> 4, tj = s_tile[t] & 15;
@@ -873,6 +909,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         }
       }
       __syncwarp();
+      if (!HREG)
       for (int pi = lane; pi < kx * kx; pi += 32) {
         const int a = pi / kx, b = pi % kx;
         const int row = ku + a, col = ku + b;
@@ -953,6 +990,11 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     if (lane + 32 < K) GW[lane + 32] = gacc1;
   }
   if (lane == 0) GW[K] = jacc;
+  if constexpr (HREG) {  // the loop is done: region A holds the warp's Gram tiles for the CTA sum
+#pragma unroll
+    for (int t = 0; t < NTRIT; ++t)
+      *reinterpret_cast<double2*>(HA + t * 64 + (lane >> 2) * 8 + 2 * (lane & 3)) = make_double2(hacc[t][0], hacc[t][1]);
+  }
   __syncthreads();
   const int PSZ = 1 + K + KP * KP;
   double* dst = r.part + ((size_t)p * gridDim.x + blockIdx.x) * PSZ;
@@ -960,8 +1002,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     double v = 0.0;
     for (int w = 0; w < nwarps; ++w) {
       const double* Sw = smem + (size_t)w * r.gx_warp_stride;
-      const double* Hw = Sw + r.gx_warp_stride - 4 - SH::gtail(KP) - SH::hsize(KP);
-      const double* Gw = Hw + SH::hsize(KP);
+      const double* Gw = Sw + r.gx_warp_stride - 4 - SH::gtail(KP);
+      const double* Hw = HREG ? Sw + SH::RA : Gw - SH::hsize(KP);
       if (i == 0) v += Gw[K];
       else if (i <= K) v += Gw[i - 1];
       else {
