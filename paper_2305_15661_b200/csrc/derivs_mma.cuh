@@ -27,6 +27,9 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_PREF
 #define STROM_PREF 0  // prefetch the projection B fragments into registers during the L stage (measured slower)
 #endif
+#ifndef STROM_PHIBUF
+#define STROM_PHIBUF 0  // k_u = 16: next element basis block copied to smem by cp.async (measured 6% slower: spills)
+#endif
 #ifndef STROM_GFRAG
 #define STROM_GFRAG 1  // CT path: gradient partials from the J accumulators
 #endif
@@ -87,9 +90,13 @@ struct MShape {
   __host__ __device__ static constexpr bool hreg(int KUT, int KXT) {
     return STROM_HREG && KUT > 0 && (KUT + KXT + 7) / 8 * ((KUT + KXT + 7) / 8 + 1) / 2 <= 6;
   }
-  __host__ __device__ static int warp_stride(int LDJ, int KP, int kx, bool hreg) {
+  // the element's basis block Phi_e (24 rows of 8 16-byte chunks; chunk c of row r at
+  // c ^ 2(r & 3): conflict-free B-fragment loads, 2-way at most for the row-wise gather)
+  static constexpr int PHS = 16;
+  __host__ __device__ static constexpr bool phibuf(int KUT) { return STROM_PHIBUF && KUT == 16; }
+  __host__ __device__ static int warp_stride(int LDJ, int KP, int kx, bool hreg, bool phib = false) {
     const int a = LO + 12 * LDO, b = drx(LDJ) + NU * LDX;
-    const int s = RA + (a > b ? a : b) + (hreg ? 0 : hsize(KP)) + gtail(KP) + psr(kx);
+    const int s = RA + (a > b ? a : b) + (hreg ? 0 : hsize(KP)) + gtail(KP) + psr(kx) + (phib ? NU * PHS : 0);
     return (s + 15) / 16 * 16 + 4;
   }
 };
@@ -137,6 +144,19 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
   double* const HA = HREG ? S + SH::RA : GW - SH::hsize(KP);
   const int PRS = SH::prs(kx);
   double* const PR = (HREG ? GW : HA) - SH::psr(kx);  // Psi rows of the element's vertex coordinates
+  constexpr bool PHB = SH::phibuf(KUT);
+  double* const PHI = PR - NU * SH::PHS;  // Phi_e block (PHB)
+  // 16-byte async copies of element ue's 24 basis rows (KUT = 16: 8 chunks per row) into PHI
+  auto phi_async = [&](int ue) {
+#pragma unroll
+    for (int i = 0; i < NU * 8 / 32; ++i) {
+      const int q = lane + 32 * i, row = q >> 3, ch = q & 7;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(PHI + row * SH::PHS + 2 * (ch ^ (2 * (row & 3))));
+      const double* src = r.phi + ((size_t)ue * NU + row) * 16 + 2 * ch;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
   constexpr int NT8T = CT ? (KUT + KXT + 7) / 8 : 1, NTRIT = NT8T * (NT8T + 1) / 2;
   double hacc[NTRIT][2];
 #pragma unroll
@@ -187,6 +207,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     const int idx0 = blockIdx.x * nwarps + warp;
     if (idx0 < nunits && lane < 10) EI[lane] = index_word(r.active ? __ldg(r.active + idx0) : idx0, lane);
     __syncwarp();
+    if (PHB && idx0 < nunits) phi_async(EI[0]);
   }
   // per-lane gather roles (CT path): row lane (own row, or neighbor face 0 rows 0..7 for
   // lanes 24..31) and row lane + 32 (neighbor rows 8..35 for lanes 0..27)
@@ -242,10 +263,22 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         if (ok1) v1 = r.u0[(size_t)p * r.u0_stride + row1];
       }
       double2 b0[H], b1[H];
+      if (!PHB || lane >= NU) {
 #pragma unroll
-      for (int k2 = 0; k2 < H; ++k2) b0[k2] = ok0 ? __ldg(reinterpret_cast<const double2*>(src0) + k2) : make_double2(0.0, 0.0);
+        for (int k2 = 0; k2 < H; ++k2) b0[k2] = ok0 ? __ldg(reinterpret_cast<const double2*>(src0) + k2) : make_double2(0.0, 0.0);
+      }
 #pragma unroll
       for (int k2 = 0; k2 < H; ++k2) b1[k2] = ok1 ? __ldg(reinterpret_cast<const double2*>(src1) + k2) : make_double2(0.0, 0.0);
+      if (PHB) {  // own rows: the block copied in by cp.async during the previous element
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+        if (lane < NU) {
+          const double2* ph2 = reinterpret_cast<const double2*>(PHI + lane * SH::PHS);
+          const int sw = 2 * (lane & 3);
+#pragma unroll
+          for (int k2 = 0; k2 < H; ++k2) b0[k2] = ph2[k2 ^ sw];
+        }
+      }
       const int lx = lane < 6 ? lane : 0;
       const int xrow = 2 * EI[1 + (lx >> 1)] + (lx & 1);
       double xv = r.xref[(size_t)p * r.x_stride + xrow];
@@ -719,7 +752,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
         for (int nt = 0; nt < 4; ++nt) {
           if (nt < ntu) {
             const int col = nt * 8 + (lane >> 2);
-            const double b = pref ? pfe[ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phe + (size_t)brow * ku + col) : 0.0);
+            const double b = PHB ? PHI[brow * SH::PHS + (((col >> 1) ^ (2 * (brow & 3))) << 1) + (col & 1)]
+                                 : (pref ? pfe[ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phe + (size_t)brow * ku + col) : 0.0));
 #pragma unroll
             for (int mt = 0; mt < 3; ++mt) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
           }
@@ -840,8 +874,12 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
       __syncwarp();
       if (nidx < nunits) {
         if (lane < 10) EI[lane] = wv;
-        const char* base = reinterpret_cast<const char*>(r.phi + (size_t)nact * NU * ku);
-        for (int off = lane * 128; off < NU * ku * 8; off += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+        if (PHB) {
+          phi_async(nact);
+        } else {
+          const char* base = reinterpret_cast<const char*>(r.phi + (size_t)nact * NU * ku);
+          for (int off = lane * 128; off < NU * ku * 8; off += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+        }
       }
     }
     // ---- G: Gram and gradient, or per-element contributions --------------------------------
