@@ -231,9 +231,12 @@ def run_mine(args):
     op = GpuReducedOperator(case.law, case.geom, bases, case.dist, device=dev, state_offset=case.state_offset)
     ku, kx = bases.k_u, bases.k_x
     K = ku + kx
-    # element range of this rank (contiguous, strong scaling)
-    lo, hi = ne * rank // world, ne * (rank + 1) // world
-    rho = None if world == 1 else WeightVector(np.where((np.arange(ne) >= lo) & (np.arange(ne) < hi), 1.0, 0.0))
+    # element range of this rank (contiguous, strong scaling); BENCH_SIM_WORLD=N runs rank 0's
+    # share of an N-GPU job on one GPU (per-rank kernel time for scaling estimates; no collective)
+    sim = int(os.environ.get("BENCH_SIM_WORLD", "0"))
+    sw, sr = (sim, 0) if (sim > 1 and world == 1) else (world, rank)
+    lo, hi = ne * sr // sw, ne * (sr + 1) // sw
+    rho = None if sw == 1 else WeightVector(np.where((np.arange(ne) >= lo) & (np.arange(ne) < hi), 1.0, 0.0))
     W = torch.zeros((1, ku), dtype=torch.float64, device=dev)
     Tau = torch.zeros((1, kx), dtype=torch.float64, device=dev)
     Mu = torch.as_tensor(case.mus, dtype=torch.float64).to(dev)

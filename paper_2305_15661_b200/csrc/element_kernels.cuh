@@ -483,28 +483,42 @@ static __global__ void sum_partials_kernel(const double* __restrict__ part, int 
   out[p] = s;
 }
 
-static __global__ void finalize_derivs_kernel(const double* __restrict__ part, int gx, int K, int KP, int P,
-                                              double* __restrict__ out, const int* __restrict__ mask) {
-  // one warp per output entry: lane-strided partial sums, then a fixed-order shuffle tree
-  // (deterministic: the same grid always sums in the same order)
+// Sum the per-CTA partials of one derivatives pass and expand the upper Gram tiles
+// into (J, S|T, H).  Block = 32 consecutive partial entries x 32 warps: warp w reads rows
+// b = w, w+32, ... as coalesced 256-byte segments, the 32 warp sums are added in a fixed
+// order (deterministic for a fixed grid), and each entry is written to the one or two
+// outputs it feeds (H symmetric).
+static __global__ void __launch_bounds__(1024) finalize_derivs_kernel(const double* __restrict__ part, int gx, int K,
+                                                                      int KP, int P, double* __restrict__ out,
+                                                                      const int* __restrict__ mask) {
+  __shared__ double red[32][33];
   const int p = blockIdx.y;
   if (mask && !mask[p]) return;
-  const int PSZ = 1 + K + KP * KP;
-  const int OSZ = 1 + K + K * K;
-  const int lane = threadIdx.x & 31;
-  const int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (o >= OSZ) return;
-  int src;
-  if (o < 1 + K) src = o;
-  else {
-    const int k = (o - 1 - K) / K, l = (o - 1 - K) % K;
-    src = 1 + K + min(k, l) * KP + max(k, l);
-  }
+  const int PSZ = 1 + K + KP * KP, OSZ = 1 + K + K * K;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int src = blockIdx.x * 32 + lane;
   double s = 0.0;
-  for (int b = lane; b < gx; b += 32) s += part[((size_t)p * gx + b) * PSZ + src];
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
-  if (lane == 0) out[(size_t)p * OSZ + o] = o == 0 ? 0.5 * s : s;
+  if (src < PSZ) {
+    const double* q = part + (size_t)p * gx * PSZ + src;
+    for (int b = w; b < gx; b += nw) s += q[(size_t)b * PSZ];
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w != 0 || src >= PSZ) return;
+  double v = red[0][lane];
+  for (int i = 1; i < nw; ++i) v += red[i][lane];
+  double* o = out + (size_t)p * OSZ;
+  if (src == 0) {
+    o[0] = 0.5 * v;
+  } else if (src <= K) {
+    o[src] = v;
+  } else {
+    const int d = src - 1 - K, k = d / KP, l = d % KP;
+    if (k <= l && l < K) {
+      o[1 + K + k * K + l] = v;
+      if (k != l) o[1 + K + l * K + k] = v;
+    }
+  }
 }
 
 }  // namespace strom

@@ -81,7 +81,8 @@ static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WS
   CK(cudaGetLastError());
   if (a.mode == MODE_DERIVS) {
     const int OSZ = 1 + r.K + r.K * r.K;
-    finalize_derivs_kernel<<<dim3((OSZ + 3) / 4, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
+    finalize_derivs_kernel<<<dim3((1 + r.K + r.KP * r.KP + 31) / 32, a.P), std::min(1024, 32 * std::max(1, std::min(32, gx))),
+                             0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
     CK(cudaGetLastError());
   }
   return 0;
@@ -149,7 +150,8 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
   CK(cudaGetLastError());
   if (a.mode == MODE_DERIVS) {
     const int OSZ = 1 + r.K + r.K * r.K;
-    finalize_derivs_kernel<<<dim3((OSZ + 3) / 4, a.P), 128, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
+    finalize_derivs_kernel<<<dim3((1 + r.K + r.KP * r.KP + 31) / 32, a.P), std::min(1024, 32 * std::max(1, std::min(32, gx))),
+                             0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
     CK(cudaGetLastError());
   }
   return 0;
