@@ -27,6 +27,12 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_PREF
 #define STROM_PREF 0  // prefetch the projection B fragments into registers during the L stage (measured slower)
 #endif
+#ifndef STROM_PREF_E
+#define STROM_PREF_E 0  // own-projection B fragments loaded before the L stage
+#endif
+#ifndef STROM_PREF_JIT
+#define STROM_PREF_JIT 0  // each face's neighbor B fragments loaded at the top of its face step
+#endif
 #ifndef STROM_PHIBUF
 #define STROM_PHIBUF 0  // k_u = 16: next element basis block copied to smem by cp.async (measured 6% slower: spills)
 #endif
@@ -598,7 +604,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     // neighbors' face nodes) so their load latency overlaps the L stage
     double pfe[6][2], pfn[3][3][2];
     const bool pref = STROM_PREF && ntu <= 2;
-    if (pref) {
+    const bool prefe = (STROM_PREF || STROM_PREF_E) && ntu <= 2;
+    if (prefe) {
       const double* phe = r.phi + (size_t)e * NU * ku;
 #pragma unroll
       for (int ks = 0; ks < 6; ++ks)
@@ -607,6 +614,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
           const int col = nt * 8 + (lane >> 2);
           pfe[ks][nt] = (nt < ntu && col < ku) ? __ldg(phe + (size_t)(4 * ks + (lane & 3)) * ku + col) : 0.0;
         }
+    }
+    if (pref) {
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
         const bool interior = (fin[f] >> 3) == 0;
@@ -686,6 +695,22 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
     double* Lo = RA + SH::LO;
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
+      double pj[3][2];  // STROM_PREF_JIT: this face's neighbor B fragments, in flight during the block sums
+      if (STROM_PREF_JIT && ntu <= 2 && (fin[f] >> 3) == 0) {
+        const int nf = fin[f] & 3;
+        const bool flip = (fin[f] >> 2) & 1;
+        const double* phn = r.phi + (size_t)nbr[f] * NU * ku;
+#pragma unroll
+        for (int ks = 0; ks < 3; ++ks) {
+          const int jn = flip ? (ks == 0 ? 1 : (ks == 1 ? 0 : 2)) : ks;
+          const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const int col = nt * 8 + (lane >> 2);
+            pj[ks][nt] = (nt < ntu && col < ku) ? __ldg(phn + (size_t)(node * M + (lane & 3)) * ku + col) : 0.0;
+          }
+        }
+      }
       {
         const int c = (lane & 15) >> 2, cp = lane & 3, side = lane >> 4;
         double cs[NS];
@@ -729,7 +754,8 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
           for (int nt = 0; nt < 4; ++nt) {
             if (nt < ntu) {
               const int col = nt * 8 + (lane >> 2);
-              const double b = pref ? pfn[f][ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phn + (size_t)brow * ku + col) : 0.0);
+              const double b = (STROM_PREF_JIT && ntu <= 2) ? pj[ks][nt < 2 ? nt : 0]
+                               : (pref ? pfn[f][ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phn + (size_t)brow * ku + col) : 0.0));
 #pragma unroll
               for (int mt = 0; mt < 3; ++mt)
                 if (mt != (f + 1) % 3) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
@@ -753,7 +779,7 @@ __global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_co
           if (nt < ntu) {
             const int col = nt * 8 + (lane >> 2);
             const double b = PHB ? PHI[brow * SH::PHS + (((col >> 1) ^ (2 * (brow & 3))) << 1) + (col & 1)]
-                                 : (pref ? pfe[ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phe + (size_t)brow * ku + col) : 0.0));
+                                 : (prefe ? pfe[ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phe + (size_t)brow * ku + col) : 0.0));
 #pragma unroll
             for (int mt = 0; mt < 3; ++mt) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
           }
