@@ -21,8 +21,14 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_RESID_MMA
 #define STROM_RESID_MMA 1  // R stage volume contraction on DMMA
 #endif
+#ifndef STROM_MMA_MAXNREG_WIDE
+#define STROM_MMA_MAXNREG_WIDE 240  // k_u > 16 runs 4 two-warp CTAs/SM (2 warps per SMSP): room for 240
+#endif
 #ifndef STROM_HREG
 #define STROM_HREG 1  // CT path, K <= 24: Gram accumulator in registers (fragment layout), to region A once
+#endif
+#ifndef STROM_HREG_WIDE
+#define STROM_HREG_WIDE 15  // k_u > 16 (240 registers): register Gram for up to 15 upper tiles (K <= 40)
 #endif
 #ifndef STROM_PREF
 #define STROM_PREF 0  // prefetch the projection B fragments into registers during the L stage (measured slower)
@@ -93,8 +99,10 @@ struct MShape {
   __host__ __device__ static int prs(int kx) { return (kx + 3) / 8 * 8 + 4; }
   __host__ __device__ static int psr(int kx) { return 6 * prs(kx); }
   // Gram accumulator in registers: compile-time K <= 24 (six upper tiles, 12 doubles per lane)
+  // k_u > 16 gets the wide register budget (measured per pass: cfg3 -10%, cfg4 -3.5%, cfg5 -6.5%)
+  __host__ __device__ static constexpr bool wide(int KUT) { return KUT > 16; }
   __host__ __device__ static constexpr bool hreg(int KUT, int KXT) {
-    return STROM_HREG && KUT > 0 && (KUT + KXT + 7) / 8 * ((KUT + KXT + 7) / 8 + 1) / 2 <= 6;
+    return STROM_HREG && KUT > 0 && (KUT + KXT + 7) / 8 * ((KUT + KXT + 7) / 8 + 1) / 2 <= (wide(KUT) ? STROM_HREG_WIDE : 6);
   }
   // the element's basis block Phi_e (24 rows of 8 16-byte chunks; chunk c of row r at
   // c ^ 2(r & 3): conflict-free B-fragment loads, 2-way at most for the row-wise gather)
@@ -123,7 +131,7 @@ __device__ __forceinline__ int prow(int mt, int lane) {
 }
 
 template <class LAW, int NQ, int KUT = 0, int KXT = 0>  // KUT/KXT > 0: compile-time reduced dimensions
-__global__ void __maxnreg__(STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
+__global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
   using SH = MShape<NQ>;
   constexpr int M = 4, NB = 6, NU = 24, NF = 3, NS = 4, NFS = 12, PD = 2;
   constexpr int NQP = SH::NQP, NFSP = SH::NFSP, LDL = SH::LDL, LDO = SH::LDO, LDX = SH::LDX;
