@@ -25,9 +25,16 @@ constexpr int VM_THREADS = 128;
 #ifndef VM_USMEM
 #define VM_USMEM 1  // U and the neighbor face values read from the warp tile (no register copies)
 #endif
+#ifndef VM_UQ
+#define VM_UQ 1  // volume-point loop unroll
+#endif
+#ifndef VM_US
+#define VM_US 1  // face-point loop unroll
+#endif
 #ifndef VM_MINB
 #define VM_MINB (VM_USMEM ? 3 : 2)
 #endif
+constexpr int kVmUq = VM_UQ, kVmUs = VM_US;
 constexpr int VM_LDU = 40;  // tile row stride: == 8 mod 16 -> conflict-free double2 C-fragment stores
 constexpr int VM_LDW = 36;  // W row stride: == 4 mod 16 -> conflict-free B-fragment loads
 
@@ -170,7 +177,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
 #pragma unroll
     for (int i = 0; i < NU; ++i) R[i] = 0.0;
     // ---- volume (dg.py:105-125)
-#pragma unroll 1
+#pragma unroll kVmUq
     for (int q = 0; q < NQ; ++q) {
       double uq[M];
 #pragma unroll
@@ -230,7 +237,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
       }
       double ghost[M];
       if (bc >= 2) LAW::ghost(bc - 2, la, ghost);
-#pragma unroll 1
+#pragma unroll kVmUs
       for (int s = 0; s < NS; ++s) {
         double ui[M], uo[M];
 #pragma unroll
