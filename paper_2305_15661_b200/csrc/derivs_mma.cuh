@@ -905,7 +905,6 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     __syncwarp();
     {  // next unit: index block into smem, L2 prefetch of its basis block (3 KB at k_u = 16).
       // (prefetching the neighbor rows, U0, Psi and coordinates too measured 4-9% slower)
-      __syncwarp();
       if (nidx < nunits) {
         if (lane < 10) EI[lane] = wv;
         if (PHB) {
