@@ -24,6 +24,9 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_MMA_MAXNREG_WIDE
 #define STROM_MMA_MAXNREG_WIDE 240  // k_u > 16 runs 4 two-warp CTAs/SM (2 warps per SMSP): room for 240
 #endif
+#ifndef STROM_FACE3
+#define STROM_FACE3 0  // all three faces buffered (block sums, one barrier, projections): 4% slower on cfg2
+#endif
 #ifndef STROM_HREG
 #define STROM_HREG 1  // CT path, K <= 24: Gram accumulator in registers (fragment layout), to region A once
 #endif
@@ -77,7 +80,8 @@ struct MShape {
   //   P/R : FX [field][NFSP] at LO           (face flux fields, read by the FD stage)
   //   F/J : one face's Lout [12][LDO] at LO  (projected right away)
   //   X/G : DRX [NU][LDX] at max(LA, NU LDJ) (CF, LOUT dead), Jt [NU][LDJ] at 0 (L dead)
-  static constexpr int LDL = 28, LDO = 20;
+  static constexpr int LDL = 28, LDO = STROM_FACE3 ? 12 : 20;  // LDO == 12 mod 16: conflict-free too
+  static constexpr int NLO = STROM_FACE3 ? 3 : 1;               // out-block buffers (faces)
   // the two sides of BQ / CF sit 12 mod 16 doubles apart, so the 24 point lanes (12 per
   // side) of one store instruction hit 24 distinct banks
   static constexpr int BQS = 16 * NQC + 12, CFS = 16 * NFSP + 12;
@@ -88,7 +92,7 @@ struct MShape {
   static constexpr int CF = LA;
   static constexpr int LO = LA + CFS + 16 * NFSP;
   static constexpr int FX = LO;
-  static_assert(FXS * NFSP <= 12 * LDO, "FX overlays the one-face Lout buffer");
+  static_assert(FXS * NFSP <= NLO * 12 * LDO, "FX overlays the Lout buffers");
   __host__ __device__ static int drx(int LDJ) { return LA > NU * LDJ ? LA : NU * LDJ; }
   __host__ __device__ static int gtail(int KP) { return KP + 8; }  // gradient (K) + residual norm
   // Gram accumulator: upper 8x8 tiles only, tile (ti <= tj) at tri_tile(ti, tj) * 64
@@ -109,7 +113,7 @@ struct MShape {
   static constexpr int PHS = 16;
   __host__ __device__ static constexpr bool phibuf(int KUT) { return STROM_PHIBUF && KUT == 16; }
   __host__ __device__ static int warp_stride(int LDJ, int KP, int kx, bool hreg, bool phib = false) {
-    const int a = LO + 12 * LDO, b = drx(LDJ) + NU * LDX;
+    const int a = LO + NLO * 12 * LDO, b = drx(LDJ) + NU * LDX;
     const int s = RA + (a > b ? a : b) + (hreg ? 0 : hsize(KP)) + gtail(KP) + psr(kx) + (phib ? NU * PHS : 0);
     return (s + 15) / 16 * 16 + 4;
   }
@@ -701,6 +705,66 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       for (int mt = 0; mt < 3; ++mt) ju[nt][mt][0] = ju[nt][mt][1] = 0.0;
     const double* L = RA + SH::LL;
     double* Lo = RA + SH::LO;
+#if STROM_FACE3
+    // all faces' block sums first (in-blocks into L, out-blocks into three buffers), one
+    // barrier, then every face's projection on the neighbor's face-node rows
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      const int c = (lane & 15) >> 2, cp = lane & 3, side = lane >> 4;
+      double* Lof = Lo + f * 12 * LDO;
+      double cs[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) cs[s] = RA[SH::CF + side * SH::CFS + (c * M + cp) * NFSP + f * NS + s];
+#pragma unroll
+      for (int j = 0; j < NF; ++j)
+#pragma unroll
+        for (int jp = j; jp < NF; ++jp) {  // t2 is symmetric in (j, j'): one sum per pair
+          double v = 0.0;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) v = fma(T.t2[j][jp][s], cs[s], v);
+          if (side == 0) {
+            RA[SH::LL + (fnode_of(PD, f, j) * M + c) * LDL + fnode_of(PD, f, jp) * M + cp] += v;
+            if (jp != j) RA[SH::LL + (fnode_of(PD, f, jp) * M + c) * LDL + fnode_of(PD, f, j) * M + cp] += v;
+          } else {
+            Lof[(j * M + c) * LDO + jp * M + cp] = v;
+            if (jp != j) Lof[(jp * M + c) * LDO + j * M + cp] = v;
+          }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      if ((fin[f] >> 3) == 0) {
+        const double* Lof = Lo + f * 12 * LDO;
+        const int nf = fin[f] & 3;
+        const bool flip = (fin[f] >> 2) & 1;
+        const double* phn = r.phi + (size_t)nbr[f] * NU * ku;
+#pragma unroll
+        for (int ks = 0; ks < 3; ++ks) {  // k = (j', c') = 4 ks + lane&3 -> j' = ks
+          const int jn = flip ? (ks == 0 ? 1 : (ks == 1 ? 0 : 2)) : ks;
+          const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
+          const int brow = node * M + (lane & 3);
+          double af[3];
+#pragma unroll
+          for (int mt = 0; mt < 3; ++mt) {
+            const int row = prow(mt, lane), n = row >> 2, c = row & 3;
+            const int j = face_local(f, n);
+            af[mt] = (mt != (f + 1) % 3 && j >= 0) ? Lof[(j * M + c) * LDO + 4 * ks + (lane & 3)] : 0.0;
+          }
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            if (nt < ntu) {
+              const int col = nt * 8 + (lane >> 2);
+              const double b = col < ku ? __ldg(phn + (size_t)brow * ku + col) : 0.0;
+#pragma unroll
+              for (int mt = 0; mt < 3; ++mt)
+                if (mt != (f + 1) % 3) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
+            }
+          }
+        }
+      }
+    }
+#else
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
       double pj[3][2];  // STROM_PREF_JIT: this face's neighbor B fragments, in flight during the block sums
@@ -773,6 +837,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       }
       __syncwarp();  // Lout_f consumed before the next face overwrites it
     }
+#endif
     // ---- J: own-state projection J_U += L Phi_e on DMMA ----------------------------------
     {
       const double* phe = r.phi + (size_t)e * NU * ku;
