@@ -42,6 +42,7 @@ struct LmState {
 
 struct LmRun {
   int P, ku, kx, K, nmu;
+  int ran_d, ran_o;  // whether the previous round ran the derivatives / objective pass
   LmCfg cfg;
   LmState* st;
   double* w;        // (P, ku) current
@@ -390,13 +391,28 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
   double* x = rhs + K;
   __shared__ int s_act, s_flag;
   __shared__ LmState s;
+  __shared__ int s_hold;
   if (threadIdx.x == 0) {
     s = R.st[p];
-    R.req_d[p] = 0;
-    for (int j = 0; j < LM_B; ++j) R.req_o[p * LM_B + j] = 0;
+    // a request the host deferred last round stays posted; the mu waits (no state change)
+    const bool wd = s.phase == PH_SI_DERIV || s.phase == PH_MAIN_DERIV || s.phase == PH_MAIN_ACCEPT_DERIV;
+    const bool wo = s.phase == PH_SI_BASEJ || s.phase == PH_SI_LS || s.phase == PH_MAIN_LS;
+    s_hold = (wd && !R.ran_d) || (wo && !R.ran_o);
+    if (!s_hold) {
+      R.req_d[p] = 0;
+      for (int j = 0; j < LM_B; ++j) R.req_o[p * LM_B + j] = 0;
+    }
     s_act = ACT_ADVANCE;
   }
   __syncthreads();
+  if (s_hold) {
+    if (threadIdx.x == 0) {
+      atomicAdd(&R.counters[0], 1);
+      if (R.req_d[p]) atomicAdd(&R.counters[1], 1);
+      if (R.req_o[p * LM_B]) atomicAdd(&R.counters[2], 1);
+    }
+    return;
+  }
   // the mu's vectors live in shared memory for the round: the state machine (thread 0)
   // then works on shared copies; loads / stores of the global arrays are block-parallel
   __shared__ double c_w[32], c_tau[KXMAX], c_dw[KMAX], c_S[KMAX], c_best[KMAX];

@@ -80,7 +80,7 @@ def cfg3(max_iters):
     t_o = cuda_time(lambda: op.eval_batched(_lib.OBJECTIVE, W, Tau, Mu, rho, out=outo), 5)
     units = 800 * 64
     cfg = LmConfig(max_iters=max_iters)
-    lm_solve_batched(op, case.mus[:4], case.W[0], None, rho, LmConfig(max_iters=2))
+    lm_solve_batched(op, case.mus, case.W[0], None, rho, LmConfig(max_iters=2))  # workspace for all 64 mu
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = lm_solve_batched(op, case.mus, case.W[0], None, rho, cfg)
@@ -130,7 +130,7 @@ def cfg5(P, max_iters):
     from paper_2305_15661_b200.greedy import indicators, local_argmax
 
     cfg = LmConfig(max_iters=max_iters)
-    lm_solve_batched(op, case.mus[:8], case.W[0], None, rho, LmConfig(max_iters=2))
+    lm_solve_batched(op, case.mus, case.W[0], None, rho, LmConfig(max_iters=1))  # workspace for all P
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = lm_solve_batched(op, case.mus, case.W[0], None, rho, cfg)
