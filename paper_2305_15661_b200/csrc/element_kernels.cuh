@@ -474,13 +474,16 @@ __global__ void __launch_bounds__(128) value_mu_kernel(const __grid_constant__ P
   if (warp == 0 && pv) r.part[(size_t)p * gridDim.x + blockIdx.x] = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
 }
 
+// one warp per parameter row: lane-strided partials, fixed-order shuffle tree (deterministic)
 static __global__ void sum_partials_kernel(const double* __restrict__ part, int nparts, int P, double* __restrict__ out,
                                     const int* __restrict__ mask) {
-  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (p >= P || (mask && !mask[p])) return;
   double s = 0.0;
-  for (int i = 0; i < nparts; ++i) s += part[(size_t)p * nparts + i];
-  out[p] = s;
+  for (int i = lane; i < nparts; i += 32) s += part[(size_t)p * nparts + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) out[p] = s;
 }
 
 // Sum the per-CTA partials of one derivatives pass and expand the upper Gram tiles

@@ -227,7 +227,7 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
     prof_mark(h, a.stream, 1);
     CK(cudaGetLastError());
     if (a.mode != MODE_RESIDUAL) {
-      sum_partials_kernel<<<(a.P + 127) / 128, 128, 0, a.stream>>>(h->part, gx, a.P, a.out, a.mask);
+      sum_partials_kernel<<<(a.P + 3) / 4, 128, 0, a.stream>>>(h->part, gx, a.P, a.out, a.mask);
       CK(cudaGetLastError());
     }
     return 0;
