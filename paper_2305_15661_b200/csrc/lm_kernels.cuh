@@ -61,7 +61,9 @@ struct LmRun {
   double* tw;          // (P*LM_B, ku) trial points
   double* ttau;        // (P*LM_B, kx)
   double* tmu;         // (P*LM_B, nmu)
-  int* counters;       // [n_active, n_derivs, n_obj, n_obj_rows]
+  int* counters;       // [n_active, n_derivs, n_obj, n_obj_rows] of this round
+  int* counters_next;  // next round's set, zeroed by this round's control kernel
+  int* degen_fill;     // the evaluation kernels' degenerate-list fill counter (zeroed per round)
   int* olist;          // (P*LM_B) compacted objective rows requested (ascending)
   double* hist;        // (P, max_iters+1, 6) or null
   double* status;      // (P, 8)
@@ -392,6 +394,7 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
   __shared__ int s_act, s_flag;
   __shared__ LmState s;
   __shared__ int s_hold;
+  if (blockIdx.x == 0 && threadIdx.x < 4) R.counters_next[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     s = R.st[p];
     // a request the host deferred last round stays posted; the mu waits (no state change)
@@ -474,6 +477,10 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
     if (s.phase != PH_DONE) atomicAdd(&R.counters[0], 1);
     if (R.req_d[p]) atomicAdd(&R.counters[1], 1);
     if (R.req_o[p * LM_B]) atomicAdd(&R.counters[2], 1);
+    // degenerate flags of the evaluations requested now start at zero (read next round)
+    if (R.req_d[p]) const_cast<int*>(R.ddeg)[p] = 0;
+    for (int j = 0; j < LM_B; ++j)
+      if (R.req_o[p * LM_B + j]) const_cast<int*>(R.odeg)[p * LM_B + j] = 0;
   }
 }
 
@@ -503,7 +510,10 @@ static __global__ void __launch_bounds__(1024) lm_compact_kernel(LmRun R) {
   int pos = x - c + (wp > 0 ? wsum[wp - 1] : 0);
   for (int i = lo; i < lo + per && i < n; ++i)
     if (R.req_o[i]) R.olist[pos++] = i;
-  if (t == blockDim.x - 1) R.counters[3] = pos;
+  if (t == blockDim.x - 1) {
+    R.counters[3] = pos;
+    *R.degen_fill = 0;
+  }
 }
 
 // results: best-iterate fallback (lm.py:266-270) and status rows
