@@ -36,6 +36,7 @@ struct LmCfg {
 
 struct LmState {
   int phase, it, si_cnt, attempts, j0, done, reason, n_done, nhist, have_best, lam_set, si_have_J, evals;
+  int ntr;  // trials posted in the current batch (first batch of a line search: nb_first)
   double lam, lam_floor, J, J_si, gdot, J_new, alpha, si_target, nS_prev, nT_prev, J_prev;
   double best_J, best_nS, best_nT;
 };
@@ -43,6 +44,7 @@ struct LmState {
 struct LmRun {
   int P, ku, kx, K, nmu;
   int ran_d, ran_o;  // whether the previous round ran the derivatives / objective pass
+  int nb_first;      // trials in the first batch of a line search (1..LM_B); later batches LM_B
   LmCfg cfg;
   LmState* st;
   double* w;        // (P, ku) current
@@ -143,6 +145,7 @@ static __global__ void lm_init_kernel(LmRun R, const double* w0, const double* t
 
 // post objective trials at w + alpha_j dw (state init: tau frozen, dz = dw only)
 static __device__ void post_trials(const LmRun& R, int p, int j0, bool frozen_tau, int ntr) {
+  ntr = min(ntr, LM_B);
   for (int j = 0; j < LM_B; ++j) {
     const int row = p * LM_B + j;
     const bool on = j < ntr;
@@ -250,14 +253,15 @@ static __device__ int lm_advance(const LmRun& R, int p, LmState& s, double* A, d
       s.si_have_J = 1;
       s.j0 = 0;
       s.phase = PH_SI_LS;
-      post_trials(R, p, 0, true, LM_B);
+      s.ntr = R.nb_first;
+      post_trials(R, p, 0, true, s.ntr);
       s.evals++;
       return ACT_WAIT;
     }
     case PH_SI_LS: {  // Armijo on the frozen-tau state step (lm.py:147-160)
       double sdw = 0.0;
       for (int i = 0; i < ku; ++i) sdw = fma(Sv[i], R.dw[p * K + i], sdw);
-      for (int j = 0; j < LM_B && s.j0 + j < 30; ++j) {
+      for (int j = 0; j < s.ntr && s.j0 + j < 30; ++j) {
         const int row = p * LM_B + j;
         const double Jt = R.odeg[row] > 0 ? INFINITY : R.oout[row];
         const double alpha = ldexp(1.0, -(s.j0 + j));
@@ -269,9 +273,10 @@ static __device__ int lm_advance(const LmRun& R, int p, LmState& s, double* A, d
           return ACT_WAIT;
         }
       }
-      if (s.j0 + LM_B < 30) {
-        s.j0 += LM_B;
-        post_trials(R, p, s.j0, true, min(LM_B, 30 - s.j0));
+      if (s.j0 + s.ntr < 30) {
+        s.j0 += s.ntr;
+        s.ntr = min(LM_B, 30 - s.j0);
+        post_trials(R, p, s.j0, true, s.ntr);
         s.evals++;
         return ACT_WAIT;
       }
@@ -317,7 +322,7 @@ static __device__ int lm_advance(const LmRun& R, int p, LmState& s, double* A, d
       return ACT_SOLVE_MAIN;
     }
     case PH_MAIN_LS: {  // Armijo backtracking results (lm.py:226-236)
-      for (int j = 0; j < LM_B && s.j0 + j < c.max_backtracks; ++j) {
+      for (int j = 0; j < s.ntr && s.j0 + j < c.max_backtracks; ++j) {
         const int row = p * LM_B + j;
         const double Jt = R.odeg[row] > 0 ? INFINITY : R.oout[row];
         const double alpha = ldexp(1.0, -(s.j0 + j));
@@ -330,9 +335,10 @@ static __device__ int lm_advance(const LmRun& R, int p, LmState& s, double* A, d
           return ACT_WAIT;
         }
       }
-      if (s.j0 + LM_B < c.max_backtracks) {
-        s.j0 += LM_B;
-        post_trials(R, p, s.j0, false, min(LM_B, c.max_backtracks - s.j0));
+      if (s.j0 + s.ntr < c.max_backtracks) {
+        s.j0 += s.ntr;
+        s.ntr = min(LM_B, c.max_backtracks - s.j0);
+        post_trials(R, p, s.j0, false, s.ntr);
         s.evals++;
         return ACT_WAIT;
       }
@@ -364,7 +370,8 @@ static __device__ int lm_after_solve(const LmRun& R, int p, LmState& s, int act,
     } else {
       s.j0 = 0;
       s.phase = PH_SI_LS;
-      post_trials(R, p, 0, true, LM_B);
+      s.ntr = R.nb_first;
+      post_trials(R, p, 0, true, s.ntr);
     }
     s.evals++;
     return ACT_WAIT;
@@ -379,7 +386,8 @@ static __device__ int lm_after_solve(const LmRun& R, int p, LmState& s, int act,
   for (int i = 0; i < K; ++i) R.dw[p * K + i] = x[i];
   s.j0 = 0;
   s.phase = PH_MAIN_LS;
-  post_trials(R, p, 0, false, min(LM_B, R.cfg.max_backtracks));
+  s.ntr = min(R.nb_first, R.cfg.max_backtracks);
+  post_trials(R, p, 0, false, s.ntr);
   s.evals++;
   return ACT_WAIT;
 }
