@@ -274,7 +274,7 @@ __device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB,
       uq[c] = v;
     }
     double f[M][2];
-    LAW::flux(uq, f, la);
+    PointVal<LAW>::flux(uq, f, la);
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       double F0 = T.wq[q] * (f[c][0] * o.adj[0][0] + f[c][1] * o.adj[0][1]);
@@ -350,9 +350,7 @@ __device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB,
         for (int c = 0; c < M; ++c) uo[c] = ghost[c];
       }
       double fi_[M][2], fo[M][2];
-      LAW::flux(ui, fi_, la);
-      LAW::flux(uo, fo, la);
-      double wi = LAW::wavespeed(ui, nh, la), wo = LAW::wavespeed(uo, nh, la);
+      const double wi = PointVal<LAW>::flux_ws(ui, nh, fi_, la), wo = PointVal<LAW>::flux_ws(uo, nh, fo, la);
       double lam = wi >= wo ? wi : wo;
 #pragma unroll
       for (int c = 0; c < M; ++c) {

@@ -340,6 +340,41 @@ struct Euler {
   }
 };
 
+// ---- value path: flux and LLF wavespeed of one state (K2) --------------------------
+// Generic: the law's templated flux / wavespeed.  Euler: one reciprocal of the density
+// and one rsqrt for the sound speed instead of five divisions and a sqrt.
+template <class LAW>
+struct PointVal {
+  __device__ static void flux(const double* u, double (*f)[2], const LawArgs& a) { LAW::flux(u, f, a); }
+  __device__ static double flux_ws(const double* u, const double* nh, double (*f)[2], const LawArgs& a) {
+    LAW::flux(u, f, a);
+    return LAW::wavespeed(u, nh, a);
+  }
+};
+template <>
+struct PointVal<Euler> {
+  __device__ static void flux(const double* u, double (*f)[2], const LawArgs& a) {
+    const double g = a.p[0];
+    const double ir = 1.0 / u[0], vx = u[1] * ir, vy = u[2] * ir;
+    const double p = (g - 1.0) * (u[3] - 0.5 * (u[1] * vx + u[2] * vy)), Ep = u[3] + p;
+    f[0][0] = u[1];          f[0][1] = u[2];
+    f[1][0] = u[1] * vx + p; f[1][1] = u[1] * vy;
+    f[2][0] = u[2] * vx;     f[2][1] = u[2] * vy + p;
+    f[3][0] = Ep * vx;       f[3][1] = Ep * vy;
+  }
+  __device__ static double flux_ws(const double* u, const double* nh, double (*f)[2], const LawArgs& a) {
+    const double g = a.p[0];
+    const double ir = 1.0 / u[0], vx = u[1] * ir, vy = u[2] * ir;
+    const double p = (g - 1.0) * (u[3] - 0.5 * (u[1] * vx + u[2] * vy)), Ep = u[3] + p;
+    f[0][0] = u[1];          f[0][1] = u[2];
+    f[1][0] = u[1] * vx + p; f[1][1] = u[1] * vy;
+    f[2][0] = u[2] * vx;     f[2][1] = u[2] * vy + p;
+    f[3][0] = Ep * vx;       f[3][1] = Ep * vy;
+    const double c2 = g * p * ir;
+    return fabs(vx * nh[0] + vy * nh[1]) + c2 * rsqrt(c2);  // |v.n| + sqrt(g p / rho)
+  }
+};
+
 // ---- point Jacobians: analytic when the law provides them, else forward mode ----
 template <class LAW, bool A = LAW::ANALYTIC>
 struct PointOps;

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
         uq[c] = v;
       }
       double f[M][2];
-      LAW::flux(uq, f, la);
+      PointVal<LAW>::flux(uq, f, la);
 #pragma unroll
       for (int c = 0; c < M; ++c) {
         const double F0 = T.wq[q] * (f[c][0] * adj00 + f[c][1] * adj01);
@@ -264,9 +264,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
           for (int c = 0; c < M; ++c) uo[c] = ghost[c];
         }
         double fi_[M][2], fo[M][2];
-        LAW::flux(ui, fi_, la);
-        LAW::flux(uo, fo, la);
-        const double wi = LAW::wavespeed(ui, nh, la), wo = LAW::wavespeed(uo, nh, la);
+        const double wi = PointVal<LAW>::flux_ws(ui, nh, fi_, la), wo = PointVal<LAW>::flux_ws(uo, nh, fo, la);
         const double lam = wi >= wo ? wi : wo;  // dual.maximum tie -> first argument
 #pragma unroll
         for (int c = 0; c < M; ++c) {
