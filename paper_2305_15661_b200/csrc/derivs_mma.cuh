@@ -39,6 +39,9 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_PREF_E
 #define STROM_PREF_E 0  // own-projection B fragments loaded before the L stage
 #endif
+#ifndef STROM_PREF_NBR
+#define STROM_PREF_NBR 0  // L2 prefetch of the next unit's neighbor face-node rows
+#endif
 #ifndef STROM_PREF_JIT
 #define STROM_PREF_JIT 0  // each face's neighbor B fragments loaded at the top of its face step
 #endif
@@ -977,6 +980,19 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         } else {
           const char* base = reinterpret_cast<const char*>(r.phi + (size_t)nact * NU * ku);
           for (int off = lane * 128; off < NU * ku * 8; off += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+          if (STROM_PREF_NBR) {  // the next unit's neighbor face-node rows (one 8*k_u-byte row per lane)
+            __syncwarp();
+            for (int i = lane; i < NF * NF * M; i += 32) {
+              const int f = i / (NF * M), jj = (i / M) % NF, c = i % M;
+              const int fi = EI[7 + f];
+              if ((fi >> 3) == 0) {
+                const int nf = fi & 3;
+                const int node = jj == 0 ? nf : (jj == 1 ? (nf == 2 ? 0 : nf + 1) : 3 + nf);
+                const double* row = r.phi + ((size_t)EI[4 + f] * NU + node * M + c) * ku;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+              }
+            }
+          }
         }
       }
     }
