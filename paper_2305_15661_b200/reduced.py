@@ -224,19 +224,45 @@ class GpuReducedOperator:
         self.stats["elements_evaluated"] += A * P
         return out, rc
 
+    def _staging(self, key, n, dtype=torch.float64, pinned=True):
+        """Reused host (pinned) / device buffers of the one-point public calls."""
+        cache = self.__dict__.setdefault("_stage", {})
+        t = cache.get((key, pinned))
+        if t is None or t.numel() < n:
+            t = (torch.empty(max(n, 1), dtype=dtype, pin_memory=True) if pinned
+                 else torch.empty(max(n, 1), dtype=dtype, device=self.device))
+            cache[(key, pinned)] = t
+        return t[:n]
+
     def _single(self, mode, coords, mu, rho):
-        buf = np.concatenate([np.asarray(coords.w, dtype=float).reshape(-1),
-                              np.asarray(coords.tau, dtype=float).reshape(-1), self._mu(mu)])
-        d = torch.as_tensor(buf).to(self.device, non_blocking=False)
+        """One parameter point through the public API: inputs staged in pinned memory, one
+        asynchronous H2D copy, the evaluation, results and the degenerate flag read back
+        with one stream synchronisation (the element ids only on the rare degenerate path)."""
         ku, kx = self.k_u, self.k_x
+        n_in = ku + kx + self.n_mu
+        hin = self._staging("in", n_in)
+        a = hin.numpy()
+        a[:ku] = np.asarray(coords.w, dtype=float).reshape(-1)
+        a[ku:ku + kx] = np.asarray(coords.tau, dtype=float).reshape(-1)
+        a[ku + kx:] = self._mu(mu)
+        d = self._staging("in", n_in, pinned=False)
+        d.copy_(hin, non_blocking=True)
         W, Tau, Mu = d[:ku].view(1, ku), d[ku:ku + kx].view(1, kx), d[ku + kx:].view(1, self.n_mu)
-        out, rc = self.eval_batched(mode, W, Tau, Mu, rho, sync=True)
-        if rc == 1:
-            n = self._lib.strom_degenerate_elements(self._h, 0, None, 0)
-            ids = np.zeros(max(n, 1), dtype=np.int32)
-            self._lib.strom_degenerate_elements(self._h, 0, ids.ctypes.data, n)
-            raise degenerate_error(ids[:n].astype(np.int64))
-        return out.cpu().numpy()
+        degen = self._staging("deg", 1, torch.int32, pinned=False)
+        out, _ = self.eval_batched(mode, W, Tau, Mu, rho, degen=degen)
+        hout = self._staging("out", out.numel())
+        hout.copy_(out, non_blocking=True)
+        hdeg = self._staging("deg", 1, torch.int32)
+        hdeg.copy_(degen, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        if int(hdeg[0]) > 0:  # degenerate elements: re-run synchronously for their ids
+            _, rc = self.eval_batched(mode, W, Tau, Mu, rho, sync=True)
+            if rc == 1:
+                n = self._lib.strom_degenerate_elements(self._h, 0, None, 0)
+                ids = np.zeros(max(n, 1), dtype=np.int32)
+                self._lib.strom_degenerate_elements(self._h, 0, ids.ctypes.data, n)
+                raise degenerate_error(ids[:n].astype(np.int64))
+        return hout.numpy().copy()
 
     # -- reference API -------------------------------------------------------------
     def objective(self, coords, mu, rho=None):
