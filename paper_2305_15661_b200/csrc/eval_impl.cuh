@@ -109,6 +109,8 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
   static int c_dev = -1, c_per_sm = 0;
   if (c_smem != smem || c_dev != h->device) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (const char* ev = getenv("STROM_MMA_CARVEOUT"))  // experiment knob: shared-memory carveout (%)
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(ev)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per_sm, kern, nwarps * 32, smem));
     c_smem = smem;
     c_dev = h->device;
