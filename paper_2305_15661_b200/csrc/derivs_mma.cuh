@@ -39,6 +39,9 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_PREF_E
 #define STROM_PREF_E 0  // own-projection B fragments loaded before the L stage
 #endif
+#ifndef STROM_XEARLY
+#define STROM_XEARLY 0  // dR/dx stage in the shadow of the L-GEMM DMMAs (own region): 2.7% slower (spills)
+#endif
 #ifndef STROM_PREF_NBR
 #define STROM_PREF_NBR 0  // L2 prefetch of the next unit's neighbor face-node rows
 #endif
@@ -117,7 +120,8 @@ struct MShape {
   __host__ __device__ static constexpr bool phibuf(int KUT) { return STROM_PHIBUF && KUT == 16; }
   __host__ __device__ static int warp_stride(int LDJ, int KP, int kx, bool hreg, bool phib = false) {
     const int a = LO + NLO * 12 * LDO, b = drx(LDJ) + NU * LDX;
-    const int s = RA + (a > b ? a : b) + (hreg ? 0 : hsize(KP)) + gtail(KP) + psr(kx) + (phib ? NU * PHS : 0);
+    const int s = RA + (a > b ? a : b) + (hreg ? 0 : hsize(KP)) + gtail(KP) + psr(kx) + (phib ? NU * PHS : 0) +
+                  (STROM_XEARLY ? NU * LDX : 0);
     return (s + 15) / 16 * 16 + 4;
   }
 };
@@ -167,6 +171,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   double* const PR = (HREG ? GW : HA) - SH::psr(kx);  // Psi rows of the element's vertex coordinates
   constexpr bool PHB = SH::phibuf(KUT);
   double* const PHI = PR - NU * SH::PHS;  // Phi_e block (PHB)
+  double* const DRXE = (PHB ? PHI : PR) - NU * LDX;  // dR/dx rows (XEARLY)
   // 16-byte async copies of element ue's 24 basis rows (KUT = 16: 8 chunks per row) into PHI
   auto phi_async = [&](int ue) {
 #pragma unroll
@@ -652,6 +657,44 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     }
     // next unit's index block: loaded here, stored to smem after the Jx stage
     const int wv = (nidx < nunits && lane < 10) ? index_word(nact, lane) : 0;
+    // ---- X: local mesh Jacobian dR/dx (24 x 6) -------------------------------------------
+    auto x_stage = [&](double* drxb) {
+    if (lane < NU) {
+      const int i = lane, n = i / M, c = i % M;
+      const double t00 = S[SH::TQ + i], t01 = S[SH::TQ + SH::TQS + i], t10 = S[SH::TQ + 2 * SH::TQS + i], t11 = S[SH::TQ + 3 * SH::TQS + i];
+      double dr[6];
+#pragma unroll
+      for (int d = 0; d < 6; ++d) {
+        const int gv = d >> 1, ic = d & 1;
+        const double c0 = (gv == 1) - (gv == 0), c1 = (gv == 2) - (gv == 0);
+        // ic = 0: dadj = [[0,-c1],[0,c0]]; ic = 1: dadj = [[c1,0],[-c0,0]]
+        dr[d] = ic == 0 ? (c1 * t01 - c0 * t11) : -(c1 * t00 - c0 * t10);
+      }
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        const int j = face_local(f, n);
+        if (j < 0) continue;
+        double rx = 0.0, ry = 0.0;  // face response to dnu = e_x, e_y
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          rx = fma(T.trace[0][s][j], S[SH::FD + (c * 2 + 0) * NFSP + f * NS + s], rx);
+          ry = fma(T.trace[0][s][j], S[SH::FD + (c * 2 + 1) * NFSP + f * NS + s], ry);
+        }
+        const int a = f, b = (f + 1) % 3;
+        // vertex g in {a, b}: del = (g == b) - (g == a); ic = 1 -> dnu = del e_x, ic = 0 -> dnu = -del e_y
+        dr[2 * b + 1] += rx;  dr[2 * a + 1] -= rx;
+        dr[2 * b + 0] -= ry;  dr[2 * a + 0] += ry;
+      }
+      {  // 16-byte pieces, order rotated by (i>>2)&1: conflict-free quarter-warp stores
+        double2* dst = reinterpret_cast<double2*>(drxb + i * LDX);
+        const bool rot = (i & 4) != 0;
+        const double2 pc[4] = {make_double2(dr[0], dr[1]), make_double2(dr[2], dr[3]), make_double2(dr[4], dr[5]),
+                               make_double2(0.0, 0.0)};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dst[rot ? (t + 1) & 3 : t] = rot ? pc[(t + 1) & 3] : pc[t];
+      }
+    }
+    };
     // ---- L: volume local Jacobian on DMMA; X = Dq^T B_q fused into the A fragments ------
     {
       double lv[4][3][2];
@@ -676,6 +719,10 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
             dmma(lv[cp][mt][0], lv[cp][mt][1], a, phib[ks]);
           }
         }
+      }
+      if (STROM_XEARLY) {  // independent scalar work while the L-GEMM DMMAs are in flight
+        __syncwarp();      // (FD / TQ rows of other lanes)
+        x_stage(DRXE);
       }
       __syncwarp();  // BQ / CF reads of other lanes finished before L overwrites region A? (L lives after CF)
       // write -L into L[(n,c)][(n',c')], n' = 2(lane&3) + {0,1}: the lane's 8 values are
@@ -863,42 +910,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       }
     }
     __syncwarp();  // LOUT reads done before DRX overwrites it
-    // ---- X: local mesh Jacobian dR/dx (24 x 6) -------------------------------------------
-    if (lane < NU) {
-      const int i = lane, n = i / M, c = i % M;
-      const double t00 = S[SH::TQ + i], t01 = S[SH::TQ + SH::TQS + i], t10 = S[SH::TQ + 2 * SH::TQS + i], t11 = S[SH::TQ + 3 * SH::TQS + i];
-      double dr[6];
-#pragma unroll
-      for (int d = 0; d < 6; ++d) {
-        const int gv = d >> 1, ic = d & 1;
-        const double c0 = (gv == 1) - (gv == 0), c1 = (gv == 2) - (gv == 0);
-        // ic = 0: dadj = [[0,-c1],[0,c0]]; ic = 1: dadj = [[c1,0],[-c0,0]]
-        dr[d] = ic == 0 ? (c1 * t01 - c0 * t11) : -(c1 * t00 - c0 * t10);
-      }
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        const int j = face_local(f, n);
-        if (j < 0) continue;
-        double rx = 0.0, ry = 0.0;  // face response to dnu = e_x, e_y
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          rx = fma(T.trace[0][s][j], S[SH::FD + (c * 2 + 0) * NFSP + f * NS + s], rx);
-          ry = fma(T.trace[0][s][j], S[SH::FD + (c * 2 + 1) * NFSP + f * NS + s], ry);
-        }
-        const int a = f, b = (f + 1) % 3;
-        // vertex g in {a, b}: del = (g == b) - (g == a); ic = 1 -> dnu = del e_x, ic = 0 -> dnu = -del e_y
-        dr[2 * b + 1] += rx;  dr[2 * a + 1] -= rx;
-        dr[2 * b + 0] -= ry;  dr[2 * a + 0] += ry;
-      }
-      {  // 16-byte pieces, order rotated by (i>>2)&1: conflict-free quarter-warp stores
-        double2* dst = reinterpret_cast<double2*>(RA + DRXo + i * LDX);
-        const bool rot = (i & 4) != 0;
-        const double2 pc[4] = {make_double2(dr[0], dr[1]), make_double2(dr[2], dr[3]), make_double2(dr[4], dr[5]),
-                               make_double2(0.0, 0.0)};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) dst[rot ? (t + 1) & 3 : t] = rot ? pc[(t + 1) & 3] : pc[t];
-      }
-    }
+    if (!STROM_XEARLY) x_stage(RA + DRXo);
     __syncwarp();
     // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
     double* Jt = RA;
@@ -935,7 +947,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         const int d = 4 * ks + (lane & 3);
         double af[3];
 #pragma unroll
-        for (int mt = 0; mt < 3; ++mt) af[mt] = RA[DRXo + prow(mt, lane) * LDX + d];
+        for (int mt = 0; mt < 3; ++mt) af[mt] = (STROM_XEARLY ? DRXE : RA + DRXo)[prow(mt, lane) * LDX + d];
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           if (nt < ntx) {
