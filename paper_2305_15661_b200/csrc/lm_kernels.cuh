@@ -115,12 +115,13 @@ static __device__ bool ldlt_solve(double* A, int n, double* b, double* x, int* f
   }
   for (int i = t; i < n; i += nt) x[i] = b[i] / A[i * n + i];
   __syncthreads();
+  // L^T x = z: column sweep, x[k] -= L[i][k] x[i] for k < i (i descending)
+  for (int i = n - 1; i > 0; --i) {
+    const double xi = x[i];
+    for (int k = t; k < i; k += nt) x[k] -= A[i * n + k] * xi;
+    __syncthreads();
+  }
   if (t == 0) {
-    for (int i = n - 1; i >= 0; --i) {  // L^T x = z
-      double v = x[i];
-      for (int k = i + 1; k < n; ++k) v -= A[k * n + i] * x[k];
-      x[i] = v;
-    }
     bool ok = true;
     for (int i = 0; i < n; ++i) ok = ok && isfinite(x[i]);
     *flag = ok ? 1 : 0;
