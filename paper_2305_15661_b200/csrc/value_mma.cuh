@@ -223,17 +223,20 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
       if (bc == 0) {  // warp-uniform (one element per warp)
         const int nf = fi & 3;
         flip = (fi >> 2) & 1;
+        if (VM_USMEM) __syncwarp();  // the previous face's reads of the face rows are done
         vm_recon<VS::MT_F, VM_NTB_F>(r, Ws, tile + VS::FROW * VM_LDU, NFR, [&](int rr) {
           const int j = rr / M, c = rr % M;
           const int node = j == 0 ? nf : (j == 1 ? (nf + 1) % 3 : 3 + nf * (PD - 1) + (j - 2));
           return nb * NU + node * M + c;
         }, s_prow, lane);
         __syncwarp();
+        if (!VM_USMEM) {
 #pragma unroll
-        for (int j = 0; j < NF; ++j)
+          for (int j = 0; j < NF; ++j)
 #pragma unroll
-          for (int c = 0; c < M; ++c) Un[j][c] = tile[(VS::FROW + j * M + c) * VM_LDU + lane];
-        __syncwarp();
+            for (int c = 0; c < M; ++c) Un[j][c] = tile[(VS::FROW + j * M + c) * VM_LDU + lane];
+          __syncwarp();
+        }
       }
       double ghost[M];
       if (bc >= 2) LAW::ghost(bc - 2, la, ghost);
@@ -253,7 +256,8 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
           for (int c = 0; c < M; ++c) {
             double v = 0.0;
 #pragma unroll
-            for (int j = 0; j < NF; ++j) v = fma(T.trace[0][sp][j], Un[j][c], v);
+            for (int j = 0; j < NF; ++j)
+              v = fma(T.trace[0][sp][j], VM_USMEM ? tile[(VS::FROW + j * M + c) * VM_LDU + lane] : Un[j][c], v);
             uo[c] = v;
           }
         } else if (bc == 1) {
