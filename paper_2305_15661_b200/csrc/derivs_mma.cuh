@@ -99,15 +99,15 @@ struct MShape {
   static constexpr int LO = LA + CFS + 16 * NFSP;
   static constexpr int FX = LO;
   static_assert(FXS * NFSP <= NLO * 12 * LDO, "FX overlays the Lout buffers");
-  __host__ __device__ static int drx(int LDJ) { return LA > NU * LDJ ? LA : NU * LDJ; }
-  __host__ __device__ static int gtail(int KP) { return KP + 8; }  // gradient (K) + residual norm
+  __host__ __device__ static constexpr int drx(int LDJ) { return LA > NU * LDJ ? LA : NU * LDJ; }
+  __host__ __device__ static constexpr int gtail(int KP) { return KP + 8; }  // gradient (K) + residual norm
   // Gram accumulator: upper 8x8 tiles only, tile (ti <= tj) at tri_tile(ti, tj) * 64
-  __host__ __device__ static int hsize(int KP) { return (KP / 8) * (KP / 8 + 1) / 2 * 64; }
+  __host__ __device__ static constexpr int hsize(int KP) { return (KP / 8) * (KP / 8 + 1) / 2 * 64; }
   __host__ __device__ static constexpr int tri_tile(int ti, int tj, int nt8) { return ti * nt8 - ti * (ti - 1) / 2 + (tj - ti); }
   // the element's six Psi rows (gathered once, read by the Jx and distortion stages),
   // row stride == 4 mod 8 (conflict-free B fragments), just below the Gram accumulator
-  __host__ __device__ static int prs(int kx) { return (kx + 3) / 8 * 8 + 4; }
-  __host__ __device__ static int psr(int kx) { return 6 * prs(kx); }
+  __host__ __device__ static constexpr int prs(int kx) { return (kx + 3) / 8 * 8 + 4; }
+  __host__ __device__ static constexpr int psr(int kx) { return 6 * prs(kx); }
   // Gram accumulator in registers: compile-time K <= 24 (six upper tiles, 12 doubles per lane)
   // k_u > 16 gets the wide register budget (measured per pass: cfg3 -10%, cfg4 -3.5%, cfg5 -6.5%)
   __host__ __device__ static constexpr bool wide(int KUT) { return KUT > 16; }
@@ -118,7 +118,7 @@ struct MShape {
   // c ^ 2(r & 3): conflict-free B-fragment loads, 2-way at most for the row-wise gather)
   static constexpr int PHS = 16;
   __host__ __device__ static constexpr bool phibuf(int KUT) { return STROM_PHIBUF && KUT == 16; }
-  __host__ __device__ static int warp_stride(int LDJ, int KP, int kx, bool hreg, bool phib = false) {
+  __host__ __device__ static constexpr int warp_stride(int LDJ, int KP, int kx, bool hreg, bool phib = false) {
     const int a = LO + NLO * 12 * LDO, b = drx(LDJ) + NU * LDX;
     const int s = RA + (a > b ? a : b) + (hreg ? 0 : hsize(KP)) + gtail(KP) + psr(kx) + (phib ? NU * PHS : 0) +
                   (STROM_XEARLY ? NU * LDX : 0);
@@ -160,11 +160,13 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   constexpr int KT = KUT + KXT, KPT = (KT + 7) / 8 * 8;
   const int ku = CT ? KUT : r.ku, kx = CT ? KXT : r.kx, K = CT ? KT : r.K, KP = CT ? KPT : r.KP;
   const int LDJ = CT ? KPT + 4 : r.LDJ;
-  double* const S = smem + (size_t)warp * r.gx_warp_stride;
+  // per-warp stride: a compile-time constant on the specialised path (cheap to rematerialise)
+  const int WSTR = CT ? SH::warp_stride(KPT + 4, KPT, KXT, SH::hreg(KUT, KXT), SH::phibuf(KUT)) : r.gx_warp_stride;
+  double* const S = smem + (size_t)warp * WSTR;
   double* const RA = S + SH::RA;
   const int DRXo = SH::drx(LDJ);
   constexpr bool HREG = SH::hreg(KUT, KXT);
-  double* const GW = S + r.gx_warp_stride - 4 - SH::gtail(KP);  // gradient + objective tail
+  double* const GW = S + WSTR - 4 - SH::gtail(KP);  // gradient + objective tail
   // warp Gram accumulator (upper 8x8 tiles): registers + region A at the end (HREG), or smem
   double* const HA = HREG ? S + SH::RA : GW - SH::hsize(KP);
   const int PRS = SH::prs(kx);
@@ -1165,8 +1167,8 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   for (int i = threadIdx.x; i < PSZ; i += blockDim.x) {
     double v = 0.0;
     for (int w = 0; w < nwarps; ++w) {
-      const double* Sw = smem + (size_t)w * r.gx_warp_stride;
-      const double* Gw = Sw + r.gx_warp_stride - 4 - SH::gtail(KP);
+      const double* Sw = smem + (size_t)w * WSTR;
+      const double* Gw = Sw + WSTR - 4 - SH::gtail(KP);
       const double* Hw = HREG ? Sw + SH::RA : Gw - SH::hsize(KP);
       if (i == 0) v += Gw[K];
       else if (i <= K) v += Gw[i - 1];
