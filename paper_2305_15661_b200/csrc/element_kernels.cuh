@@ -118,8 +118,9 @@ __device__ __forceinline__ double distortion_eta(const Geo& o, double wsum, doub
 
 // d N / d x_d for one local coordinate direction d = 2*vertex + component
 __device__ __forceinline__ double distortion_grad_dir(const Geo& o, double wsum, double eps, double kappa, int d) {
-  double ratio, den;
-  distortion_eta(o, wsum, eps, &ratio, &den);
+  const double fro2 = o.G[0][0] * o.G[0][0] + o.G[0][1] * o.G[0][1] + o.G[1][0] * o.G[1][0] + o.G[1][1] * o.G[1][1];
+  const double den = o.g >= eps ? o.g : eps, iden = 1.0 / den;  // one reciprocal for ratio and its derivative
+  const double ratio = fro2 * iden;
   const int gv = d >> 1, ic = d & 1;
   const double c0 = (gv == 1) - (gv == 0), c1 = (gv == 2) - (gv == 0);
   const double dJ00 = ic == 0 ? c0 : 0.0, dJ01 = ic == 0 ? c1 : 0.0, dJ10 = ic == 1 ? c0 : 0.0, dJ11 = ic == 1 ? c1 : 0.0;
@@ -128,7 +129,7 @@ __device__ __forceinline__ double distortion_grad_dir(const Geo& o, double wsum,
   const double dg = dG00 * o.G[1][1] + o.G[0][0] * dG11 - dG01 * o.G[1][0] - o.G[0][1] * dG10;
   const double dfro = 2.0 * (o.G[0][0] * dG00 + o.G[0][1] * dG01 + o.G[1][0] * dG10 + o.G[1][1] * dG11);
   const double dden = o.g >= eps ? dg : 0.0;
-  const double dratio = (dfro - ratio * dden) / den;
+  const double dratio = (dfro - ratio * dden) * iden;
   return kappa * wsum * o.detr * 2.0 * ratio * dratio;
 }
 
@@ -180,8 +181,9 @@ __device__ __forceinline__ void face_normal(const double* x, int f, double* nu, 
   int a = f, b = (f + 1) % 3;
   double tx = x[2 * b] - x[2 * a], ty = x[2 * b + 1] - x[2 * a + 1];
   nu[0] = ty; nu[1] = -tx;
-  len = sqrt(nu[0] * nu[0] + nu[1] * nu[1]);
-  nh[0] = nu[0] / len; nh[1] = nu[1] / len;
+  const double l2 = nu[0] * nu[0] + nu[1] * nu[1], il = rsqrt(l2);  // one rsqrt: |nu| and nu / |nu|
+  len = l2 * il;
+  nh[0] = nu[0] * il; nh[1] = nu[1] * il;
 }
 
 // row . w for a basis row of length ku <= 32 with w in registers (compile-time
