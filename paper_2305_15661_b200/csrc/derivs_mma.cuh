@@ -42,6 +42,9 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_XEARLY
 #define STROM_XEARLY 0  // dR/dx stage in the shadow of the L-GEMM DMMAs (own region): 2.7% slower (spills)
 #endif
+#ifndef STROM_L1PF
+#define STROM_L1PF 0  // L1 prefetch of the projection basis rows before the face stage (3% slower: spills)
+#endif
 #ifndef STROM_PREF_NBR
 #define STROM_PREF_NBR 0  // L2 prefetch of the next unit's neighbor face-node rows
 #endif
@@ -747,6 +750,17 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       }
     }
     __syncwarp();
+    if (STROM_L1PF && CT) {  // projection B-fragment rows back into L1 (no registers held)
+      if (lane < NU) asm volatile("prefetch.global.L1 [%0];" ::"l"(r.phi + ((size_t)e * NU + lane) * ku));
+      for (int i = lane; i < NF * NF * M; i += 32) {
+        const int f = i / (NF * M), jj = (i / M) % NF, c = i % M;
+        if ((fin[f] >> 3) == 0) {
+          const int nf = fin[f] & 3;
+          const int node = jj == 0 ? nf : (jj == 1 ? (nf == 2 ? 0 : nf + 1) : 3 + nf);
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(r.phi + ((size_t)nbr[f] * NU + node * M + c) * ku));
+        }
+      }
+    }
     // face blocks, one face at a time: lanes 0-15 add the in-side block into L, lanes
     // 16-31 form Lout_f in a one-face buffer, then the warp projects it on the
     // neighbor's face-node basis rows straight into the J accumulators
