@@ -144,7 +144,8 @@ __device__ __forceinline__ int prow(int mt, int lane) {
   return node * 4 + ((lane >> 2) & 3);
 }
 
-template <class LAW, int NQ, int KUT = 0, int KXT = 0>  // KUT/KXT > 0: compile-time reduced dimensions
+template <class LAW, int NQ, int KUT = 0, int KXT = 0, int DM = -1>  // KUT/KXT > 0: compile-time reduced dimensions;
+                                                                     // DM: 1 derivatives / 0 contributions / -1 runtime
 __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STROM_MMA_MAXNREG) derivs_mma_kernel(const __grid_constant__ Params<6, NQ, 4, 3> prm) {
   using SH = MShape<NQ>;
   constexpr int M = 4, NB = 6, NU = 24, NF = 3, NS = 4, NFS = 12, PD = 2;
@@ -160,6 +161,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   const int p = blockIdx.y;
   if (r.mask && !r.mask[p]) return;
   constexpr bool CT = KUT > 0;
+  const bool DERIVS = DM >= 0 ? DM == 1 : r.mode == MODE_DERIVS;  // compile-time on the specialised path
   constexpr int KT = KUT + KXT, KPT = (KT + 7) / 8 * 8;
   const int ku = CT ? KUT : r.ku, kx = CT ? KXT : r.kx, K = CT ? KT : r.K, KP = CT ? KPT : r.KP;
   const int LDJ = CT ? KPT + 4 : r.LDJ;
@@ -931,7 +933,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
     double* Jt = RA;
     constexpr bool GFRAG = CT && STROM_GFRAG;  // gradient from the fragments
-    const bool gfrag = GFRAG && r.mode == MODE_DERIVS;
+    const bool gfrag = GFRAG && DERIVS;
     double rr[3];  // rho * R at the lane's three projection rows
 #pragma unroll
     for (int mt = 0; mt < 3; ++mt) rr[mt] = gfrag ? rho * S[SH::RT + prow(mt, lane)] : 0.0;
@@ -1025,7 +1027,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       }
     }
     // ---- G: Gram and gradient, or per-element contributions --------------------------------
-    if (r.mode == MODE_DERIVS) {
+    if (DERIVS) {
       if constexpr (CT) {
         // fragments of J^T per (tile column, k-step), loaded once and shared by the tiles
         constexpr int NT8C = KPT / 8;
@@ -1140,7 +1142,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     }
     __syncwarp();
   }
-  if (r.mode != MODE_DERIVS) return;
+  if (!DERIVS) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) jacc += __shfl_xor_sync(0xffffffffu, jacc, o);
   if constexpr (CT && STROM_GFRAG) {

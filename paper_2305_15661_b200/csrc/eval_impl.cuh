@@ -102,20 +102,22 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
   if (const char* ev = getenv("STROM_MMA_WARPS")) nwarps = std::max(1, std::min(nwarps, atoi(ev)));
   if (nwarps < 1) return fail(-1, "element does not fit in shared memory");
   const size_t smem = nwarps * warp_bytes;
-  auto kern = derivs_mma_kernel<LAW, NQ, KUT, KXT>;
+  auto kern = KUT > 0 ? (a.mode == MODE_DERIVS ? derivs_mma_kernel<LAW, NQ, KUT, KXT, 1> : derivs_mma_kernel<LAW, NQ, KUT, KXT, 0>)
+                      : derivs_mma_kernel<LAW, NQ, KUT, KXT>;
   // attribute + occupancy query once per (kernel, shared-memory size, device): host API
   // calls on every launch dominate the small LM rounds
-  static size_t c_smem = 0;
-  static int c_dev = -1, c_per_sm = 0;
-  if (c_smem != smem || c_dev != h->device) {
+  const int ck = (KUT > 0 && a.mode == MODE_DERIVS) ? 1 : 0;  // one cache slot per kernel variant
+  static size_t c_smem[2] = {0, 0};
+  static int c_dev[2] = {-1, -1}, c_per_sm[2] = {0, 0};
+  if (c_smem[ck] != smem || c_dev[ck] != h->device) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (const char* ev = getenv("STROM_MMA_CARVEOUT"))  // experiment knob: shared-memory carveout (%)
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(ev)));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per_sm, kern, nwarps * 32, smem));
-    c_smem = smem;
-    c_dev = h->device;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per_sm[ck], kern, nwarps * 32, smem));
+    c_smem[ck] = smem;
+    c_dev[ck] = h->device;
   }
-  int per_sm = c_per_sm;
+  int per_sm = c_per_sm[ck];
   if (getenv("STROM_DEBUG")) {
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, kern));
