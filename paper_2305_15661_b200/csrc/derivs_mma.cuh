@@ -45,6 +45,9 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_L1PF
 #define STROM_L1PF 0  // L1 prefetch of the projection basis rows before the face stage (3% slower: spills)
 #endif
+#ifndef STROM_DRX_ROT
+#define STROM_DRX_ROT 0  // rotated conflict-free dR/dx stores (selects) vs three plain stores
+#endif
 #ifndef STROM_PREF_NBR
 #define STROM_PREF_NBR 0  // L2 prefetch of the next unit's neighbor face-node rows
 #endif
@@ -692,6 +695,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         dr[2 * b + 1] += rx;  dr[2 * a + 1] -= rx;
         dr[2 * b + 0] -= ry;  dr[2 * a + 0] += ry;
       }
+#if STROM_DRX_ROT
       {  // 16-byte pieces, order rotated by (i>>2)&1: conflict-free quarter-warp stores
         double2* dst = reinterpret_cast<double2*>(drxb + i * LDX);
         const bool rot = (i & 4) != 0;
@@ -700,6 +704,14 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
 #pragma unroll
         for (int t = 0; t < 4; ++t) dst[rot ? (t + 1) & 3 : t] = rot ? pc[(t + 1) & 3] : pc[t];
       }
+#else
+      {  // three 16-byte pieces (columns 6, 7 are never read: the Jx A fragments are predicated)
+        double2* dst = reinterpret_cast<double2*>(drxb + i * LDX);
+        dst[0] = make_double2(dr[0], dr[1]);
+        dst[1] = make_double2(dr[2], dr[3]);
+        dst[2] = make_double2(dr[4], dr[5]);
+      }
+#endif
     }
     };
     // ---- L: volume local Jacobian on DMMA; X = Dq^T B_q fused into the A fragments ------
@@ -965,7 +977,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         const int d = 4 * ks + (lane & 3);
         double af[3];
 #pragma unroll
-        for (int mt = 0; mt < 3; ++mt) af[mt] = (STROM_XEARLY ? DRXE : RA + DRXo)[prow(mt, lane) * LDX + d];
+        for (int mt = 0; mt < 3; ++mt) af[mt] = d < 6 ? (STROM_XEARLY ? DRXE : RA + DRXo)[prow(mt, lane) * LDX + d] : 0.0;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           if (nt < ntx) {
