@@ -45,6 +45,9 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_L1PF
 #define STROM_L1PF 0  // L1 prefetch of the projection basis rows before the face stage (3% slower: spills)
 #endif
+#ifndef STROM_L_ROT
+#define STROM_L_ROT 1  // rotated conflict-free L stores (selects) vs plain stores (2-way conflicts)
+#endif
 #ifndef STROM_DRX_ROT
 #define STROM_DRX_ROT 0  // rotated conflict-free dR/dx stores (selects) vs three plain stores
 #endif
@@ -748,7 +751,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       // contiguous (columns 8(lane&3) .. +7), written as four 16-byte pieces in an order
       // rotated by (lane&3)>>1 so every quarter-warp store hits 8 distinct bank groups
       if ((lane & 3) < 3) {
-        const bool rot = (lane & 2) != 0;
+        const bool rot = STROM_L_ROT && (lane & 2) != 0;
 #pragma unroll
         for (int mt = 0; mt < 3; ++mt) {
           double2* dst = reinterpret_cast<double2*>(RA + SH::LL + (mt * 8 + (lane >> 2)) * LDL + 8 * (lane & 3));
@@ -758,7 +761,8 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
             const int pa = t, pb = (t + 1) & 3;
             const double xa = -lv[2 * (pa & 1)][mt][pa >> 1], ya = -lv[2 * (pa & 1) + 1][mt][pa >> 1];
             const double xb = -lv[2 * (pb & 1)][mt][pb >> 1], yb = -lv[2 * (pb & 1) + 1][mt][pb >> 1];
-            dst[rot ? pb : pa] = make_double2(rot ? xb : xa, rot ? yb : ya);
+            if (STROM_L_ROT) dst[rot ? pb : pa] = make_double2(rot ? xb : xa, rot ? yb : ya);
+            else dst[pa] = make_double2(xa, ya);
           }
         }
       }
