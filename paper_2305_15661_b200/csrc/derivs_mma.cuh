@@ -48,6 +48,9 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_L_ROT
 #define STROM_L_ROT 1  // rotated conflict-free L stores (selects) vs plain stores (2-way conflicts)
 #endif
+#ifndef STROM_J_FLIP
+#define STROM_J_FLIP 0  // flipped conflict-free J fragment stores (selects): neutral vs plain stores
+#endif
 #ifndef STROM_DRX_ROT
 #define STROM_DRX_ROT 0  // rotated conflict-free dR/dx stores (selects) vs three plain stores
 #endif
@@ -956,7 +959,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     // fragment stores: the lane's two columns in an order flipped by jflip so the 16 lanes
     // of a half-warp (rows c = 0..3 x column pairs k = 0..3, LDJ == 12 mod 16) never collide
     const int jc = (lane >> 2) & 3, jk = lane & 3;
-    const int jflip = jc == 3 ? 1 : ((jc == 1 || jc == 2) ? (jk >> 1) : 0);
+    const int jflip = STROM_J_FLIP ? (jc == 3 ? 1 : ((jc == 1 || jc == 2) ? (jk >> 1) : 0)) : 0;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
