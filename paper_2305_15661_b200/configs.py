@@ -130,8 +130,15 @@ def strip_case(ncell=64, ku=4, kx=2, n_active=10, P=8, seed=1, quad_order=None, 
 
 
 # -- config 2 -----------------------------------------------------------------------
-def euler_square_case(n=256, ku=16, kx=8, seed=2, mach=2.0, quad_order=6):
+def euler_square_case(n=256, ku=16, kx=8, seed=2, mach=2.0, quad_order=6, per_component=True):
     """Element microbench: unit square, 2 n^2 triangles, explicit (U, x) fields.
+
+    The state is freestream x (1 + U(-0.05, 0.05)) per DG node, drawn
+    independently per component (``per_component=True``, the default and the
+    benchmarked input): a factor shared by the four components of a node
+    leaves velocity and sound speed identical on both sides of every face, so
+    every LLF max(ws_in, ws_out) would be an exact tie decided by last-bit
+    rounding (tests/test_gpu_bench_inputs.py).
 
     The state and deformed coordinates enter as the affine offsets of the
     reduced parametrisation (U = U0 + Phi w, x = x_field + Psi tau) at
@@ -141,7 +148,7 @@ def euler_square_case(n=256, ku=16, kx=8, seed=2, mach=2.0, quad_order=6):
     mesh, maps = build_box_mesh(((0.0, 0.0), (1.0, 1.0)), n, n, degree_sol=2, n_comp=4)
     rng = np.random.default_rng(seed)
     nb = 6
-    U0 = freestream_field(rng, mesh.num_elements, nb, mach)
+    U0 = freestream_field(rng, mesh.num_elements, nb, mach, per_component=per_component)
     x = (mesh.nodes + displacement(rng, mesh.nodes, 1.0 / n)).ravel()
     phi = orthonormal(rng, maps.n_global_state, ku)
     psi = orthonormal(rng, maps.n_global_coord, kx)

@@ -385,6 +385,8 @@ static __device__ int lm_after_solve(const LmRun& R, int p, LmState& s, int act,
   if (!isfinite(gd) || gd >= 0.0) return lm_escalate(R, p, s, A, rhs, false);
   s.gdot = gd;
   for (int i = 0; i < K; ++i) R.dw[p * K + i] = x[i];
+  // no backtracking budget: the Armijo loop posts nothing and J_new stays None (lm.py:226-241)
+  if (R.cfg.max_backtracks <= 0) return lm_escalate(R, p, s, A, rhs, false);
   s.j0 = 0;
   s.phase = PH_MAIN_LS;
   s.ntr = min(R.nb_first, R.cfg.max_backtracks);

@@ -64,8 +64,12 @@ def indicators(op, mus, W, Tau):
     Mu = torch.as_tensor(np.stack([op._mu(m) for m in np.atleast_2d(mus)])).to(op.device)
     W = torch.as_tensor(np.asarray(W, float)).to(op.device)
     Tau = torch.as_tensor(np.asarray(Tau, float)).to(op.device)
-    out, _ = op.eval_batched(_lib.RESNORM2, W, Tau, Mu, None)
-    return torch.sqrt(out).cpu().numpy()
+    degen = torch.zeros(Mu.shape[0], dtype=torch.int32, device=op.device)
+    out, _ = op.eval_batched(_lib.RESNORM2, W, Tau, Mu, None, degen=degen)
+    # a degenerate reconstructed mesh is a failed candidate: the reference's
+    # assemble_global raises DegenerateMappingError there (dg.py:177-178)
+    ind = torch.sqrt(out).cpu().numpy()
+    return np.where(degen.cpu().numpy() > 0, np.inf, ind)
 
 
 def greedy_step(op, cand_mus, selected, rho, W0=None, Tau0=None, lm_config=None, rank=0, world=1, group=None):
@@ -80,5 +84,8 @@ def greedy_step(op, cand_mus, selected, rho, W0=None, Tau0=None, lm_config=None,
     W = np.stack([r.w for r in res])
     Tau = np.stack([r.tau for r in res])
     ind = indicators(op, np.asarray(cand_mus)[ids], W, Tau)
-    ind = np.where([np.isfinite(r.objective) for r in res], ind, np.inf)
+    # per-candidate solver failures count as +inf: a non-finite objective or a
+    # solve that ended on a degenerate mapping (lm.py:150,231 catch DegenerateMappingError)
+    failed = np.array([(not np.isfinite(r.objective)) or r.reason == "degenerate" for r in res])
+    ind = np.where(failed, np.inf, ind)
     return global_argmax(ind, ids, selected, group)

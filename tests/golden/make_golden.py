@@ -36,7 +36,7 @@ from paper_2305_15661_b200 import configs, laws as L, tables  # noqa: E402
 
 L.register_dual_backend(sdual.Dual, sdual)
 tables.install_degree6_rule(squad)
-OUT = os.path.dirname(os.path.abspath(__file__))
+OUT = os.environ.get("GOLDEN_OUT", os.path.dirname(os.path.abspath(__file__)))
 
 
 class OffsetOperator(sred.ReducedOperator):
@@ -145,7 +145,7 @@ def save(name, d):
 
 
 def case_strip():
-    case = configs.strip_case(ncell=16, n_active=10, P=3, seed=11)
+    case = configs.strip_case(ncell=16, n_active=10, P=3, seed=11, boundary_in_sample=False)
     rng = np.random.default_rng(111)
     w = rng.standard_normal(4) * 3.0
     tau = rng.standard_normal(2) * 1e-2
@@ -157,7 +157,7 @@ def case_strip():
 
 
 def case_euler_square(quad_order, name):
-    case = configs.euler_square_case(n=4, ku=16, kx=8, seed=12, quad_order=quad_order)
+    case = configs.euler_square_case(n=4, ku=16, kx=8, seed=12, quad_order=quad_order, per_component=False)
     rng = np.random.default_rng(112)
     w = rng.standard_normal(16) * 0.05
     tau = rng.standard_normal(8) * 1e-3
@@ -202,7 +202,7 @@ def case_reference_law(law, name, p, box, nx, ny, mu, ku, kx, seed):
 
 
 def case_degenerate():
-    case = configs.euler_square_case(n=4, ku=4, kx=2, seed=14, quad_order=6)
+    case = configs.euler_square_case(n=4, ku=4, kx=2, seed=14, quad_order=6, per_component=False)
     x = case.ref_coords.reshape(-1, 2).copy()
     node = 1 * 5 + 2  # interior node (i=2, j=1)
     x[node, 0] += 0.6  # pushed across the neighbouring cells -> inverted triangles
