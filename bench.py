@@ -9,17 +9,24 @@ seeded orthonormal; one step = one full reduced derivatives pass
 all elements, rho = 1) — ``ReducedOperator.derivatives`` (strom/reduced.py:
 209-229).
 
+The same JSON line carries "gn": the second half of BASELINE.json's metric,
+ROM Gauss-Newton solves/s on config 3 (40k-triangle half-cylinder sector,
+k_u=20, k_x=10, 800 EQP elements, 64 mu per batch, LM max_iters=30).
+
 Arms:
   default            this repo's CUDA path; ``value`` = elements/s with inputs
                      resident in HBM (Phi alone is 403 MB > 126 MB L2, so no
                      L2 flush is needed); ``e2e`` = the same metric through
                      GpuReducedOperator.derivatives with host numpy inputs
                      (H2D of w, tau, mu and D2H of J,S,T,H inside the timed
-                     region).
-  --impl reference   the reference algorithm on the host CPU: the oracle port
-                     (numpy restatement of strom's dual-number path,
-                     oracle/) on a bounded sample of config-2 elements, one
-                     process per host core.
+                     region).  ``cpu_baseline`` (rank 0, N=1): the arm below on a
+                     bounded sample.
+  --impl reference   the reference's CPU path on all host cores: the UNMODIFIED
+                     strom installed in baseline/_ref (oracle/strom_ref.py),
+                     ``ReducedOperator.derivatives`` on a bounded sample of
+                     config-2-generator elements per process, and stock
+                     ``lm_solve`` on config-3 mu for "gn"; the oracle port
+                     (oracle/) only if the install is missing.
 Multi-GPU (torchrun): elements are split into contiguous ranges, each rank
 reduces its range and the 1+K+K^2 sums are all-reduced over NCCL
 (strong scaling; max-over-ranks device time).
@@ -38,7 +45,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "element residual+Jacobian+projection evals/sec (fp64)"
+METRIC = "element residual+Jacobian+projection evals/sec (fp64)"  # first half of BASELINE.json's metric; GN solves/s in "gn"
 UNIT = "elements/s"
 FP64_PEAK_TFLOPS = None  # filled from profiles/fp64_peak_r01.json
 
@@ -118,42 +125,63 @@ def dist_env():
 _WORKER = {}
 
 
-def _cpu_init(n, seed):
-    """Pool initializer: build a cfg2-shaped oracle problem once per process."""
+def _cpu_init(n, seed, kind):
+    """Pool initializer: build a cfg2-shaped problem once per process (stock reference or port)."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    import oracle.dual  # noqa: F401
-    from oracle.element import OracleGeometry, OracleReducedOperator
     from paper_2305_15661_b200 import configs
 
     case = configs.euler_square_case(n=n, seed=seed)
-    geom = OracleGeometry(case.mesh, case.maps, case.quad_order)
-    op = OracleReducedOperator(case.law, geom, case.phi, case.psi, case.ref_coords, case.kappa, case.eps,
-                               state_offset=case.state_offset)
-    op.derivatives(case.W[0], case.Tau[0], case.mus[0], None)  # warm caches (eta_ref, einsum paths)
-    _WORKER.update(case=case, op=op)
+    if kind == "reference":
+        from oracle import strom_ref
+
+        op = strom_ref.operator(case)
+        c = strom_ref.coords(case.W[0], case.Tau[0])
+        call = lambda: op.derivatives(c, case.mus[0])  # noqa: E731  (reduced.py:209-229, stock)
+    else:
+        import oracle.dual  # noqa: F401
+        from oracle.element import OracleGeometry, OracleReducedOperator
+
+        geom = OracleGeometry(case.mesh, case.maps, case.quad_order)
+        op = OracleReducedOperator(case.law, geom, case.phi, case.psi, case.ref_coords, case.kappa, case.eps,
+                                   state_offset=case.state_offset)
+        call = lambda: op.derivatives(case.W[0], case.Tau[0], case.mus[0], None)  # noqa: E731
+    call()  # warm caches (element slices, geometry tables, einsum paths)
+    _WORKER.update(case=case, call=call)
 
 
 def _cpu_step(_):
-    case, op = _WORKER["case"], _WORKER["op"]
+    case, call = _WORKER["case"], _WORKER["call"]
     t0 = time.perf_counter()
-    op.derivatives(case.W[0], case.Tau[0], case.mus[0], None)
+    call()
     return case.mesh.num_elements, time.perf_counter() - t0
 
 
-class CpuArm:
-    """Oracle port (numpy restatement of strom's dual-number derivatives) on all host cores.
+def cpu_kind():
+    """"reference" when the unmodified strom is importable (baseline/_ref), else "port"."""
+    from oracle import strom_ref
 
-    Each process owns a 2 n^2-element config-2-shaped mesh (same p, rules,
-    k_u, k_x, law -> same per-element work as config 2); one step = one
-    derivatives pass in every process.
+    return "reference" if strom_ref.locate() else "port"
+
+
+class CpuArm:
+    """The reference's CPU derivatives path on all host cores.
+
+    kind "reference": the unmodified ``strom`` installed in baseline/_ref,
+    ``ReducedOperator.derivatives`` on its own dual numbers (oracle/strom_ref.py
+    lists the plugin-level additions: Euler law spec, 12-point rule, state
+    offset); kind "port": the oracle restatement (oracle/), used only when the
+    install is missing.  Each process owns a 2 n^2-element config-2-shaped mesh
+    (same p, rules, k_u, k_x, law, generator -> same per-element work as
+    config 2); one step = one derivatives pass in every process.
     """
 
-    def __init__(self, cores=None, n=16):
+    def __init__(self, cores=None, n=16, kind=None):
         import multiprocessing as mp
 
         self.cores = cores or os.cpu_count() or 1
         self.n = n
-        self.pool = mp.get_context("spawn").Pool(self.cores, initializer=_cpu_init, initargs=(n, 100))
+        self.kind = kind or cpu_kind()
+        self.pool = mp.get_context("spawn").Pool(self.cores, initializer=_cpu_init, initargs=(n, 100, self.kind))
 
     def step(self):
         t0 = time.perf_counter()
@@ -165,8 +193,9 @@ class CpuArm:
         self.pool.join()
 
     def describe(self, steps):
-        return (f"{self.cores} processes x {steps} derivatives pass(es) over {2 * self.n * self.n} cfg2-shaped elements "
-                f"each (Euler p=2, 12/4 rules, k_u=16, k_x=8)")
+        what = "stock strom ReducedOperator.derivatives" if self.kind == "reference" else "oracle port of strom's derivatives"
+        return (f"{what}: {self.cores} processes x {steps} pass(es) over {2 * self.n * self.n} cfg2-generator elements "
+                f"each (Euler p=2, 12/4 rules, k_u=16, k_x=8, W=Tau=0)")
 
 
 def cpu_baseline(n=16, steps=3):
@@ -179,11 +208,83 @@ def cpu_baseline(n=16, steps=3):
             elems, wall = elems + e, wall + t
     finally:
         arm.close()
-    return {"value": elems / wall, "unit": UNIT, "cores": arm.cores, "kind": "port",
+    return {"value": elems / wall, "unit": UNIT, "cores": arm.cores, "kind": arm.kind,
             "sample": arm.describe(steps) + f"; {elems} element evals in {wall:.1f}s wall"}
 
 
+# -- ROM Gauss-Newton solves (config 3), the second half of the BASELINE metric ----------------
+GN_METRIC = "ROM Gauss-Newton solves/sec (fp64)"
+GN_UNIT = "solves/s"
+GN_ITERS = 30
+
+
+def _gn_init(kind):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from paper_2305_15661_b200 import configs
+
+    case = configs.cfg3()
+    if kind == "reference":
+        from oracle import strom_ref
+
+        op = strom_ref.operator(case)
+        solve = lambda mu: strom_ref.lm_solve(op, mu, case.rho, case.W[0], GN_ITERS)  # noqa: E731 (lm.py:164, stock)
+        op.objective(strom_ref.coords(case.W[0], case.Tau[0]), case.mus[0], strom_ref.weights(case.rho))  # slices
+    else:
+        import oracle.dual  # noqa: F401
+        from oracle import lm as olm
+        from oracle.element import OracleGeometry, OracleReducedOperator
+
+        op = OracleReducedOperator(case.law, OracleGeometry(case.mesh, case.maps, case.quad_order), case.phi,
+                                   case.psi, case.ref_coords, case.kappa, case.eps)
+        solve = lambda mu: olm.lm_solve(olm.OracleProblem(op, mu, case.rho, case.W[0]), olm.LmConfig(max_iters=GN_ITERS))  # noqa: E731
+    _WORKER.update(gn_case=case, gn_solve=solve)
+
+
+def _gn_step(i):
+    case, solve = _WORKER["gn_case"], _WORKER["gn_solve"]
+    t0 = time.perf_counter()
+    r = solve(case.mus[i])
+    return time.perf_counter() - t0, int(r.n_iters), str(r.reason)
+
+
+def gn_cpu_baseline(max_procs=16):
+    """Stock ``strom.lm.lm_solve`` (max_iters=30) on the first min(cores, 16) config-3 mu, one
+    full solve per process, all in parallel: solves / wall seconds."""
+    import multiprocessing as mp
+
+    kind = cpu_kind()
+    n = max(1, min(os.cpu_count() or 1, max_procs))
+    pool = mp.get_context("spawn").Pool(n, initializer=_gn_init, initargs=(kind,))
+    try:
+        pool.map(time.sleep, [0.0] * n, chunksize=1)  # initializers done
+        t0 = time.perf_counter()
+        res = pool.map(_gn_step, range(n), chunksize=1)
+        wall = time.perf_counter() - t0
+    finally:
+        pool.close()
+        pool.join()
+    it = [r[1] for r in res]
+    what = "stock strom lm_solve" if kind == "reference" else "oracle port of strom lm_solve"
+    return {"value": n / wall, "unit": GN_UNIT, "cores": n, "kind": kind,
+            "sample": f"{what}: {n} of the 64 config-3 mu, one full solve (max_iters={GN_ITERS}, w0 lsq) per process, "
+                      f"{wall:.1f}s wall; iterations mean {np.mean(it):.1f}; per-solve {np.mean([r[0] for r in res]):.1f}s"}
+
+
 # ---------------------------------------------------------------------------------
+def cfg2_config(n, ku, kx, world):
+    return {"workload": "cfg2: Euler p=2, 12/4-point rules, 2x%dx%d triangles, k_u=%d, k_x=%d, rho=1, one derivatives pass per step" % (n, n, ku, kx),
+            "elements": 2 * n * n, "n_u": 24, "K": ku + kx,
+            "state": "freestream x (1+U(-0.05,0.05)) per DG node and component (no LLF wavespeed ties; DESIGN.md §6)",
+            "l2": "inputs larger than L2 (Phi %.0f MB)" % (2 * n * n * 24 * ku * 8 / 1e6),
+            "parallelism": f"element-range x{world}" + (" + NCCL all_reduce of 1+K+K^2 sums" if world > 1 else "")}
+
+
+def gn_config(world):
+    return {"workload": "cfg3: half-cylinder sector 100x200 quads = 40,000 triangles, Euler p=2, k_u=20, k_x=10, "
+                        "800 EQP elements (2%%), 64 mu ~ U[2,4] per batch, LM max_iters=%d, w0 = Phi^T U_ff(3) + lsq state init" % GN_ITERS,
+            "parallelism": f"mu batches x{world} (each rank its own 64-mu batch, no collective)"}
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -199,16 +300,100 @@ def run_reference(args):
     finally:
         arm.close()
     value = elems / wall
+    cfg = cfg2_config(args.n, 16, 8, 1)
+    cfg["sample_elements_per_step"] = elems // args.steps
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-            "impl": "reference",
-            "config": {"workload": "cfg2: Euler p=2, 12/4-point rules, k_u=16, k_x=8 — bounded CPU sample of cfg2-shaped elements",
-                       "sample_elements_per_step": elems // args.steps},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": arm.cores, "kind": "port",
+            "impl": "reference", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": arm.cores, "kind": arm.kind,
                              "sample": arm.describe(args.steps)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not args.no_gn:
+        g = gn_cpu_baseline()
+        line["gn"] = {"metric": GN_METRIC, "value": g["value"], "unit": GN_UNIT, "higher_is_better": True,
+                      "config": gn_config(1), "cpu_baseline": g,
+                      "e2e": {"value": g["value"], "unit": GN_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def run_gn(args, dev, world, rank, local):
+    """Config 3: batched ROM Gauss-Newton (LM) solves of 64 mu per step on this rank.
+
+    value: device-resident (strom_lm_solve on device buffers; W reset from w0 inside the
+    timed region), CUDA events on the launching stream, max over ranks; e2e: the public
+    ``lm_solve_batched`` with host numpy mu / w0 in and LmResult objects out, wall clock."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_15661_b200 import configs
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.lm import REASONS, LmConfig, lm_solve_batched, lm_solve_device
+    from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases
+
+    case = configs.cfg3()
+    mus = case.mus if rank == 0 else np.random.default_rng(1000 + rank).uniform(2.0, 4.0, size=case.mus.shape)
+    op = GpuReducedOperator(case.law, case.geom, ReducedBases(case.phi, case.psi, case.ref_coords), case.dist, device=dev)
+    rho = WeightVector(case.rho)
+    cfg = LmConfig(max_iters=GN_ITERS)
+    P, ku, kx = len(mus), op.k_u, op.k_x
+    Mu = torch.as_tensor(mus, dtype=torch.float64).to(dev)
+    W0 = torch.as_tensor(np.tile(case.W[0], (P, 1))).to(dev)
+    W = torch.empty_like(W0)
+    Tau = torch.zeros((P, kx), dtype=torch.float64, device=dev)
+    status = torch.zeros((P, 8), dtype=torch.float64, device=dev)
+
+    def step():
+        W.copy_(W0)
+        Tau.zero_()
+        lm_solve_device(op, W, Tau, Mu, rho, cfg, status)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    steps = max(3, args.gn_steps)
+    clk = Clocks(local)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    stat = status.cpu().numpy()
+    # e2e through the public API (host numpy in, LmResult out)
+    lm_solve_batched(op, mus, case.W[0], None, rho, cfg, want_history=False)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = lm_solve_batched(op, mus, case.W[0], None, rho, cfg, want_history=False)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([ms, e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_s = float(t[0]), float(t[1])
+    reasons = {}
+    for r in stat[:, 5]:
+        reasons[REASONS[int(r)]] = reasons.get(REASONS[int(r)], 0) + 1
+    assert all(np.isfinite(r.objective) for r in res)
+    return {"metric": GN_METRIC, "value": world * P * steps / (ms / 1e3), "unit": GN_UNIT, "higher_is_better": True,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": ms / steps, "solves_per_step": world * P,
+            "config": gn_config(world), "scaling": "weak",
+            "iterations": {"mean": float(stat[:, 4].mean()), "max": int(stat[:, 4].max()), "reasons": reasons},
+            "lm_rounds_last": int(_lib_rounds(op)), "clocks": clocks,
+            "e2e": {"value": world * P * steps / e2e_s, "unit": GN_UNIT, "h2d_bytes_per_step": 8 * P * (1 + ku + kx),
+                    "d2h_bytes_per_step": 8 * P * (ku + kx + 8)}}
+
+
+def _lib_rounds(op):
+    from paper_2305_15661_b200 import _lib
+
+    f = getattr(_lib.load(), "strom_lm_rounds", None)
+    return f(op._h) if f is not None else -1
 
 
 def run_mine(args):
@@ -317,6 +502,7 @@ def run_mine(args):
         e2e_value = ne * args.steps / float(tt[0])
         n_out = 1 + ku + kx + ku * ku + ku * kx + kx * kx
         e2e_io = (8 * (ku + kx + op.n_mu) + 8 * n_out, 2 * 8 * n_out + 4)
+    gn = None if args.no_gn else run_gn(args, dev, world, rank, local)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -337,9 +523,7 @@ def run_mine(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded: perturbed freestream state, sinusoidal mesh displacement, Gaussian-QR bases)",
-        "config": {"workload": "cfg2: Euler p=2, 12/4-point rules, 2x%dx%d triangles, k_u=%d, k_x=%d, rho=1, one derivatives pass per step" % (n, n, ku, kx),
-                   "elements": ne, "n_u": nu, "K": K, "l2": "inputs larger than L2 (Phi %.0f MB)" % (case.phi.nbytes / 1e6),
-                   "parallelism": f"element-range x{world}" + (" + NCCL all_reduce of 1+K+K^2 sums" if world > 1 else "")},
+        "config": cfg2_config(n, ku, kx, world),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "derivs_mma_kernel<Euler,12,16,8>",
                      "flops_per_element": F, "flops_per_launch": per_launch_flops,
@@ -350,8 +534,12 @@ def run_mine(args):
     }
     if e2e_value is not None:
         line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_io[0], "d2h_bytes_per_step": e2e_io[1]}
+    if gn is not None:
+        line["gn"] = gn
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(n=args.cpu_n)
+        if gn is not None:
+            gn["cpu_baseline"] = gn_cpu_baseline()
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -366,6 +554,8 @@ def main():
     ap.add_argument("--cells", "--n", dest="n", type=int, default=256, help="cells per side of the unit square (cfg2: 256)")
     ap.add_argument("--cpu-n", type=int, default=16, help="CPU-baseline sample: cells per side per process")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gn", action="store_true", help="skip the config-3 Gauss-Newton solves/s measurement")
+    ap.add_argument("--gn-steps", type=int, default=20, help="timed 64-mu LM batches of the GN measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -98,6 +98,22 @@ class ReducedTrackingProblem:
         return self.op.derivatives(ReducedCoords(w, tau), self.mu, self.rho)
 
 
+def lm_solve_device(op, W, Tau, Mu, rho, config, status, hist=None, w0_mode="lsq"):
+    """Device-resident batched solve: W (P, k_u) / Tau (P, k_x) cuda float64 tensors are
+    overwritten with the solutions, ``status`` (P, 8) and ``hist`` (P, max_iters+1, 6) filled;
+    stream-ordered on the current stream (strom_lm_solve, include/strom_b200.h)."""
+    P, kx = int(Mu.shape[0]), op.k_x
+    act, rw, A = op._weights(rho)
+    packed = config.packed(w0_mode)
+    stream = torch.cuda.current_stream(op.device).cuda_stream
+    rc = _lib.load().strom_lm_solve(op._h, W.data_ptr(), Tau.data_ptr() if kx else W.data_ptr(), Mu.data_ptr(), P,
+                                    act.data_ptr() if act is not None else None,
+                                    rw.data_ptr() if rw is not None else None, A, packed.ctypes.data,
+                                    status.data_ptr(), hist.data_ptr() if hist is not None else None, stream)
+    _lib.check(rc, "strom_lm_solve")
+    op.stats["lm_solves"] = op.stats.get("lm_solves", 0) + P
+
+
 def lm_solve_batched(op, mus, W0=None, Tau0=None, rho=None, config=None, w0_mode="lsq", want_history=True,
                      raise_degenerate=False):
     """Solve P reduced problems (one per row of ``mus``) on the GPU at once."""
@@ -112,17 +128,9 @@ def lm_solve_batched(op, mus, W0=None, Tau0=None, rho=None, config=None, w0_mode
     Mu = torch.as_tensor(np.stack([op._mu(m) for m in mus])).to(dev)
     W = torch.as_tensor(np.zeros((P, ku)) if W0 is None else np.broadcast_to(np.asarray(W0, float), (P, ku)).copy()).to(dev)
     Tau = torch.as_tensor(np.zeros((P, kx)) if Tau0 is None else np.broadcast_to(np.asarray(Tau0, float), (P, kx)).copy()).to(dev)
-    act, rw, A = op._weights(rho)
     status = torch.zeros((P, 8), dtype=torch.float64, device=dev)
     hist = torch.zeros((P, cfg.max_iters + 1, 6), dtype=torch.float64, device=dev) if want_history else None
-    packed = cfg.packed(w0_mode)
-    stream = torch.cuda.current_stream(dev).cuda_stream
-    lib = _lib.load()
-    rc = lib.strom_lm_solve(op._h, W.data_ptr(), Tau.data_ptr() if kx else W.data_ptr(), Mu.data_ptr(), P,
-                            act.data_ptr() if act is not None else None, rw.data_ptr() if rw is not None else None, A,
-                            packed.ctypes.data, status.data_ptr(), hist.data_ptr() if hist is not None else None, stream)
-    _lib.check(rc, "strom_lm_solve")
-    op.stats["lm_solves"] = op.stats.get("lm_solves", 0) + P
+    lm_solve_device(op, W, Tau, Mu, rho, cfg, status, hist, w0_mode)
     Wh, Th, st = W.cpu().numpy(), Tau.cpu().numpy(), status.cpu().numpy()
     H = hist.cpu().numpy() if hist is not None else None
     out = []

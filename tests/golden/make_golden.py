@@ -217,6 +217,50 @@ def case_degenerate():
     save("degenerate", out)
 
 
+def case_cfg1():
+    """Config 1 exactly as BASELINE states it: 64 cells, 10 EQP elements, 8 mu, full LM solves."""
+    case = configs.strip_case()
+    op, rm, rmaps, geom = operator(case)
+    out = inputs_of(case, case.W[0], case.Tau[0])
+    lm_runs(case, op, case.mus, out, max_iters=200)
+    save("cfg1", out)
+
+
+def case_sector_shape(name, n_radial, n_circ, ku, kx, frac, P, seed, max_iters):
+    """Config 3 / 5 reduced dimensions (K = 30 / 36, the specialised DMMA kernels) on a reduced
+    sector mesh: LM histories of the reference for P mu."""
+    case = configs.sector_rom_case(n_radial=n_radial, n_circ=n_circ, ku=ku, kx=kx, frac_active=frac,
+                                   rho_scale=1.0 / frac, P=P, seed=seed)
+    op, rm, rmaps, geom = operator(case)
+    out = inputs_of(case, case.W[0], case.Tau[0])
+    out["nrnc"] = np.array([n_radial, n_circ])
+    lm_runs(case, op, case.mus, out, w0=case.W[0], max_iters=max_iters)
+    save(name, out)
+
+
+def case_lprows():
+    """Config 4 LP rows at (k_u, k_x) = (20, 10): per snapshot s the element contributions
+    S_e, T_e (reduced.py:231-251) and 0.5 (|R_e|^2 + N_e^2) at explicit (U_s, x_s)."""
+    case = configs.sector_rom_case(n_radial=6, n_circ=10, ku=20, kx=10, frac_active=0.2, rho_scale=5.0, P=2, seed=41)
+    mus, U, X = configs.snapshot_fields(case, 3, seed=42)
+    ne = case.mesh.num_elements
+    out = inputs_of(case, np.zeros(20), np.zeros(10))
+    out.update(snap_mus=mus, snap_U=U, snap_X=X)
+    rows = np.zeros((3, 31, ne))
+    for s in range(3):
+        case.state_offset, case.ref_coords = U[s], X[s]
+        op, rm, rmaps, geom = operator(case)
+        c = sred.ReducedCoords(np.zeros(20), np.zeros(10))
+        Se, Te = op.elemental_contributions(c, mus[s])
+        rows[s, :20], rows[s, 20:30] = Se.T, Te.T
+        for e in range(ne):  # the element objective: the weighted objective at a one-hot weight
+            wv = np.zeros(ne)
+            wv[e] = 1.0
+            rows[s, 30, e] = op.objective(c, mus[s], WeightVector(wv))
+    out["lprows"] = rows
+    save("lprows", out)
+
+
 if __name__ == "__main__":
     case_strip()
     case_euler_square(6, "euler_square_q6")
@@ -227,3 +271,7 @@ if __name__ == "__main__":
     case_reference_law(slaw.linear_advection((1.0, 0.5)), "linadv_p2", 2, ((0.0, 0.0), (1.0, 1.0)), 3, 3, (0.5,), 5, 3, 17)
     case_reference_law(slaw.linear_advection((-0.7, 1.0)), "linadv_p1", 1, ((0.0, 0.0), (1.0, 1.0)), 4, 2, (0.5,), 4, 2, 18)
     case_degenerate()
+    case_cfg1()
+    case_sector_shape("sector_k30", 6, 12, 20, 10, 0.25, 4, 51, 30)
+    case_sector_shape("sector_k36", 6, 12, 24, 12, 0.25, 3, 52, 15)
+    case_lprows()
