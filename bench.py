@@ -365,6 +365,7 @@ def run_gn(args, dev, world, rank, local):
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
     stat = status.cpu().numpy()
+    lm_stats = _lm_stats(op)
     # e2e through the public API (host numpy in, LmResult out)
     lm_solve_batched(op, mus, case.W[0], None, rho, cfg, want_history=False)
     torch.cuda.synchronize()
@@ -384,16 +385,20 @@ def run_gn(args, dev, world, rank, local):
             "steps": steps, "warmup": args.warmup, "ms_per_step": ms / steps, "solves_per_step": world * P,
             "config": gn_config(world), "scaling": "weak",
             "iterations": {"mean": float(stat[:, 4].mean()), "max": int(stat[:, 4].max()), "reasons": reasons},
-            "lm_rounds_last": int(_lib_rounds(op)), "clocks": clocks,
+            "lm_graph_last_batch": lm_stats, "clocks": clocks,
             "e2e": {"value": world * P * steps / e2e_s, "unit": GN_UNIT, "h2d_bytes_per_step": 8 * P * (1 + ku + kx),
                     "d2h_bytes_per_step": 8 * P * (ku + kx + 8)}}
 
 
-def _lib_rounds(op):
+def _lm_stats(op):
+    """(control rounds, derivative passes, objective passes) of the op's last batched solve."""
+    import ctypes
+
     from paper_2305_15661_b200 import _lib
 
-    f = getattr(_lib.load(), "strom_lm_rounds", None)
-    return f(op._h) if f is not None else -1
+    out = (ctypes.c_int32 * 3)()
+    _lib.check(_lib.load().strom_lm_stats(op._h, out), "strom_lm_stats")
+    return {"rounds": out[0], "derivative_passes": out[1], "objective_passes": out[2]}
 
 
 def run_mine(args):

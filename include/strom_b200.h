@@ -120,11 +120,18 @@ int strom_degenerate_elements(strom_handle* h, int32_t p, int32_t* ids, int32_t 
  * ratio_lo, max_iters, wolfe_c1, wolfe_c2, max_backtracks, lambda_cap,
  * w0_inner_tol, w0_inner_iters) plus w0_mode (0 keep, 1 lsq) as a 15th.
  * status: (P, 8) doubles out: converged, objective, |S|, |T|, n_iters,
- * reason (0 first-order, 1 max-iters, 2 line-search-failure), lambda, evals.
+ * reason (0 first-order, 1 max-iters, 2 line-search-failure, 3 degenerate), lambda,
+ * evaluation requests.  Returns -3 if the round guard is exhausted.
  * history: (P, max_iters+1, 6) doubles out or NULL. */
 int strom_lm_solve(strom_handle* h, double* w, double* tau, const double* mu, int32_t P,
                    const int32_t* active, const double* rho, int32_t A, const double* cfg,
                    double* status, double* history, void* stream);
+
+/* Statistics of the last strom_lm_solve on this handle: out3 = (control rounds,
+ * derivative passes, objective passes).  The rounds run device-resident as one
+ * CUDA graph (a WHILE node over the control round with IF nodes for the two
+ * batched passes), so these counts are read back once per solve batch. */
+int strom_lm_stats(strom_handle* h, int32_t* out3);
 
 /* Benchmark probe: while enabled, the dominant kernel of every strom_eval is
  * bracketed by CUDA events recorded on the call's stream (capacity 4096

@@ -29,7 +29,7 @@ class DistDesc(C.Structure):
 
 
 EXPORTS = ("strom_create", "strom_set_bases", "strom_set_offsets", "strom_reserve", "strom_eval", "strom_degenerate_elements",
-           "strom_lm_solve", "strom_profile", "strom_profile_ms", "strom_last_error", "strom_destroy")
+           "strom_lm_solve", "strom_lm_stats", "strom_profile", "strom_profile_ms", "strom_last_error", "strom_destroy")
 
 _lib = None
 
@@ -55,6 +55,7 @@ def load(path=SO_PATH):
     lib.strom_eval.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp, i32]
     lib.strom_degenerate_elements.argtypes = [vp, i32, vp, i32]
     lib.strom_lm_solve.argtypes = [vp, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp, vp]
+    lib.strom_lm_stats.argtypes = [vp, vp]
     lib.strom_profile.argtypes = [vp, i32]
     lib.strom_profile_ms.argtypes = [vp, C.POINTER(i32)]
     lib.strom_profile_ms.restype = C.c_double

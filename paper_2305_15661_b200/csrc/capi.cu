@@ -219,6 +219,7 @@ extern "C" void strom_destroy(strom_handle* h) {
   if (h->degen_fill) cudaFree(h->degen_fill);
   if (h->degen_scratch) cudaFree(h->degen_scratch);
   lm_free(h->lm);
+  if (h->lm_stream) cudaStreamDestroy(h->lm_stream);
   for (auto& e : h->ev) cudaEventDestroy(e);
   delete h;
 }

@@ -167,8 +167,22 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   __shared__ __align__(16) double s_dphi[NQ * NB * 2];
   __shared__ int s_tile[15];  // upper 8x8 tiles of the Gram (KP <= 40): (ti << 4) | tj
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int p = blockIdx.y;
-  if (r.mask && !r.mask[p]) return;
+  // CTA -> (parameter row, element chunk): grid (gx, P) with a row mask, or a device-sized
+  // 1-D grid over the live rows list[0 .. *dyn_count) (graph-resident LM rounds)
+  int p, prow_, bx, gxr;
+  if (r.dyn_count) {
+    const int live = *r.dyn_count;
+    gxr = dyn_gx(r.dyn_target, r.dyn_maxb, r.dyn_ceil, live);
+    prow_ = blockIdx.x / gxr;
+    bx = blockIdx.x - prow_ * gxr;
+    if (prow_ >= live) return;
+    p = r.list[prow_];
+  } else {
+    p = prow_ = blockIdx.y;
+    bx = blockIdx.x;
+    gxr = gridDim.x;
+    if (r.mask && !r.mask[p]) return;
+  }
   constexpr bool CT = KUT > 0;
   const bool DERIVS = DM >= 0 ? DM == 1 : r.mode == MODE_DERIVS;  // compile-time on the specialised path
   constexpr int KT = KUT + KXT, KPT = (KT + 7) / 8 * 8;
@@ -240,13 +254,13 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   // Each iteration loads the next unit's block mid-way and stores it after the Jx
   // stage, so the gather's address chain starts from shared memory.
   int* const EI = reinterpret_cast<int*>(S + SH::MINT);
-  const int ustride = gridDim.x * nwarps;
+  const int ustride = gxr * nwarps;
   auto index_word = [&](int ue, int l) -> int {
     return l == 0 ? ue : (l < 4 ? __ldg(r.elem_nodes + 3 * ue + l - 1)
                                : (l < 7 ? __ldg(r.nbr + 3 * ue + l - 4) : __ldg(r.finfo + 3 * ue + l - 7)));
   };
   {
-    const int idx0 = blockIdx.x * nwarps + warp;
+    const int idx0 = bx * nwarps + warp;
     if (idx0 < nunits && lane < 10) EI[lane] = index_word(r.active ? __ldg(r.active + idx0) : idx0, lane);
     __syncwarp();
     if (PHB && idx0 < nunits) phi_async(EI[0]);
@@ -255,7 +269,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   // lanes 24..31) and row lane + 32 (neighbor rows 8..35 for lanes 0..27)
   const int g0j = (lane - NU) >> 2;                       // lanes >= NU: face-node slot on face 0
   const int g1i = lane + 32 - NU, g1f = g1i / (NF * M), g1j = (g1i / M) % NF;
-  for (int idx = blockIdx.x * nwarps + warp; idx < nunits; idx += ustride) {
+  for (int idx = bx * nwarps + warp; idx < nunits; idx += ustride) {
     const int e = EI[0];
     const double rho = r.active ? r.rho[idx] : 1.0;
     const int nidx = idx + ustride;
@@ -1198,7 +1212,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   }
   __syncthreads();
   const int PSZ = 1 + K + KP * KP;
-  double* dst = r.part + ((size_t)p * gridDim.x + blockIdx.x) * PSZ;
+  double* dst = r.part + ((size_t)prow_ * gxr + bx) * PSZ;
   for (int i = threadIdx.x; i < PSZ; i += blockDim.x) {
     double v = 0.0;
     for (int w = 0; w < nwarps; ++w) {

@@ -110,8 +110,22 @@ __global__ void __launch_bounds__(WTHREADS) derivs_warp_kernel(
   __shared__ double s_w[KMAX], s_tau[KMAX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int h = lane / TPU, k = lane % TPU;
-  const int p = blockIdx.y;
-  if (r.mask && !r.mask[p]) return;
+  // CTA -> (parameter row, element chunk): grid (gx, P) with a row mask, or a device-sized
+  // 1-D grid over the live rows list[0 .. *dyn_count) (graph-resident LM rounds)
+  int p, prow_, bx, gxr;
+  if (r.dyn_count) {
+    const int live = *r.dyn_count;
+    gxr = dyn_gx(r.dyn_target, r.dyn_maxb, r.dyn_ceil, live);
+    prow_ = blockIdx.x / gxr;
+    bx = blockIdx.x - prow_ * gxr;
+    if (prow_ >= live) return;
+    p = r.list[prow_];
+  } else {
+    p = prow_ = blockIdx.y;
+    bx = blockIdx.x;
+    gxr = gridDim.x;
+    if (r.mask && !r.mask[p]) return;
+  }
   const int ku = r.ku, kx = r.kx, K = r.K, KP = r.KP, LDJ = r.LDJ, STR = r.unit_stride;
   double* const Wb = smem + (size_t)warp * r.gx_warp_stride;
   double* const S = Wb + h * STR;
@@ -134,7 +148,7 @@ __global__ void __launch_bounds__(WTHREADS) derivs_warp_kernel(
   const int ngroups = (nunits + UPW - 1) / UPW;
   const int nt8 = KP / 8, ntri = nt8 * (nt8 + 1) / 2;
 
-  for (int grp = blockIdx.x * nwarps + warp; grp < ngroups; grp += gridDim.x * nwarps) {
+  for (int grp = bx * nwarps + warp; grp < ngroups; grp += gxr * nwarps) {
     const int idx = grp * UPW + h;
     const bool valid = idx < nunits;
     const int nvalid = min(UPW, nunits - grp * UPW);
@@ -389,7 +403,7 @@ __global__ void __launch_bounds__(WTHREADS) derivs_warp_kernel(
     for (int i = 0; i < NU; ++i) acc[i] = 0.0;
     {
       // prefetch the next group's basis blocks into L2 while this one computes
-      const int ng = grp + gridDim.x * nwarps;
+      const int ng = grp + gxr * nwarps;
       if (ng < ngroups) {
         const int ni = ng * UPW + h;
         if (ni < nunits) {
@@ -697,7 +711,7 @@ __global__ void __launch_bounds__(WTHREADS) derivs_warp_kernel(
   if (lane == 0) GW[K] = jacc;
   __syncthreads();
   const int PSZ = 1 + K + KP * KP;
-  double* dst = r.part + ((size_t)p * gridDim.x + blockIdx.x) * PSZ;
+  double* dst = r.part + ((size_t)prow_ * gxr + bx) * PSZ;
   for (int i = threadIdx.x; i < PSZ; i += blockDim.x) {
     double v = 0.0;
     for (int w = 0; w < nwarps; ++w) {

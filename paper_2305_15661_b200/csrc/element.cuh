@@ -63,6 +63,10 @@ struct Run {
   const int* __restrict__ mask;  // per-row enable (batched LM), or null
   const int* __restrict__ list;  // value_mu_kernel: compacted enabled rows (nlist of them), or null
   int nlist;
+  // device-sized launch (graph-resident LM rounds): the live row count is read on the device
+  // (*dyn_count rows, list[0 .. count)) and the 1-D grid is split over them there (dyn_gx)
+  const int* __restrict__ dyn_count;
+  int dyn_target, dyn_maxb, dyn_ceil;
   int U;          // units per tile (derivs kernel)
   int ntiles;     // tiles per parameter
   int gx;         // blocks per parameter
@@ -71,6 +75,14 @@ struct Run {
   double kappa, eps;
   double lawp[8];
 };
+
+// CTAs per live row of a device-sized launch: the host formulas of eval_impl.cuh
+// (launch_mma_t: one wave, floor; launch_warp: ceil) evaluated with the device count
+__device__ __forceinline__ int dyn_gx(int target, int maxb, int ceil_div, int live) {
+  live = live > 0 ? live : 1;
+  const int g = ceil_div ? (target + live - 1) / live : target / live;
+  return g < 1 ? 1 : (g > maxb ? maxb : g);
+}
 
 template <int NB, int NQ, int NS, int NF>
 struct Params {

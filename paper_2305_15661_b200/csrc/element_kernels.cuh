@@ -475,15 +475,30 @@ __global__ void __launch_bounds__(128) value_mu_kernel(const __grid_constant__ P
 }
 
 // one warp per parameter row: lane-strided partials, fixed-order shuffle tree (deterministic)
+struct DynRows {  // device-sized launch of the pass being finalized (Run::dyn_*), count == null: static grid
+  const int* count;
+  const int* list;
+  int target, maxb, ceil_div;
+};
+
 static __global__ void sum_partials_kernel(const double* __restrict__ part, int nparts, int P, double* __restrict__ out,
-                                    const int* __restrict__ mask) {
-  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (p >= P || (mask && !mask[p])) return;
-  double s = 0.0;
-  for (int i = lane; i < nparts; i += 32) s += part[(size_t)p * nparts + i];
+                                    const int* __restrict__ mask, DynRows dyn) {
+  // warp per row; device-sized value passes index their partials by the compacted slot
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  int p = s;
+  if (dyn.count) {
+    const int live = *dyn.count;
+    if (s >= live) return;
+    p = dyn.list[s];
+    nparts = dyn_gx(dyn.target, dyn.maxb, 1, (live + 31) / 32);
+  } else if (p >= P || (mask && !mask[p])) {
+    return;
+  }
+  double v = 0.0;
+  for (int i = lane; i < nparts; i += 32) v += part[(size_t)s * nparts + i];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-  if (lane == 0) out[p] = s;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) out[p] = v;
 }
 
 // Sum the per-CTA partials of one derivatives pass and expand the upper Gram tiles
@@ -493,16 +508,23 @@ static __global__ void sum_partials_kernel(const double* __restrict__ part, int 
 // outputs it feeds (H symmetric).
 static __global__ void __launch_bounds__(1024) finalize_derivs_kernel(const double* __restrict__ part, int gx, int K,
                                                                       int KP, int P, double* __restrict__ out,
-                                                                      const int* __restrict__ mask) {
+                                                                      const int* __restrict__ mask, DynRows dyn) {
   __shared__ double red[32][33];
-  const int p = blockIdx.y;
-  if (mask && !mask[p]) return;
+  int p = blockIdx.y, prow = blockIdx.y;
+  if (dyn.count) {  // row slot -> parameter row; the pass split the grid with the same formula
+    const int live = *dyn.count;
+    if (prow >= live) return;
+    p = dyn.list[prow];
+    gx = dyn_gx(dyn.target, dyn.maxb, dyn.ceil_div, live);
+  } else if (mask && !mask[p]) {
+    return;
+  }
   const int PSZ = 1 + K + KP * KP, OSZ = 1 + K + K * K;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int src = blockIdx.x * 32 + lane;
   double s = 0.0;
   if (src < PSZ) {
-    const double* q = part + (size_t)p * gx * PSZ + src;
+    const double* q = part + (size_t)prow * gx * PSZ + src;
     for (int b = w; b < gx; b += nw) s += q[(size_t)b * PSZ];
   }
   red[w][lane] = s;

@@ -32,6 +32,48 @@ static void fill_tabs(const strom_handle* h, Tabs<NB, NQ, NS, NF>& t) {
 }
 
 
+// Launch a derivatives / contribution pass split into `gx` element chunks per parameter row
+// (grid (gx, P), rows masked), or, for a device-sized pass (a.dyn_count: graph-resident LM
+// rounds, row count read on the device), a 1-D grid of target + P CTAs that the kernel splits
+// over the live rows with the same formula (dyn_gx); partials are indexed by the live slot, so
+// their buffer is bounded by (target + P) * PSZ however few rows are live.
+template <class KERN, class PRM>
+static int launch_pass(strom_handle* h, const EvalArgs& a, KERN kern, PRM& prm, int nwarps, size_t smem, int target,
+                       int maxb, int ceil_div) {
+  Run& r = prm.r;
+  const int PSZ = 1 + r.K + r.KP * r.KP;
+  const bool dyn = a.dyn_count != nullptr;
+  int gx = 0;
+  dim3 grid;
+  if (dyn) {
+    r.dyn_count = a.dyn_count; r.list = a.list;
+    r.dyn_target = target; r.dyn_maxb = maxb; r.dyn_ceil = ceil_div;
+    grid = dim3(target + a.P);
+  } else {
+    gx = std::max(1, std::min(maxb, ceil_div ? (target + a.P - 1) / a.P : target / a.P));
+    grid = dim3(gx, a.P);
+  }
+  r.gx = gx;
+  if (a.mode == MODE_DERIVS) {
+    const size_t need = dyn ? (size_t)(target + a.P) * PSZ : (size_t)a.P * gx * PSZ;
+    if (dyn && need > h->part_cap) return fail(-2, "device-sized pass: partial buffer not reserved");
+    if (ensure_part(h, need)) return -2;
+    r.part = h->part;
+  }
+  if (!dyn) prof_mark(h, a.stream, 0);
+  kern<<<grid, nwarps * 32, smem, a.stream>>>(prm);
+  if (!dyn) prof_mark(h, a.stream, 1);
+  CK(cudaGetLastError());
+  if (a.mode == MODE_DERIVS) {
+    const DynRows dr{a.dyn_count, a.list, target, maxb, ceil_div};
+    const int fthreads = dyn ? 1024 : std::min(1024, 32 * std::max(1, std::min(32, gx)));
+    finalize_derivs_kernel<<<dim3((PSZ + 31) / 32, a.P), fthreads, 0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out,
+                                                                                  a.mask, dr);
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
 template <class LAW, int NB, int NQ, int NS, int TPU>
 static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WShape<LAW, NB, NQ, NS>::NF>& prm,
                        int nunits) {
@@ -55,37 +97,10 @@ static int launch_warp(strom_handle* h, const EvalArgs& a, Params<NB, NQ, NS, WS
     c_smem = smem;
     c_dev = h->device;
   }
-  int per_sm = c_per_sm;
-  if (getenv("STROM_DEBUG")) {
-    cudaFuncAttributes fa;
-    CK(cudaFuncGetAttributes(&fa, kern));
-    fprintf(stderr, "[strom] mma kernel attrs: %d regs, %zu B static smem, max dyn %d\n", fa.numRegs, fa.sharedSizeBytes,
-            fa.maxDynamicSharedSizeBytes);
-  }
-  per_sm = std::max(per_sm, 1);
+  const int per_sm = std::max(c_per_sm, 1);
   const int ngroups = (nunits + UPW - 1) / UPW;
-  const int target = h->num_sms * per_sm;
-  const int maxb = std::max(1, (ngroups + nwarps - 1) / nwarps);
-  const int live = a.live > 0 ? a.live : a.P;
-  int gx = std::max(1, std::min(maxb, (target + live - 1) / live));
-  r.gx = gx;
   r.ntiles = ngroups;
-  const int PSZ = 1 + r.K + r.KP * r.KP;
-  if (a.mode == MODE_DERIVS) {
-    if (ensure_part(h, (size_t)a.P * gx * PSZ)) return -2;
-    r.part = h->part;
-  }
-  prof_mark(h, a.stream, 0);
-  kern<<<dim3(gx, a.P), nwarps * 32, smem, a.stream>>>(prm);
-  prof_mark(h, a.stream, 1);
-  CK(cudaGetLastError());
-  if (a.mode == MODE_DERIVS) {
-    const int OSZ = 1 + r.K + r.K * r.K;
-    finalize_derivs_kernel<<<dim3((1 + r.K + r.KP * r.KP + 31) / 32, a.P), std::min(1024, 32 * std::max(1, std::min(32, gx))),
-                             0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
-    CK(cudaGetLastError());
-  }
-  return 0;
+  return launch_pass(h, a, kern, prm, nwarps, smem, h->num_sms * per_sm, std::max(1, (ngroups + nwarps - 1) / nwarps), 1);
 }
 
 template <class LAW, int NQ, int KUT, int KXT>
@@ -98,8 +113,7 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
   r.gx_warp_stride = SH::warp_stride(r.LDJ, r.KP, r.kx, SH::hreg(KUT, KXT), SH::phibuf(KUT));
   const int smem_cap = 227 * 1024;
   const size_t warp_bytes = (size_t)r.gx_warp_stride * sizeof(double);
-  int nwarps = std::min<int>(2, (int)(smem_cap / warp_bytes));  // 2-warp CTAs (measured fastest)
-  if (const char* ev = getenv("STROM_MMA_WARPS")) nwarps = std::max(1, std::min(nwarps, atoi(ev)));
+  const int nwarps = std::min<int>(2, (int)(smem_cap / warp_bytes));  // 2-warp CTAs (measured fastest)
   if (nwarps < 1) return fail(-1, "element does not fit in shared memory");
   const size_t smem = nwarps * warp_bytes;
   auto kern = KUT > 0 ? (a.mode == MODE_DERIVS ? derivs_mma_kernel<LAW, NQ, KUT, KXT, 1> : derivs_mma_kernel<LAW, NQ, KUT, KXT, 0>)
@@ -111,64 +125,25 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
   static int c_dev[2] = {-1, -1}, c_per_sm[2] = {0, 0};
   if (c_smem[ck] != smem || c_dev[ck] != h->device) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (const char* ev = getenv("STROM_MMA_CARVEOUT"))  // experiment knob: shared-memory carveout (%)
-      CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(ev)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per_sm[ck], kern, nwarps * 32, smem));
     c_smem[ck] = smem;
     c_dev[ck] = h->device;
   }
-  int per_sm = c_per_sm[ck];
-  if (getenv("STROM_DEBUG")) {
-    cudaFuncAttributes fa;
-    CK(cudaFuncGetAttributes(&fa, kern));
-    fprintf(stderr, "[strom] mma kernel attrs: %d regs, %zu B static smem, max dyn %d\n", fa.numRegs, fa.sharedSizeBytes,
-            fa.maxDynamicSharedSizeBytes);
-  }
-  per_sm = std::max(per_sm, 1);
+  int per_sm = std::max(c_per_sm[ck], 1);
   // k_u > 16: the larger per-warp footprint leaves too little L1 for the basis rows above
   // 8 warps/SM (measured: cfg3/4/5 fastest at 4 two-warp CTAs per SM; cfg2 at 6)
   if (r.ku > 16) per_sm = std::min(per_sm, 4);
-  if (const char* ev = getenv("STROM_MMA_BPS")) per_sm = std::max(1, std::min(per_sm, atoi(ev)));  // blocks/SM cap
-  const int target = h->num_sms * per_sm;
-  const int maxb = std::max(1, (nunits + nwarps - 1) / nwarps);
-  const int live = a.live > 0 ? a.live : a.P;
-  // one wave: at most `target` co-resident CTAs (a partial second wave doubles the pass time)
-  int gx = std::max(1, std::min(maxb, target / live));
-  if (const char* ev = getenv("STROM_MMA_UPW")) {  // experiment knob: at least this many units per warp
-    const int upw = std::max(1, atoi(ev));
-    gx = std::max(1, std::min(gx, (nunits + nwarps * upw - 1) / (nwarps * upw)));
-  }
-  r.gx = gx;
   r.ntiles = nunits;
-  if (getenv("STROM_DEBUG"))
-    fprintf(stderr, "[strom] mma kernel: %d warps/CTA, %zu B smem/CTA, %d CTAs/SM, grid %d x %d\n", nwarps, smem, per_sm,
-            gx, a.P);
-  const int PSZ = 1 + r.K + r.KP * r.KP;
-  if (a.mode == MODE_DERIVS) {
-    if (ensure_part(h, (size_t)a.P * gx * PSZ)) return -2;
-    r.part = h->part;
-  }
-  prof_mark(h, a.stream, 0);
-  kern<<<dim3(gx, a.P), nwarps * 32, smem, a.stream>>>(prm);
-  prof_mark(h, a.stream, 1);
-  CK(cudaGetLastError());
-  if (a.mode == MODE_DERIVS) {
-    const int OSZ = 1 + r.K + r.K * r.K;
-    finalize_derivs_kernel<<<dim3((1 + r.K + r.KP * r.KP + 31) / 32, a.P), std::min(1024, 32 * std::max(1, std::min(32, gx))),
-                             0, a.stream>>>(h->part, gx, r.K, r.KP, a.P, a.out, a.mask);
-    CK(cudaGetLastError());
-  }
-  return 0;
+  // one wave: at most `target` co-resident CTAs (a partial second wave doubles the pass time)
+  return launch_pass(h, a, kern, prm, nwarps, smem, h->num_sms * per_sm, std::max(1, (nunits + nwarps - 1) / nwarps), 0);
 }
 
 template <class LAW, int NQ>
 static int launch_mma(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& prm, int nunits) {
   // compile-time reduced dimensions for the BASELINE configs (addressing folds to immediates)
-  if (!getenv("STROM_GENERIC_K")) {
-    if (h->ku == 16 && h->kx == 8) return launch_mma_t<LAW, NQ, 16, 8>(h, a, prm, nunits);
-    if (h->ku == 20 && h->kx == 10) return launch_mma_t<LAW, NQ, 20, 10>(h, a, prm, nunits);
-    if (h->ku == 24 && h->kx == 12) return launch_mma_t<LAW, NQ, 24, 12>(h, a, prm, nunits);
-  }
+  if (h->ku == 16 && h->kx == 8) return launch_mma_t<LAW, NQ, 16, 8>(h, a, prm, nunits);
+  if (h->ku == 20 && h->kx == 10) return launch_mma_t<LAW, NQ, 20, 10>(h, a, prm, nunits);
+  if (h->ku == 24 && h->kx == 12) return launch_mma_t<LAW, NQ, 24, 12>(h, a, prm, nunits);
   return launch_mma_t<LAW, NQ, 0, 0>(h, a, prm, nunits);
 }
 
@@ -204,18 +179,10 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
     return 0;
   }
   if (a.mode == MODE_OBJECTIVE || a.mode == MODE_RESNORM2 || a.mode == MODE_RESIDUAL) {
-    const bool multi = a.P >= 8;  // many parameter points: warp per element, lanes over mu
-    const bool listed = multi && a.list != nullptr && a.live > 0;  // lanes over the compacted enabled rows
-    if (listed) { r.list = a.list; r.nlist = a.live; }
-    const int gy = multi ? ((listed ? a.live : a.P) + 31) / 32 : a.P;
-    const int gx = multi ? std::max(1, std::min((nunits + 3) / 4, (h->num_sms * 16 + gy - 1) / gy)) : (nunits + 127) / 128;
-    if (a.mode != MODE_RESIDUAL) {
-      if (ensure_part(h, (size_t)a.P * gx)) return -2;
-      r.part = h->part;
-    }
+    const bool multi = a.P >= 8 && h->ku <= 32;  // many parameter points: warp per element, lanes over mu
+    const bool dyn = multi && a.dyn_count != nullptr;  // lanes over the device-counted compacted rows
     prof_mark(h, a.stream, 0);
-    static const bool old_value = getenv("STROM_VALUE_OLD") != nullptr;
-    if (multi && h->ku <= 32 && !old_value) {
+    if (multi) {
       using VS = VShape<LAW, NB>;
       constexpr int vsmem = (VM_THREADS / 32) * VS::TILE * sizeof(double);
       static int c_dev = -1;
@@ -223,15 +190,42 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
         CK(cudaFuncSetAttribute(value_mma_kernel<LAW, NB, NQ, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, vsmem));
         c_dev = h->device;
       }
-      value_mma_kernel<LAW, NB, NQ, NS><<<dim3(gy, gx), VM_THREADS, vsmem, a.stream>>>(prm);
-    } else if (multi)
-      value_mu_kernel<LAW, NB, NQ, NS><<<dim3(gx, gy), 128, 0, a.stream>>>(prm);
-    else
-      value_kernel<LAW, NB, NQ, NS><<<dim3(gx, a.P), 128, 0, a.stream>>>(prm);
+      // point groups x element chunks of 4 warps; a device-sized pass splits a 1-D grid of
+      // target + groups CTAs over the live groups (dyn_gx with the same target / cap)
+      const int gy = (a.P + 31) / 32, target = h->num_sms * 16, cap = std::max(1, (nunits + 3) / 4);
+      const int gx = std::max(1, std::min(cap, (target + gy - 1) / gy));
+      if (a.mode != MODE_RESIDUAL) {
+        const size_t need = dyn ? (size_t)(target + gy) * 32 : (size_t)a.P * gx;
+        if (dyn && need > h->part_cap) return fail(-2, "device-sized pass: partial buffer not reserved");
+        if (ensure_part(h, need)) return -2;
+        r.part = h->part;
+      }
+      if (dyn) {
+        r.list = a.list; r.dyn_count = a.dyn_count; r.dyn_target = target; r.dyn_maxb = cap; r.dyn_ceil = 1;
+        value_mma_kernel<LAW, NB, NQ, NS><<<dim3(target + gy), VM_THREADS, vsmem, a.stream>>>(prm);
+      } else {
+        if (a.list) { r.list = a.list; r.nlist = a.P; }
+        value_mma_kernel<LAW, NB, NQ, NS><<<dim3(gy, gx), VM_THREADS, vsmem, a.stream>>>(prm);
+      }
+      prof_mark(h, a.stream, 1);
+      CK(cudaGetLastError());
+      if (a.mode != MODE_RESIDUAL) {
+        const DynRows dr{dyn ? a.dyn_count : nullptr, a.list, target, cap, 1};
+        sum_partials_kernel<<<(a.P + 3) / 4, 128, 0, a.stream>>>(h->part, gx, a.P, a.out, a.mask, dr);
+        CK(cudaGetLastError());
+      }
+      return 0;
+    }
+    const int gx = (nunits + 127) / 128;
+    if (a.mode != MODE_RESIDUAL) {
+      if (ensure_part(h, (size_t)a.P * gx)) return -2;
+      r.part = h->part;
+    }
+    value_kernel<LAW, NB, NQ, NS><<<dim3(gx, a.P), 128, 0, a.stream>>>(prm);
     prof_mark(h, a.stream, 1);
     CK(cudaGetLastError());
     if (a.mode != MODE_RESIDUAL) {
-      sum_partials_kernel<<<(a.P + 3) / 4, 128, 0, a.stream>>>(h->part, gx, a.P, a.out, a.mask);
+      sum_partials_kernel<<<(a.P + 3) / 4, 128, 0, a.stream>>>(h->part, gx, a.P, a.out, a.mask, DynRows{});
       CK(cudaGetLastError());
     }
     return 0;
@@ -239,7 +233,7 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
   if (h->ku < 1) return fail(-1, "derivative modes need k_u >= 1");
   if (h->ku > 32) return fail(-1, "derivative modes need k_u <= 32");
   if constexpr (LAW::M == 4 && NB == 6 && NS == 4) {
-    if (!h->force_warp_kernel) return launch_mma<LAW, NQ>(h, a, prm, nunits);
+    return launch_mma<LAW, NQ>(h, a, prm, nunits);
   }
   if (h->ku <= 16) return launch_warp<LAW, NB, NQ, NS, 16>(h, a, prm, nunits);
   return launch_warp<LAW, NB, NQ, NS, 32>(h, a, prm, nunits);

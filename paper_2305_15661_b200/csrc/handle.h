@@ -13,12 +13,10 @@ struct LmWork {
   int P = 0, K = 0, ku = 0, kx = 0, nmu = 0;
   void* buf = nullptr;
   size_t bytes = 0;
-  int* counters_h = nullptr;  // pinned
 };
 
 inline void lm_free(LmWork& w) {
   if (w.buf) cudaFree(w.buf);
-  if (w.counters_h) cudaFreeHost(w.counters_h);
   w = LmWork();
 }
 
@@ -46,8 +44,8 @@ struct EvalArgs {
   double* out;
   int* degen;
   cudaStream_t stream;
-  int live = 0;  // number of unmasked rows (0 = all): sizes the grid for sparse LM rounds
-  const int* list = nullptr;  // value modes: ascending unmasked rows (compacted), `live` of them
+  const int* list = nullptr;       // ascending requested rows (compacted); with dyn_count: *dyn_count of them
+  const int* dyn_count = nullptr;  // device-sized pass (graph-resident LM rounds): live row count on the device
 };
 
 }  // namespace strom_host
@@ -80,9 +78,9 @@ struct strom_handle {
   std::vector<std::vector<int>> last_degen;
   int num_sms = 148;
   strom::LmWork lm;
-  // benchmark probe
-  int lm_rounds = 0;
-  int force_warp_kernel = 0;  // testing / A-B: use the tangent-lane kernel instead of the DMMA one
+  cudaStream_t lm_stream = nullptr;  // private capture stream of the LM graph
+  // statistics of the last strom_lm_solve: control rounds, derivative / objective passes
+  int lm_rounds = 0, lm_dpasses = 0, lm_opasses = 0;
   bool prof = false;
   std::vector<cudaEvent_t> ev;
   int nprof = 0;

@@ -6,7 +6,9 @@
 // batch of objective trials at w + alpha_j dw (speculative backtracking:
 // alpha_j = 2^-j for the next LM_B values of j; the accepted step is the
 // first j that passes Armijo, exactly the sequential loop's choice).  The
-// host loop launches the masked batched evaluations and the next round.
+// rounds run as a CUDA-graph WHILE loop (lm_capi.inc): the compaction kernel
+// decides on the device which batched evaluations a round launches (IF nodes)
+// and whether another round follows, so a batch of solves is one graph launch.
 // The K x K normal equations [[H_ww, H_wt],[H_wt^T, H_tt + lam I]] dz = -[S;T]
 // are solved in-kernel by LDL^T (no pivoting; singular = zero / non-finite
 // pivot or non-finite solution, lm.py:111-126).
@@ -41,10 +43,22 @@ struct LmState {
   double best_J, best_nS, best_nT;
 };
 
+// Device-side round control (one per solve batch)
+struct LmCtl {
+  int cnt[2][4];      // per round parity: [n_unfinished, n_derivs, n_obj mu, unused]
+  int round;          // control rounds run so far
+  int waited;         // consecutive rounds a derivatives pass was deferred
+  int ran_d, ran_o;   // whether the previous round ran the derivatives / objective pass
+  int dcount, ocount; // rows of this round's derivatives / objective passes (dlist / olist)
+  int nd, no;         // passes run (statistics)
+  int overflow;       // max_rounds reached with unfinished solves
+};
+
 struct LmRun {
   int P, ku, kx, K, nmu;
-  int ran_d, ran_o;  // whether the previous round ran the derivatives / objective pass
   int nb_first;      // trials in the first batch of a line search (1..LM_B); later batches LM_B
+  int max_rounds;
+  LmCtl* ctl;
   LmCfg cfg;
   LmState* st;
   double* w;        // (P, ku) current
@@ -63,10 +77,9 @@ struct LmRun {
   double* tw;          // (P*LM_B, ku) trial points
   double* ttau;        // (P*LM_B, kx)
   double* tmu;         // (P*LM_B, nmu)
-  int* counters;       // [n_active, n_derivs, n_obj, n_obj_rows] of this round
-  int* counters_next;  // next round's set, zeroed by this round's control kernel
   int* degen_fill;     // the evaluation kernels' degenerate-list fill counter (zeroed per round)
   int* olist;          // (P*LM_B) compacted objective rows requested (ascending)
+  int* dlist;          // (P) compacted derivatives rows requested (ascending)
   double* hist;        // (P, max_iters+1, 6) or null
   double* status;      // (P, 8)
 };
@@ -170,7 +183,6 @@ enum LmAction { ACT_ADVANCE = 0, ACT_SOLVE_SI = 1, ACT_SOLVE_MAIN = 2, ACT_WAIT 
 
 // the solve's system is filled by all threads of the block right before the solve
 // (lm_control_kernel); the state machine only decides which one (ACT_SOLVE_SI / _MAIN)
-__device__ __forceinline__ void lm_fill_main(const LmRun&, int, const LmState&, double*, double*) {}
 
 __device__ __forceinline__ void lm_request_derivs(const LmRun& R, int p, LmState& s, int phase) {
   s.phase = phase;
@@ -188,7 +200,6 @@ __device__ __forceinline__ int lm_escalate(const LmRun& R, int p, LmState& s, do
     s.phase = PH_DONE;
     return ACT_WAIT;
   }
-  lm_fill_main(R, p, s, A, rhs);
   return ACT_SOLVE_MAIN;
 }
 
@@ -319,7 +330,6 @@ static __device__ int lm_advance(const LmRun& R, int p, LmState& s, double* A, d
       s.n_done = s.it + 1;
       s.nS_prev = nS; s.nT_prev = nT; s.J_prev = s.J;
       s.attempts = 0;
-      lm_fill_main(R, p, s, A, rhs);
       return ACT_SOLVE_MAIN;
     }
     case PH_MAIN_LS: {  // Armijo backtracking results (lm.py:226-236)
@@ -405,13 +415,15 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
   __shared__ int s_act, s_flag;
   __shared__ LmState s;
   __shared__ int s_hold;
-  if (blockIdx.x == 0 && threadIdx.x < 4) R.counters_next[threadIdx.x] = 0;
+  const int par = R.ctl->round & 1;
+  int* const counters = R.ctl->cnt[par];
+  if (blockIdx.x == 0 && threadIdx.x < 4) R.ctl->cnt[par ^ 1][threadIdx.x] = 0;  // next round's set
   if (threadIdx.x == 0) {
     s = R.st[p];
-    // a request the host deferred last round stays posted; the mu waits (no state change)
+    // a request deferred last round stays posted; the mu waits (no state change)
     const bool wd = s.phase == PH_SI_DERIV || s.phase == PH_MAIN_DERIV || s.phase == PH_MAIN_ACCEPT_DERIV;
     const bool wo = s.phase == PH_SI_BASEJ || s.phase == PH_SI_LS || s.phase == PH_MAIN_LS;
-    s_hold = (wd && !R.ran_d) || (wo && !R.ran_o);
+    s_hold = (wd && !R.ctl->ran_d) || (wo && !R.ctl->ran_o);
     if (!s_hold) {
       R.req_d[p] = 0;
       for (int j = 0; j < LM_B; ++j) R.req_o[p * LM_B + j] = 0;
@@ -421,9 +433,9 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
   __syncthreads();
   if (s_hold) {
     if (threadIdx.x == 0) {
-      atomicAdd(&R.counters[0], 1);
-      if (R.req_d[p]) atomicAdd(&R.counters[1], 1);
-      if (R.req_o[p * LM_B]) atomicAdd(&R.counters[2], 1);
+      atomicAdd(&counters[0], 1);
+      if (R.req_d[p]) atomicAdd(&counters[1], 1);
+      if (R.req_o[p * LM_B]) atomicAdd(&counters[2], 1);
     }
     return;
   }
@@ -485,9 +497,9 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
   }
   if (t == 0) {
     R.st[p] = s;
-    if (s.phase != PH_DONE) atomicAdd(&R.counters[0], 1);
-    if (R.req_d[p]) atomicAdd(&R.counters[1], 1);
-    if (R.req_o[p * LM_B]) atomicAdd(&R.counters[2], 1);
+    if (s.phase != PH_DONE) atomicAdd(&counters[0], 1);
+    if (R.req_d[p]) atomicAdd(&counters[1], 1);
+    if (R.req_o[p * LM_B]) atomicAdd(&counters[2], 1);
     // degenerate flags of the evaluations requested now start at zero (read next round)
     if (R.req_d[p]) const_cast<int*>(R.ddeg)[p] = 0;
     for (int j = 0; j < LM_B; ++j)
@@ -495,13 +507,13 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
   }
 }
 
-// compact the objective requests into an ascending row list (one block, deterministic)
-static __global__ void __launch_bounds__(1024) lm_compact_kernel(LmRun R) {
-  __shared__ int wsum[32];
-  const int n = R.P * LM_B, t = threadIdx.x, lane = t & 31, wp = t >> 5;
+// ascending compaction of flags[0 .. n) into list (one block, deterministic); returns the
+// count to every thread
+static __device__ int block_compact(const int* flags, int n, int* list, int* wsum) {
+  const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
   const int per = (n + blockDim.x - 1) / blockDim.x, lo = t * per;
   int c = 0;
-  for (int i = lo; i < lo + per && i < n; ++i) c += R.req_o[i] != 0;
+  for (int i = lo; i < lo + per && i < n; ++i) c += flags[i] != 0;
   int x = c;  // inclusive warp scan
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, x, o);
@@ -520,10 +532,47 @@ static __global__ void __launch_bounds__(1024) lm_compact_kernel(LmRun R) {
   __syncthreads();
   int pos = x - c + (wp > 0 ? wsum[wp - 1] : 0);
   for (int i = lo; i < lo + per && i < n; ++i)
-    if (R.req_o[i]) R.olist[pos++] = i;
-  if (t == blockDim.x - 1) {
-    R.counters[3] = pos;
-    *R.degen_fill = 0;
+    if (flags[i]) list[pos++] = i;
+  const int total = wsum[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return total;
+}
+
+// End of a control round (one block): compact the requested derivative / objective rows and
+// decide on the device what the round launches.  A derivatives pass waits until every
+// unfinished mu asks for one (or no objective trials are pending, or it was deferred
+// LM_MAXWAIT rounds in a row): the mu meet at their derivative evaluations, so each K1 pass
+// is a full batch (cfg3: 92 -> ~40 passes per batch); deferred requests stay posted and the
+// mu waits, so no mu's iterates change.  In graph mode the IF / WHILE conditions are set here.
+constexpr int LM_MAXWAIT = 3;
+
+static __global__ void __launch_bounds__(1024) lm_compact_kernel(LmRun R, cudaGraphConditionalHandle h_while,
+                                                                 cudaGraphConditionalHandle h_d,
+                                                                 cudaGraphConditionalHandle h_o, int graph) {
+  __shared__ int wsum[32];
+  LmCtl& C = *R.ctl;
+  const int* cnt = C.cnt[C.round & 1];
+  const int nobj = block_compact(R.req_o, R.P * LM_B, R.olist, wsum);
+  const int nder = block_compact(R.req_d, R.P, R.dlist, wsum);
+  if (threadIdx.x != 0) return;
+  const int n_active = cnt[0], n_d = cnt[1], n_o = cnt[2];
+  const bool run_d = n_d > 0 && (n_o == 0 || n_d >= n_active || C.waited >= LM_MAXWAIT);
+  const bool run_o = n_o > 0;
+  C.waited = (n_d > 0 && !run_d) ? C.waited + 1 : 0;
+  C.ran_d = run_d;
+  C.ran_o = run_o;
+  C.nd += run_d;
+  C.no += run_o;
+  C.dcount = nder;
+  C.ocount = nobj;
+  C.round += 1;
+  const bool more = n_active > 0 && C.round < R.max_rounds;
+  if (n_active > 0 && !more) C.overflow = 1;
+  *R.degen_fill = 0;
+  if (graph) {
+    cudaGraphSetConditional(h_d, more && run_d ? 1u : 0u);
+    cudaGraphSetConditional(h_o, more && run_o ? 1u : 0u);
+    cudaGraphSetConditional(h_while, more ? 1u : 0u);
   }
 }
 

