@@ -390,6 +390,113 @@ def run_gn(args, dev, world, rank, local):
                     "d2h_bytes_per_step": 8 * P * (ku + kx + 8)}}
 
 
+def _sync_max(world, dev, *vals):
+    """Max over ranks of host-side numbers (timing)."""
+    if world == 1:
+        return vals
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return tuple(float(v) for v in t)
+
+
+def run_cfg4(args, dev, world, rank, local):
+    """Config 4: EQP constraint rows of 64 training snapshots over the 400k-triangle sector,
+    snapshots sharded over the ranks (s mod G = r, no collective in the compute; the row
+    blocks are gathered to rank 0 for the LP afterwards, timed separately)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_15661_b200 import configs, sharded
+    from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases
+
+    S = 64
+    case = configs.cfg4_case()
+    op = GpuReducedOperator(case.law, case.geom, ReducedBases(case.phi, case.psi, case.ref_coords), case.dist, device=dev)
+    ne, K = case.mesh.num_elements, op.k_u + op.k_x
+    ids = sharded.snapshot_ids(S, rank, world)
+    mus, U, X = sharded.snapshot_fields_device(case, ids, 4, dev)
+    out = torch.empty(len(ids) * (K + 1) * ne, dtype=torch.float64, device=dev)
+
+    def step():
+        if len(ids):
+            op.contributions_at_snapshots(U, X, mus, "lprows", out=out)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    steps = max(1, args.cfg_steps)
+    clk = Clocks(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.current_stream()
+    e0.record(st)
+    for _ in range(steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / steps
+    t0 = time.perf_counter()
+    full = sharded.gather_rows(out.view(len(ids), K + 1, ne), S, rank, world)
+    torch.cuda.synchronize()
+    gather_ms = 1e3 * (time.perf_counter() - t0)
+    ms, gather_ms = _sync_max(world, dev, ms, gather_ms)
+    ok = bool(torch.isfinite(full).all()) if full is not None else True
+    return {"metric": "EQP constraint-row element-snapshot evals/sec (fp64)", "value": S * ne / (ms / 1e3),
+            "unit": "element-snapshots/s", "higher_is_better": True, "scaling": "strong", "ms_per_step": ms,
+            "steps": steps, "gather_to_rank0_ms": gather_ms if world > 1 else 0.0, "finite": ok,
+            "config": {"workload": "cfg4: 400,000-triangle sector, 64 snapshots x (k_u+k_x+1) = 31 rows, k_u=20, k_x=10",
+                       "matrix": [S * (K + 1), ne], "parallelism": f"snapshots s mod {world} per rank, no compute collective"},
+            "clocks": clocks}
+
+
+def run_cfg5(args, dev, world, rank, local, group=None):
+    """Config 5: one greedy search step over 1024 candidates (batched ROM LM solves, k_u=24,
+    k_x=12, 3% EQP elements, then full-mesh residual-norm indicators and the argmax),
+    candidates interleaved over the ranks, one all-gather of (indicator, index) winners."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_15661_b200 import configs
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.greedy import greedy_step
+    from paper_2305_15661_b200.lm import LmConfig
+    from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases
+
+    case = configs.cfg5_rom(1024)
+    op = GpuReducedOperator(case.law, case.geom, ReducedBases(case.phi, case.psi, case.ref_coords), case.dist, device=dev)
+    rho = WeightVector(case.rho)
+    cfg = LmConfig(max_iters=10)
+
+    def step():
+        return greedy_step(op, case.mus, [], rho, case.W[0], None, cfg, rank, world, group)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    steps = max(1, args.cfg_steps)
+    clk = Clocks(local)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        v, i = step()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / steps
+    clocks = clk.stop()
+    (wall,) = _sync_max(world, dev, wall)
+    return {"metric": "greedy candidate evaluations/sec (ROM LM solve + full-mesh indicator, fp64)",
+            "value": len(case.mus) / wall, "unit": "candidates/s", "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": 1e3 * wall, "steps": steps, "argmax": [float(v), int(i)],
+            "config": {"workload": "cfg5: 160,000-triangle sector, 1024 candidate mu ~ U[2,4], k_u=24, k_x=12, "
+                                   "4,800 EQP elements (3%), LM max_iters=10, indicator ||R||_2 on the full mesh",
+                       "parallelism": f"candidates interleaved over {world} rank(s) + all_gather argmax",
+                       "timing": "wall clock of the public greedy_step (host in / out), max over ranks"},
+            "clocks": clocks}
+
+
 def _lm_stats(op):
     """(control rounds, derivative passes, objective passes) of the op's last batched solve."""
     import ctypes
@@ -508,6 +615,11 @@ def run_mine(args):
         n_out = 1 + ku + kx + ku * ku + ku * kx + kx * kx
         e2e_io = (8 * (ku + kx + op.n_mu) + 8 * n_out, 2 * 8 * n_out + 4)
     gn = None if args.no_gn else run_gn(args, dev, world, rank, local)
+    cfg4 = cfg5 = None
+    if not args.no_sharded:
+        cfg4 = run_cfg4(args, dev, world, rank, local)
+        torch.cuda.empty_cache()
+        cfg5 = run_cfg5(args, dev, world, rank, local)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -541,6 +653,8 @@ def run_mine(args):
         line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_io[0], "d2h_bytes_per_step": e2e_io[1]}
     if gn is not None:
         line["gn"] = gn
+    if cfg4 is not None:
+        line["cfg4"], line["cfg5"] = cfg4, cfg5
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(n=args.cpu_n)
         if gn is not None:
@@ -561,6 +675,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gn", action="store_true", help="skip the config-3 Gauss-Newton solves/s measurement")
     ap.add_argument("--gn-steps", type=int, default=20, help="timed 64-mu LM batches of the GN measurement")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the config-4 / config-5 sharded measurements")
+    ap.add_argument("--cfg-steps", type=int, default=3, help="timed steps of the config-4 / config-5 measurements")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -182,6 +182,12 @@ def cfg3():
     return sector_rom_case()
 
 
+def cfg4_case():
+    """Config 4 geometry: the config-3 sector scaled to 320 x 625 quads = 400,000 triangles,
+    k_u = 20, k_x = 10 (the snapshots come from sharded.snapshot_fields_device)."""
+    return sector_rom_case(320, 625, 20, 10, 0.02, 50.0, 1, seed=4, name="cfg4-eqp-rows")
+
+
 def cfg5_rom(P=1024):
     return sector_rom_case(200, 400, 24, 12, 0.03, 100.0 / 3.0, P, seed=5, name="cfg5-greedy")
 

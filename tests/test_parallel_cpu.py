@@ -57,3 +57,51 @@ def test_global_argmax_two_ranks():
     for rank, got, total in res:
         assert got == want == (vals[3], 3)
         assert abs(total - vals.sum()) < 1e-12
+
+
+# -- config 4 snapshot sharding (paper_2305_15661_b200.sharded) ----------------------------
+def test_snapshot_fields_rank_independent():
+    """A snapshot's fields do not depend on which rank (which id subset) generates it."""
+    from paper_2305_15661_b200 import configs
+    from paper_2305_15661_b200.sharded import snapshot_fields_device, snapshot_ids
+
+    case = configs.sector_rom_case(n_radial=3, n_circ=4, ku=4, kx=2, frac_active=0.5, rho_scale=2.0, P=1, seed=9)
+    S = 5
+    mus, U, X = snapshot_fields_device(case, np.arange(S), 7, "cpu")
+    for world in (2, 3):
+        for r in range(world):
+            ids = snapshot_ids(S, r, world)
+            m, u, x = snapshot_fields_device(case, ids, 7, "cpu")
+            assert np.array_equal(m, mus[ids]) and torch.equal(u, U[ids]) and torch.equal(x, X[ids])
+    # freestream x (1 + U(-0.05, 0.05)) per node and component, Mach in [2, 4]
+    ff = U.view(S, -1, 4)
+    assert np.all((mus >= 2.0) & (mus <= 4.0))
+    assert torch.all((ff[:, :, 0] > 0.95 - 1e-12) & (ff[:, :, 0] < 1.05 + 1e-12))
+    assert torch.allclose(X.view(S, -1, 2).mean(0), torch.as_tensor(case.mesh.nodes), atol=0.05 / 2)
+
+
+def _rows_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2305_15661_b200.sharded import gather_rows, snapshot_ids
+
+    S = 7
+    ids = snapshot_ids(S, rank, world)
+    rows = torch.stack([torch.full((3, 4), float(s)) + torch.arange(12.0).view(3, 4) for s in ids])
+    full = gather_rows(rows, S, rank, world)
+    q.put((rank, None if full is None else full.numpy()))
+    dist.destroy_process_group()
+
+
+def test_gather_rows_two_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_rows_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    want = np.stack([np.full((3, 4), float(s)) + np.arange(12.0).reshape(3, 4) for s in range(7)])
+    assert res[1] is None and np.array_equal(res[0], want)
