@@ -153,6 +153,13 @@ def element_eval(law, geom, els, Ue, Un, xe, mu, check_degenerate=True):
                     u_out.tan[mask] = np.broadcast_to(u_in.tan, u_out.tan.shape)[mask]
                 else:
                     u_out[mask] = D.val(u_in)[mask]
+            elif bc.kind == "reflect":  # slip wall (GPU-only extension): u_g = R(nhat) u_in
+                refl = reflect_state(u_in, nhat)
+                if isinstance(u_out, D.Dual):
+                    u_out.val[mask] = np.broadcast_to(D.val(refl), u_out.val.shape)[mask]
+                    u_out.tan[mask] = np.broadcast_to(refl.tan, u_out.tan.shape)[mask]
+                else:
+                    u_out[mask] = D.val(refl)[mask]
             else:  # prescribed ghost at deformed positions, zero tangent (dg.py:151-161)
                 if posF is None:
                     posF = D.val(D.einsum("sg,bgi->bsi", geom.gphi_face[fi], xe))
@@ -164,8 +171,21 @@ def element_eval(law, geom, els, Ue, Un, xe, mu, check_degenerate=True):
                     u_out[mask] = ghost
         fn = D.einsum("bsci,bsi->bsc", law.flux(u_in, None, mu), ntil) + D.einsum(
             "bsci,bsi->bsc", law.flux(u_out, None, mu), ntil)
-        lam = D.maximum(law.wavespeed(u_in, nhat, mu), law.wavespeed(u_out, nhat, mu))
-        H = 0.5 * fn - 0.5 * D.expand(lam * sigma, 1) * (u_out - u_in)
+        numflux = getattr(law, "numflux", None)
+        if numflux is not None:  # matrix dissipation (Roe, GPU-only extension): H = fn/2 - sigma D/2
+            H = 0.5 * fn - 0.5 * D.expand(sigma, 1) * numflux(u_in, u_out, nhat, mu)
+        else:
+            ws_in, ws_out = law.wavespeed(u_in, nhat, mu), law.wavespeed(u_out, nhat, mu)
+            wall = np.isin(tags, [tid for tid in np.unique(tags)
+                                  if tid >= 0 and law.bc(tag_name[int(tid)]).kind == "reflect"])
+            if np.any(wall):  # ws(R u) = ws(u) exactly in exact arithmetic: use ws_in (no rounding tie)
+                if isinstance(ws_out, D.Dual):
+                    ws_out.val[wall] = D.val(ws_in)[wall]
+                    ws_out.tan[wall] = ws_in.tan[wall]
+                else:
+                    ws_out[wall] = ws_in[wall]
+            lam = D.maximum(ws_in, ws_out)
+            H = 0.5 * fn - 0.5 * D.expand(lam * sigma, 1) * (u_out - u_in)
         c = D.einsum("bsn,bsc->bnc", geom.wphi_face[els, fi], H)
         res_face = c if res_face is None else res_face + c
     if bad:
@@ -173,6 +193,13 @@ def element_eval(law, geom, els, Ue, Un, xe, mu, check_degenerate=True):
     res_vol = D.reshape(res_vol, (B, nb * m))
     res_face = D.reshape(res_face, (B, nb * m))
     return KernelOut(res_vol + res_face, res_vol, res_face)
+
+
+def reflect_state(u, nhat):
+    """Slip-wall ghost of 2-D Euler states: momentum mirrored in the wall, m - 2 (m . n) n."""
+    mn = u[..., 1] * nhat[..., 0] + u[..., 2] * nhat[..., 1]
+    return D.stack([u[..., 0], u[..., 1] - 2.0 * mn * nhat[..., 0], u[..., 2] - 2.0 * mn * nhat[..., 1], u[..., 3]],
+                   axis=-1)
 
 
 # -- distortion (strom/distortion.py:33-68) -----------------------------------------

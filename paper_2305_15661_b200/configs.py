@@ -158,38 +158,59 @@ def euler_square_case(n=256, ku=16, kx=8, seed=2, mach=2.0, quad_order=6, per_co
 
 
 # -- configs 3-5 (half cylinder) -----------------------------------------------------------
-SECTOR_BCS = {"inflow": "freestream", "outflow": "extrapolate", "wall": "extrapolate"}
+def sector_bcs(wall="slip"):
+    """Half-cylinder boundary conditions: inflow = prescribed freestream(mu), outflow =
+    extrapolate, cylinder wall = slip wall ("slip", the physical one that forms the bow shock;
+    a GPU-only extension the reference cannot express) or "extrapolate" (the reference-
+    expressible variant the reference goldens and CPU timings use)."""
+    return {"inflow": "freestream", "outflow": "extrapolate", "wall": "wall" if wall == "slip" else "extrapolate"}
+
+
+SECTOR_BCS = sector_bcs("extrapolate")
+
+
+def smooth_modes(rng, nodes, k, n_modes=4):
+    """(2 n_nodes, k) orthonormal basis of smooth mesh motions: each column is a sum of
+    ``n_modes`` seeded sinusoid modes (integer wave numbers in [1, 4], random phase and
+    direction, as ``displacement``) interleaved (x, y) per node, then QR."""
+    cols = [displacement(rng, nodes, 1.0, n_modes, 1.0).ravel() for _ in range(k)]
+    Q, R = np.linalg.qr(np.stack(cols, axis=1))
+    return Q * np.sign(np.diag(R))[None, :]
 
 
 def sector_rom_case(n_radial=100, n_circ=200, ku=20, kx=10, frac_active=0.02, rho_scale=50.0, P=64, seed=3,
-                    quad_order=6, name="cfg3-half-cylinder"):
+                    quad_order=6, name="cfg3-half-cylinder", wall="slip", psi_kind="smooth", flux="llf"):
+    """Half-cylinder ROM case (configs 3-5).  Phi = QR([normalised freestream(3), Gaussian
+    columns]); Psi = seeded orthonormal smooth mesh motions (``smooth_modes``; a Gaussian Psi
+    moves neighbouring nodes independently and inverts elements outside the EQP sample once
+    tau is O(0.1)), or ``psi_kind="gaussian"``."""
     mesh, maps = build_sector_mesh(n_radial, n_circ, degree_sol=2, n_comp=4)
     rng = np.random.default_rng(seed)
     ne = mesh.num_elements
     ff = np.tile(L.euler_freestream(3.0), ne * 6)
     phi = orthonormal(rng, maps.n_global_state, ku, first=ff / np.linalg.norm(ff))
-    psi = orthonormal(rng, maps.n_global_coord, kx)
+    psi = orthonormal(rng, maps.n_global_coord, kx) if psi_kind == "gaussian" else smooth_modes(rng, mesh.nodes, kx)
     n_act = max(1, int(round(frac_active * ne)))
     rho = eqp_weights(rng, ne, n_act, rho_scale)
     mus = rng.uniform(2.0, 4.0, size=(P, 1))
     w0 = phi.T @ ff
-    law = L.euler(tags=SECTOR_BCS)
+    law = L.euler(tags=sector_bcs(wall), flux=flux)
     return Case(name, law, mesh, maps, quad_order, phi, psi, mesh.nodes.ravel().copy(), mus,
                 np.tile(w0, (P, 1)), np.zeros((P, kx)), rho)
 
 
-def cfg3():
-    return sector_rom_case()
+def cfg3(wall="slip"):
+    return sector_rom_case(wall=wall)
 
 
-def cfg4_case():
+def cfg4_case(wall="slip"):
     """Config 4 geometry: the config-3 sector scaled to 320 x 625 quads = 400,000 triangles,
     k_u = 20, k_x = 10 (the snapshots come from sharded.snapshot_fields_device)."""
-    return sector_rom_case(320, 625, 20, 10, 0.02, 50.0, 1, seed=4, name="cfg4-eqp-rows")
+    return sector_rom_case(320, 625, 20, 10, 0.02, 50.0, 1, seed=4, name="cfg4-eqp-rows", wall=wall)
 
 
-def cfg5_rom(P=1024):
-    return sector_rom_case(200, 400, 24, 12, 0.03, 100.0 / 3.0, P, seed=5, name="cfg5-greedy")
+def cfg5_rom(P=1024, wall="slip"):
+    return sector_rom_case(200, 400, 24, 12, 0.03, 100.0 / 3.0, P, seed=5, name="cfg5-greedy", wall=wall)
 
 
 def snapshot_fields(case, S, seed, mach_range=(2.0, 4.0)):

@@ -39,6 +39,8 @@ static int dispatch(strom_handle* h, const EvalArgs& a) {
     case 1: return eval_burgers_st(h, a);
     case 2: return eval_strip(h, a);
     case 3: return eval_euler(h, a);
+    case 4: return eval_euler_roe(h, a);
+    case 5: return eval_euler_wall(h, a);
     default: return fail(-1, "unknown law id");
   }
 }
@@ -115,6 +117,16 @@ extern "C" int strom_create(const strom_mesh_desc* mesh, const strom_law_desc* l
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { delete h; return fail(-2, cudaGetErrorString(e)); }
   }
+  if (h->ne > 0) {  // slip walls present? (their Jacobians exist on the DMMA path only)
+    std::vector<uint8_t> fi((size_t)h->ne * 3);
+    if (cudaMemcpy(fi.data(), h->finfo, fi.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      delete h;
+      return fail(-2, "face info read");
+    }
+    for (uint8_t v : fi) h->has_wall |= (v >> 3) == BC_REFLECT;
+  }
+  // slip walls need a wall-capable Euler instantiation: 4 (Roe) or 5 (LLF with walls)
+  if (h->has_wall && law->law_id != 4 && law->law_id != 5) { delete h; return fail(-1, "slip walls need law id 4 or 5"); }
   h->degen_cap = std::max(1024, h->ne);
   if (cudaMalloc(&h->degen_list, sizeof(int) * 2 * h->degen_cap) != cudaSuccess ||
       cudaMalloc(&h->degen_fill, sizeof(int)) != cudaSuccess) {
@@ -133,6 +145,7 @@ extern "C" int strom_set_bases(strom_handle* h, const double* phi, int32_t ku, c
   if ((ku && !phi) || (kx && !psi) || !ref_coords) return fail(-1, "missing basis pointer");
   h->Phi = phi; h->ku = ku; h->Psi = psi; h->kx = kx; h->xref = ref_coords; h->u0 = state_offset;
   h->u0_stride = 0; h->x_stride = 0;
+  h->epoch++;
   return 0;
 }
 
@@ -142,6 +155,7 @@ extern "C" int strom_set_offsets(strom_handle* h, const double* state_offset, in
   if (state_stride < 0 || coord_stride < 0) return fail(-1, "strom_set_offsets: negative stride");
   h->u0 = state_offset; h->u0_stride = state_offset ? state_stride : 0;
   h->xref = ref_coords; h->x_stride = coord_stride;
+  h->epoch++;
   return 0;
 }
 
@@ -210,6 +224,8 @@ extern "C" int strom_degenerate_elements(strom_handle* h, int32_t p, int32_t* id
   return (int)v.size();
 }
 
+static void lm_graph_free(strom_handle* h);  // lm_capi.inc
+
 extern "C" void strom_destroy(strom_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
@@ -218,6 +234,7 @@ extern "C" void strom_destroy(strom_handle* h) {
   if (h->degen_list) cudaFree(h->degen_list);
   if (h->degen_fill) cudaFree(h->degen_fill);
   if (h->degen_scratch) cudaFree(h->degen_scratch);
+  lm_graph_free(h);
   lm_free(h->lm);
   if (h->lm_stream) cudaStreamDestroy(h->lm_stream);
   for (auto& e : h->ev) cudaEventDestroy(e);

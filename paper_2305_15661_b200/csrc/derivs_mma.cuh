@@ -440,12 +440,17 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         const double t = T.trace[0][sp][j];
         us[0] = fma(t, a.x, us[0]); us[1] = fma(t, a.y, us[1]); us[2] = fma(t, b.x, us[2]); us[3] = fma(t, b.y, us[3]);
       }
-      if (side && bc >= 2) LAW::ghost(bc - 2, la, us);
+      const bool wall = LAW::WALLS && bc == BC_REFLECT;  // slip wall: exterior = R(nh) u_in
+      if (side && bc >= 2) {
+        if (wall) reflect_state(us, nh, us);
+        else LAW::ghost(bc - 2, la, us);
+      }
       // A(n) is linear in n: evaluated along sc * nu it comes out already scaled by the face
       // weight and the LLF 1/2 (weight 1 on an extrapolated exterior, whose C_out folds into
-      // C_in since u_out == u_in there; 0 for exterior sides, which carry no state tangent)
+      // C_in since u_out == u_in there; 0 for prescribed exteriors, which carry no state
+      // tangent; a wall's exterior block is kept and folded into C_in through R after P)
       const double wsq = T.ws[s];
-      const double sc = (side == 1 && bc >= 1) ? 0.0 : ((side == 0 && bc == 1) ? wsq : 0.5 * wsq);
+      const double sc = (side == 1 && bc >= 1 && !wall) ? 0.0 : ((side == 0 && bc == 1) ? wsq : 0.5 * wsq);
       const double nus[2] = {sc * nu[0], sc * nu[1]};
       double f2[M][2], A[M][M], g[M], gn[2];
       const double ws = PointOps<LAW>::face_side(us, nus, nh, f2, A, g, gn, la);
@@ -471,9 +476,69 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         fp[c][0] = __shfl_sync(0xffffffffu, f2[c][0], partner);
         fp[c][1] = __shfl_sync(0xffffffffu, f2[c][1], partner);
       }
-      if (lane < 2 * NFS) {
+      if constexpr (LAW::ROE) {  // Roe (GPU-only extension): D = |A_roe(nh)| (u_out - u_in)
+        if (lane < 2 * NFS) {
+          // D and its Jacobian along this lane's own state (and, side 0, along nh): forward mode
+          Dn<6> ua[M], ub[M], nd[2];
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            ua[c] = side ? cst<6>(up[c]) : seed<6>(us[c], c);
+            ub[c] = side ? seed<6>(us[c], c) : cst<6>(up[c]);
+          }
+          nd[0] = seed<6>(nh[0], M);
+          nd[1] = seed<6>(nh[1], M + 1);
+          Dn<6> Dd[M];
+          roe_diss(ua, ub, nd, la.p[0], la.p[1], Dd);
+          const bool dz = bc == 1;  // extrapolated exterior: u_out == u_in, D == 0 identically
+          const bool ext0 = side == 1 && bc >= 1 && !wall;
+          double* FXp = RA + SH::FX;
+          if (side == 0) {
+#pragma unroll
+            for (int c = 0; c < M; ++c) {
+              const double dv = dz ? 0.0 : Dd[c].v;
+              const double fni = f2[c][0] * nu[0] + f2[c][1] * nu[1], fno = fp[c][0] * nu[0] + fp[c][1] * nu[1];
+              RA[SH::HS + c * NFSP + fs] = wsq * (0.5 * (fni + fno) - 0.5 * len * dv);
+              FXp[(2 * c + 0) * NFSP + fs] = 0.5 * wsq * (f2[c][0] + fp[c][0]);
+              FXp[(2 * c + 1) * NFSP + fs] = 0.5 * wsq * (f2[c][1] + fp[c][1]);
+              FXp[(2 * M + c) * NFSP + fs] = 0.5 * wsq * dv;  // the FD stage's "du" slot carries D
+            }
+            FXp[(3 * M + 0) * NFSP + fs] = 1.0;  // "lam" = 1, its normal gradient 0: coef = dlen
+            FXp[(3 * M + 1) * NFSP + fs] = 0.0;
+            FXp[(3 * M + 2) * NFSP + fs] = 0.0;
+            // D's own normal dependence: -wsq len / 2 (dD/dnh . dnh) per unit normal perturbation,
+            // pre-written into the FD slots (the FD stage adds the flux and |nu| terms)
+            const double il = 1.0 / len;
+#pragma unroll
+            for (int dir = 0; dir < 2; ++dir) {
+              const double dlen = nh[dir];
+              const double dn0 = ((dir == 0 ? 1.0 : 0.0) - nh[0] * dlen) * il, dn1 = ((dir == 1 ? 1.0 : 0.0) - nh[1] * dlen) * il;
+#pragma unroll
+              for (int c = 0; c < M; ++c)
+                S[SH::FD + (c * 2 + dir) * NFSP + fs] =
+                    dz ? 0.0 : -0.5 * wsq * len * (Dd[c].d[M] * dn0 + Dd[c].d[M + 1] * dn1);
+            }
+          }
+          // C_side = wsq (A_side / 2 - len / 2 dD/du_side)
+#pragma unroll
+          for (int c = 0; c < M; ++c)
+#pragma unroll
+            for (int cp = 0; cp < M; ++cp)
+              RA[SH::CF + side * SH::CFS + (c * M + cp) * NFSP + fs] =
+                  A[c][cp] + ((ext0 || dz) ? 0.0 : -0.5 * wsq * len * Dd[c].d[cp]);
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            if (side == 0) {
+              RA[SH::FQ + (c * 2 + 0) * SH::NQC + q] = wq * fq[c][0];
+              RA[SH::FQ + (c * 2 + 1) * SH::NQC + q] = wq * fq[c][1];
+            }
+#pragma unroll
+            for (int cp = 0; cp < M; ++cp) RA[SH::BQ + side * SH::BQS + (cp * M + c) * SH::NQC + q] = Aq[c][cp];
+          }
+        }
+      } else if (lane < 2 * NFS) {
         const double wsi = side ? wsp : ws, wso = side ? ws : wsp;
-        const bool in_wins = wsi >= wso;  // dual.maximum tie -> first argument (dual.py:171)
+        // dual.maximum tie -> first argument (dual.py:171); a wall's ws(R u) equals ws(u): interior
+        const bool in_wins = wall || wsi >= wso;
         const bool mine = (side == 0) == in_wins;
         const double lam = in_wins ? wsi : wso;
         double* FXp = RA + SH::FX;
@@ -497,7 +562,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         }
         // C_side = wsq (A/2 -+ lam len/2 I - len/2 du (d lam/du_side)^T); the extrapolated
         // exterior (du = 0) adds its C_out = A/2 - lam len/2 I into C_in, exterior sides are 0
-        const bool ext0 = side == 1 && bc >= 1;
+        const bool ext0 = side == 1 && bc >= 1 && !wall;
         const double dgn = (bc == 1 || ext0) ? 0.0 : (side ? -0.5 : 0.5) * lam * len * wsq;
         const double dsc = ext0 ? 0.0 : -0.5 * len * wsq;
         double gm[M];
@@ -546,6 +611,48 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       }
     }
     __syncwarp();
+    // ---- slip walls: fold the exterior block into C_in through u_g = R(nh) u_in, and the
+    // ghost's normal dependence into the FD slots (warp-uniform: elements without walls skip)
+    if (LAW::WALLS && ((fin[0] >> 3) == BC_REFLECT || (fin[1] >> 3) == BC_REFLECT || (fin[2] >> 3) == BC_REFLECT)) {
+      if (lane < NFS && (fin[lane / NS] >> 3) == BC_REFLECT) {
+        const int fs = lane, f = fs / NS, s = fs % NS;
+        const double* nh = S + SH::MNHAT + 2 * f;
+        const double len = S[SH::MNLEN + f], il = 1.0 / len;
+        double ui[M] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < NF; ++j)
+#pragma unroll
+          for (int c = 0; c < M; ++c) ui[c] = fma(T.trace[0][s][j], S[SH::UE + fnode_of(PD, f, j) * M + c], ui[c]);
+        double X[M][M];
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+#pragma unroll
+          for (int cp = 0; cp < M; ++cp) X[c][cp] = RA[SH::CF + SH::CFS + (c * M + cp) * NFSP + fs];
+        const double mn = ui[1] * nh[0] + ui[2] * nh[1];
+#pragma unroll
+        for (int dir = 0; dir < 2; ++dir) {  // d(R u_in)/dnh . dnh for a unit perturbation of nu
+          const double dlen = nh[dir];
+          const double dn0 = ((dir == 0 ? 1.0 : 0.0) - nh[0] * dlen) * il, dn1 = ((dir == 1 ? 1.0 : 0.0) - nh[1] * dlen) * il;
+          const double dmn = ui[1] * dn0 + ui[2] * dn1;
+          const double w1 = -2.0 * (dmn * nh[0] + mn * dn0), w2 = -2.0 * (dmn * nh[1] + mn * dn1);
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            const double ex = X[c][1] * w1 + X[c][2] * w2;
+            double& slot = S[SH::FD + (c * 2 + dir) * NFSP + fs];
+            slot = LAW::ROE ? slot + ex : ex;
+          }
+        }
+        // C_in += X R, R = diag(1, I - 2 nh nh^T, 1)
+#pragma unroll
+        for (int c = 0; c < M; ++c) {
+          const double xn = X[c][1] * nh[0] + X[c][2] * nh[1];
+          const double xr[M] = {X[c][0], X[c][1] - 2.0 * xn * nh[0], X[c][2] - 2.0 * xn * nh[1], X[c][3]};
+#pragma unroll
+          for (int cp = 0; cp < M; ++cp) RA[SH::CF + (c * M + cp) * NFSP + fs] += xr[cp];
+        }
+      }
+      __syncwarp();
+    }
     // ---- R: residual rows (volume / face split) and Tq ------------------------------
 #if !STROM_RESID_MMA
     if (lane < NU) {
@@ -635,6 +742,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       const double len = S[SH::MNLEN + f];
       const double* FXp = RA + SH::FX + fs;
       const double lam = FXp[(3 * M) * NFSP];
+      const bool wallf = LAW::WALLS && (fin[f] >> 3) == BC_REFLECT;
       const double il = 1.0 / len;
 #pragma unroll
       for (int dir = 0; dir < 2; ++dir) {  // dnu = e_x or e_y
@@ -644,9 +752,12 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         const double dlam = FXp[(3 * M + 1) * NFSP] * dnh0 + FXp[(3 * M + 2) * NFSP] * dnh1;
         const double coef = dlam * len + lam * dlen;
 #pragma unroll
-        for (int c = 0; c < M; ++c)
+        for (int c = 0; c < M; ++c) {
+          // Roe: D's normal dependence, walls: the ghost's, were pre-written to the slot
+          const double pre = (LAW::ROE || wallf) ? S[SH::FD + (c * 2 + dir) * NFSP + fs] : 0.0;
           S[SH::FD + (c * 2 + dir) * NFSP + fs] =
-              FXp[(2 * c) * NFSP] * dnu0 + FXp[(2 * c + 1) * NFSP] * dnu1 - FXp[(2 * M + c) * NFSP] * coef;
+              pre + FXp[(2 * c) * NFSP] * dnu0 + FXp[(2 * c + 1) * NFSP] * dnu1 - FXp[(2 * M + c) * NFSP] * coef;
+        }
       }
     }
     // (no barrier: the L stage reads only BQ / CF; TQ / FD / R rows are read after later barriers)

@@ -324,7 +324,7 @@ __device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB,
       }
     }
     double ghost[M];
-    if (bc >= 2) LAW::ghost(bc - 2, la, ghost);
+    if (bc >= 2 && bc != BC_REFLECT) LAW::ghost(bc - 2, la, ghost);
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       double ui[M], uo[M];
@@ -351,13 +351,11 @@ __device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB,
 #pragma unroll
         for (int c = 0; c < M; ++c) uo[c] = ghost[c];
       }
-      double fi_[M][2], fo[M][2];
-      const double wi = PointVal<LAW>::flux_ws(ui, nh, fi_, la), wo = PointVal<LAW>::flux_ws(uo, nh, fo, la);
-      double lam = wi >= wo ? wi : wo;
+      double Hs[M];
+      face_flux_val<LAW>(ui, uo, bc, nu, len, nh, la, Hs);
 #pragma unroll
       for (int c = 0; c < M; ++c) {
-        double fn = (fi_[c][0] * nu[0] + fi_[c][1] * nu[1]) + (fo[c][0] * nu[0] + fo[c][1] * nu[1]);
-        double H = T.ws[s] * (0.5 * fn - 0.5 * (lam * len) * (uo[c] - ui[c]));
+        const double H = T.ws[s] * Hs[c];
 #pragma unroll
         for (int j = 0; j < NF; ++j) R[fnode_of(PD, f, j) * M + c] = fma(T.trace[f][s][j], H, R[fnode_of(PD, f, j) * M + c]);
       }

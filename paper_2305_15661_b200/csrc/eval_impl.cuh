@@ -235,6 +235,8 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
   if constexpr (LAW::M == 4 && NB == 6 && NS == 4) {
     return launch_mma<LAW, NQ>(h, a, prm, nunits);
   }
+  // the Roe flux and slip-wall Jacobians exist on the DMMA path (4 components, p = 2) only
+  if (LAW::ROE || h->has_wall) return fail(-1, "Roe flux / slip-wall derivatives need p = 2 (DMMA path)");
   if (h->ku <= 16) return launch_warp<LAW, NB, NQ, NS, 16>(h, a, prm, nunits);
   return launch_warp<LAW, NB, NQ, NS, 32>(h, a, prm, nunits);
 }

@@ -77,8 +77,14 @@ struct strom_handle {
   int degen_scratch_cap = 0;
   std::vector<std::vector<int>> last_degen;
   int num_sms = 148;
+  bool has_wall = false;  // slip-wall faces (BC_REFLECT) in the mesh
   strom::LmWork lm;
   cudaStream_t lm_stream = nullptr;  // private capture stream of the LM graph
+  cudaGraph_t lm_graph = nullptr;    // the last built LM graph, reused while its key matches
+  cudaGraphExec_t lm_exec = nullptr;
+  std::vector<char> lm_key;
+  int lm_graph_builds = 0;
+  unsigned long long epoch = 0;      // bumped whenever bases / offsets change (graph key)
   // statistics of the last strom_lm_solve: control rounds, derivative / objective passes
   int lm_rounds = 0, lm_dpasses = 0, lm_opasses = 0;
   bool prof = false;
@@ -93,4 +99,6 @@ int eval_linadv(strom_handle* h, const EvalArgs& a);
 int eval_burgers_st(strom_handle* h, const EvalArgs& a);
 int eval_strip(strom_handle* h, const EvalArgs& a);
 int eval_euler(strom_handle* h, const EvalArgs& a);
+int eval_euler_roe(strom_handle* h, const EvalArgs& a);
+int eval_euler_wall(strom_handle* h, const EvalArgs& a);
 }  // namespace strom_host

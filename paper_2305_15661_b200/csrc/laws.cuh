@@ -13,6 +13,8 @@
 
 namespace strom {
 
+constexpr int BC_REFLECT = 31;  // face-info bc code of a slip wall (laws.py BC_REFLECT); ghosts are 2..30
+
 template <int N>
 struct Dn {
   double v;
@@ -114,6 +116,8 @@ struct LawArgs {
 // linear advection, conslaw.py:174-253 (no manufactured solution)
 struct LinAdv {
   static constexpr bool ANALYTIC = false;
+  static constexpr bool ROE = false;
+  static constexpr bool WALLS = false;
   static constexpr int M = 1;
   static constexpr int SRC = SRC_NONE;
   template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
@@ -132,6 +136,8 @@ struct LinAdv {
 // space-time Burgers, conslaw.py:94-163
 struct BurgersST {
   static constexpr bool ANALYTIC = false;
+  static constexpr bool ROE = false;
+  static constexpr bool WALLS = false;
   static constexpr int M = 1;
   static constexpr int SRC = SRC_POS;
   template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
@@ -151,6 +157,8 @@ struct BurgersST {
 // steady Burgers strip (config 1): (u^2/2)_x = mu u
 struct BurgersStrip {
   static constexpr bool ANALYTIC = false;
+  static constexpr bool ROE = false;
+  static constexpr bool WALLS = false;
   static constexpr int M = 1;
   static constexpr int SRC = SRC_U;
   template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
@@ -170,6 +178,8 @@ struct BurgersStrip {
 // compressible Euler, conservative (rho, rho u, rho v, E); LLF speed |v.n| + c
 struct Euler {
   static constexpr bool ANALYTIC = true;
+  static constexpr bool ROE = false;    // numerical flux: LLF (the reference's)
+  static constexpr bool WALLS = false;  // slip-wall faces compiled in (EulerWall / EulerRoe)
   static constexpr int M = 4;
   static constexpr int SRC = SRC_NONE;
   // fn = f(u).n and A = d(f.n)/du for a (not necessarily unit) direction n
@@ -340,6 +350,69 @@ struct Euler {
   }
 };
 
+// Euler with the Roe numerical flux (GPU-only extension; laws.py roe_dissipation):
+// H = (f_in + f_out).nu / 2 - |nu| D / 2, D = |A_roe(nh)| (u_out - u_in); p[1] = entropy delta
+struct EulerRoe : Euler {
+  static constexpr bool ROE = true;
+  static constexpr bool WALLS = true;
+};
+
+// Euler (LLF) on meshes with slip walls (GPU-only extension): a separate instantiation so the
+// wall-free kernels carry none of the wall code
+struct EulerWall : Euler {
+  static constexpr bool WALLS = true;
+};
+
+// slip-wall ghost (bc code BC_REFLECT): momentum mirrored in the face, m - 2 (m . nh) nh
+template <class T>
+__device__ __forceinline__ void reflect_state(const T* u, const T* nh, T* out) {
+  const T mn = u[1] * nh[0] + u[2] * nh[1];
+  out[0] = u[0];
+  out[1] = u[1] - 2.0 * mn * nh[0];
+  out[2] = u[2] - 2.0 * mn * nh[1];
+  out[3] = u[3];
+}
+
+// Roe matrix dissipation D = |A_roe(nh)| (uR - uL) for 2-D Euler: Roe-averaged state, the three
+// wave families, smooth entropy correction |l| -> sqrt(l^2 + (delta c)^2).  Templated on the
+// scalar: T = Dn<N> gives its exact Jacobians (K1), T = double its value (K2).  Restates the
+// host spec laws.py roe_dissipation, against which the oracle checks it.
+template <class T>
+__device__ __forceinline__ void roe_diss(const T* uL, const T* uR, const T* nh, double g, double delta, T* D) {
+  const double gm = g - 1.0;
+  const T sl = dsqrt(uL[0]), sr = dsqrt(uR[0]);
+  const T vxl = uL[1] / uL[0], vyl = uL[2] / uL[0], vxr = uR[1] / uR[0], vyr = uR[2] / uR[0];
+  const T pl = gm * (uL[3] - 0.5 * (uL[1] * vxl + uL[2] * vyl));
+  const T pr = gm * (uR[3] - 0.5 * (uR[1] * vxr + uR[2] * vyr));
+  const T hl = (uL[3] + pl) / uL[0], hr = (uR[3] + pr) / uR[0];
+  const T den = sl + sr;
+  const T ux = (sl * vxl + sr * vxr) / den, uy = (sl * vyl + sr * vyr) / den, ht = (sl * hl + sr * hr) / den;
+  const T q2 = ux * ux + uy * uy;
+  const T c2 = gm * (ht - 0.5 * q2);
+  const T c = dsqrt(c2);
+  const T rt = sl * sr;
+  const T un = ux * nh[0] + uy * nh[1];
+  const T dr = uR[0] - uL[0], dp = pr - pl, dvx = vxr - vxl, dvy = vyr - vyl;
+  const T dun = dvx * nh[0] + dvy * nh[1];
+  const T a1 = (dp - rt * c * dun) / (2.0 * c2);
+  const T a3 = (dp + rt * c * dun) / (2.0 * c2);
+  const T a2 = dr - dp / c2;
+  const T d2 = (delta * delta) * c2;
+  const T l1 = dsqrt((un - c) * (un - c) + d2), l2 = dsqrt(un * un + d2), l3 = dsqrt((un + c) * (un + c) + d2);
+  const T w1 = l1 * a1, w3 = l3 * a3;
+  D[0] = w1 + l2 * a2 + w3;
+  D[1] = w1 * (ux - c * nh[0]) + l2 * (a2 * ux + rt * (dvx - dun * nh[0])) + w3 * (ux + c * nh[0]);
+  D[2] = w1 * (uy - c * nh[1]) + l2 * (a2 * uy + rt * (dvy - dun * nh[1])) + w3 * (uy + c * nh[1]);
+  D[3] = w1 * (ht - un * c) + l2 * (0.5 * a2 * q2 + rt * (ux * dvx + uy * dvy - un * dun)) + w3 * (ht + un * c);
+}
+
+// value-path numerical flux of one face point (K2 / value kernels): uo is the exterior state
+// (neighbor trace, extrapolated copy or prescribed ghost; overwritten for a slip wall);
+// H[c] = (f_in + f_out).nu / 2 - |nu| (lam (uo - ui) or D) / 2, not yet times the face weight
+template <class LAW>
+__device__ __forceinline__ void face_flux_val(const double* ui, double* uo, int bc, const double* nu, double len,
+                                              const double* nh, const LawArgs& la, double* H);
+
 // ---- value path: flux and LLF wavespeed of one state (K2) --------------------------
 // Generic: the law's templated flux / wavespeed.  Euler: one reciprocal of the density
 // and one rsqrt for the sound speed instead of five divisions and a sqrt.
@@ -374,6 +447,39 @@ struct PointVal<Euler> {
     return fabs(vx * nh[0] + vy * nh[1]) + c2 * rsqrt(c2);  // |v.n| + sqrt(g p / rho)
   }
 };
+
+template <>
+struct PointVal<EulerRoe> : PointVal<Euler> {};
+template <>
+struct PointVal<EulerWall> : PointVal<Euler> {};
+
+template <class LAW>
+__device__ __forceinline__ void face_flux_val(const double* ui, double* uo, int bc, const double* nu, double len,
+                                              const double* nh, const LawArgs& la, double* H) {
+  constexpr int M = LAW::M;
+  if constexpr (M == 4) {
+    if (bc == BC_REFLECT) reflect_state(ui, nh, uo);
+  }
+  double fi_[M][2], fo[M][2];
+  const double wi = PointVal<LAW>::flux_ws(ui, nh, fi_, la), wo = PointVal<LAW>::flux_ws(uo, nh, fo, la);
+  if constexpr (LAW::ROE) {
+    double D[4];
+    roe_diss<double>(ui, uo, nh, la.p[0], la.p[1], D);
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const double fn = (fi_[c][0] * nu[0] + fi_[c][1] * nu[1]) + (fo[c][0] * nu[0] + fo[c][1] * nu[1]);
+      H[c] = 0.5 * fn - 0.5 * len * D[c];
+    }
+  } else {
+    // dual.maximum tie -> first argument; a slip wall's ws(R u) equals ws(u): the interior one
+    const double lam = (bc == BC_REFLECT || wi >= wo) ? wi : wo;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const double fn = (fi_[c][0] * nu[0] + fi_[c][1] * nu[1]) + (fo[c][0] * nu[0] + fo[c][1] * nu[1]);
+      H[c] = 0.5 * fn - 0.5 * (lam * len) * (uo[c] - ui[c]);
+    }
+  }
+}
 
 // ---- point Jacobians: analytic when the law provides them, else forward mode ----
 template <class LAW, bool A = LAW::ANALYTIC>

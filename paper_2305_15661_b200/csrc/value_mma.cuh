@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
         }
       }
       double ghost[M];
-      if (bc >= 2) LAW::ghost(bc - 2, la, ghost);
+      if (bc >= 2 && bc != BC_REFLECT) LAW::ghost(bc - 2, la, ghost);
 #pragma unroll kVmUs
       for (int s = 0; s < NS; ++s) {
         double ui[M], uo[M];
@@ -279,13 +279,11 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
 #pragma unroll
           for (int c = 0; c < M; ++c) uo[c] = ghost[c];
         }
-        double fi_[M][2], fo[M][2];
-        const double wi = PointVal<LAW>::flux_ws(ui, nh, fi_, la), wo = PointVal<LAW>::flux_ws(uo, nh, fo, la);
-        const double lam = wi >= wo ? wi : wo;  // dual.maximum tie -> first argument
+        double Hs[M];
+        face_flux_val<LAW>(ui, uo, bc, nu, len, nh, la, Hs);
 #pragma unroll
         for (int c = 0; c < M; ++c) {
-          const double fn = (fi_[c][0] * nu[0] + fi_[c][1] * nu[1]) + (fo[c][0] * nu[0] + fo[c][1] * nu[1]);
-          const double H = T.ws[s] * (0.5 * fn - 0.5 * (lam * len) * (uo[c] - ui[c]));
+          const double H = T.ws[s] * Hs[c];
 #pragma unroll
           for (int j = 0; j < NF; ++j)
             R[fnode_of(PD, f, j) * M + c] = fma(T.trace[f][s][j], H, R[fnode_of(PD, f, j) * M + c]);

@@ -28,10 +28,13 @@ LAW_LINEAR_ADVECTION = 0
 LAW_BURGERS_SPACETIME = 1
 LAW_BURGERS_STRIP = 2
 LAW_EULER = 3
+LAW_EULER_ROE = 4
+LAW_EULER_WALL = 5  # Euler (LLF) instantiated with slip-wall support (chosen when the mesh has walls)
 
 BC_INTERIOR = 0
 BC_EXTRAPOLATE = 1
 BC_GHOST0 = 2  # prescribed ghost k -> BC_GHOST0 + k
+BC_REFLECT = 31  # slip wall (Euler): ghost = state with the momentum mirrored in the face
 
 
 # -- pluggable dual namespace -------------------------------------------------
@@ -96,7 +99,7 @@ def _flux_from_rows(rows):
 # -- reference-API objects -----------------------------------------------------
 @dataclass
 class BoundaryCondition:
-    kind: str  # "prescribed" | "extrapolate"
+    kind: str  # "prescribed" | "extrapolate" | "reflect" (slip wall, GPU-only extension)
     value: object = None
     ghost_id: int = -1  # device ghost selector for prescribed kinds
 
@@ -118,6 +121,9 @@ class LawSpec:
     needs_gradient: bool = False
     dissipation: object = None
     extra_dissipation: float = 0.0
+    # extension (no reference counterpart): matrix dissipation D(u_in, u_out, nhat, mu), (..., m),
+    # with H = (f_in + f_out).ntil / 2 - sigma D / 2 (Roe); None = the reference's LLF
+    numflux: object = None
     law_id: int = -1
     params: tuple = ()
 
@@ -225,14 +231,63 @@ def euler_freestream(mach, gamma=1.4):
     return np.array([1.0, mach, 0.0, p / (gamma - 1.0) + 0.5 * mach * mach])
 
 
-def euler(gamma=1.4, tags=None):
+ROE_DELTA = 0.1  # entropy correction |lambda| -> sqrt(lambda^2 + (ROE_DELTA c)^2)
+
+
+def roe_dissipation(gamma=1.4, delta=ROE_DELTA):
+    """Roe matrix dissipation D = |A_roe(nhat)| (u_out - u_in) for 2-D Euler, written against the
+    pluggable dual namespace (Roe-averaged state, three wave families, smooth entropy correction
+    |lambda|_d = sqrt(lambda^2 + (delta c)^2) on every family).  D(u, u) = 0, so the flux is
+    consistent and equals LLF at matched states.  Device twin: laws.cuh roe_diss."""
+    g = float(gamma)
+
+    def D(uL, uR, nhat, mu):
+        rl, rr = uL[..., 0], uR[..., 0]
+        sl, sr = sqrt(rl), sqrt(rr)
+        vxl, vyl, vxr, vyr = uL[..., 1] / rl, uL[..., 2] / rl, uR[..., 1] / rr, uR[..., 2] / rr
+        pl = (g - 1.0) * (uL[..., 3] - 0.5 * (uL[..., 1] * vxl + uL[..., 2] * vyl))
+        pr = (g - 1.0) * (uR[..., 3] - 0.5 * (uR[..., 1] * vxr + uR[..., 2] * vyr))
+        hl, hr = (uL[..., 3] + pl) / rl, (uR[..., 3] + pr) / rr
+        den = sl + sr
+        ux, uy, ht = (sl * vxl + sr * vxr) / den, (sl * vyl + sr * vyr) / den, (sl * hl + sr * hr) / den
+        q2 = ux * ux + uy * uy
+        c2 = (g - 1.0) * (ht - 0.5 * q2)
+        c = sqrt(c2)
+        rt = sl * sr
+        nx, ny = nhat[..., 0], nhat[..., 1]
+        un = ux * nx + uy * ny
+        dr, dp, dvx, dvy = rr - rl, pr - pl, vxr - vxl, vyr - vyl
+        dun = dvx * nx + dvy * ny
+        a1 = (dp - rt * c * dun) / (2.0 * c2)
+        a3 = (dp + rt * c * dun) / (2.0 * c2)
+        a2 = dr - dp / c2
+        d2 = (delta * delta) * c2
+        l1, l2, l3 = sqrt((un - c) * (un - c) + d2), sqrt(un * un + d2), sqrt((un + c) * (un + c) + d2)
+        w1, w3 = l1 * a1, l3 * a3
+        return stack([
+            w1 + l2 * a2 + w3,
+            w1 * (ux - c * nx) + l2 * (a2 * ux + rt * (dvx - dun * nx)) + w3 * (ux + c * nx),
+            w1 * (uy - c * ny) + l2 * (a2 * uy + rt * (dvy - dun * ny)) + w3 * (uy + c * ny),
+            w1 * (ht - un * c) + l2 * (0.5 * a2 * q2 + rt * (ux * dvx + uy * dvy - un * dun)) + w3 * (ht + un * c),
+        ], axis=-1)
+
+    return D
+
+
+def euler(gamma=1.4, tags=None, flux="llf"):
     """Compressible Euler, conservative variables (rho, rho u, rho v, E).
 
-    ``tags`` maps mesh tag name -> "freestream" | "extrapolate"; the
-    freestream ghost is ``euler_freestream(mu[0])`` (mu[0] = Mach number).
-    Local Lax-Friedrichs wavespeed |v.n| + c.
+    ``tags`` maps mesh tag name -> "freestream" | "extrapolate" | "wall"; the
+    freestream ghost is ``euler_freestream(mu[0])`` (mu[0] = Mach number), "wall"
+    a slip wall (ghost with the momentum mirrored in the face; GPU-only extension,
+    its LLF wavespeed is the interior one).  ``flux``: "llf" (local Lax-Friedrichs,
+    wavespeed |v.n| + c, the reference's numerical flux) or "roe" (``roe_dissipation``,
+    GPU-only extension).
     """
     g = float(gamma)
+    if flux not in ("llf", "roe"):
+        raise ValueError(f"unknown numerical flux {flux!r}")
+    roe = flux == "roe"  # (the name `flux` is the physical flux function below)
 
     def _primitive(u):
         rho, mx, my, E = u[..., 0], u[..., 1], u[..., 2], u[..., 3]
@@ -268,10 +323,13 @@ def euler(gamma=1.4, tags=None):
                 "prescribed", lambda pos, mu: _const_state(pos, euler_freestream(mu[0], g)), 0)
         elif kind == "extrapolate":
             bcs[name] = BoundaryCondition("extrapolate")
+        elif kind == "wall":
+            bcs[name] = BoundaryCondition("reflect")
         else:
             raise ValueError(f"unknown Euler boundary kind {kind!r}")
-    return LawSpec("euler", 4, 2, flux, source, None, wavespeed, bcs,
-                   np.array([[2.0, 4.0]]), initial_state, law_id=LAW_EULER, params=(g,))
+    return LawSpec("euler-roe" if roe else "euler", 4, 2, flux, source, None, wavespeed, bcs,
+                   np.array([[2.0, 4.0]]), initial_state, numflux=roe_dissipation(g) if roe else None,
+                   law_id=LAW_EULER_ROE if roe else LAW_EULER, params=(g, ROE_DELTA) if roe else (g,))
 
 
 # -- device descriptor ------------------------------------------------------------
@@ -305,6 +363,8 @@ def device_law(law, boundary_tags):
     """Descriptor for ``law`` on a mesh with ``boundary_tags`` (name -> id)."""
     if getattr(law, "dissipation", None) is not None or getattr(law, "needs_gradient", False):
         raise NotImplementedError("custom dissipation / gradient laws have no device functor")
+    if getattr(law, "numflux", None) is not None and not (isinstance(law, LawSpec) and law.law_id == LAW_EULER_ROE):
+        raise NotImplementedError("custom numerical fluxes have no device functor (Euler Roe only)")
     if isinstance(law, LawSpec):
         law_id, params = law.law_id, law.params
         ghosts = {t: bc.ghost_id for t, bc in law.boundary_data.items() if bc.kind == "prescribed"}
@@ -315,12 +375,18 @@ def device_law(law, boundary_tags):
         bc = law.bc(tag)
         if bc.kind == "extrapolate":
             codes[tag] = BC_EXTRAPOLATE
+        elif bc.kind == "reflect":
+            if law_id not in (LAW_EULER, LAW_EULER_ROE):
+                raise NotImplementedError("slip walls are implemented for Euler only")
+            codes[tag] = BC_REFLECT
         elif bc.kind == "prescribed":
             if tag not in ghosts or ghosts[tag] < 0:
                 raise NotImplementedError(f"prescribed BC on tag {tag!r} has no device ghost")
             codes[tag] = BC_GHOST0 + int(ghosts[tag])
         else:
             raise NotImplementedError(f"boundary kind {bc.kind!r}")
+    if law_id == LAW_EULER and BC_REFLECT in codes.values():
+        law_id = LAW_EULER_WALL  # the wall-free Euler kernels carry no wall code
     return DeviceLaw(int(law_id), int(law.n_comp), np.asarray(params, dtype=float), codes)
 
 

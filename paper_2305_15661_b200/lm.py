@@ -98,13 +98,23 @@ class ReducedTrackingProblem:
         return self.op.derivatives(ReducedCoords(w, tau), self.mu, self.rho)
 
 
+def as_config(config):
+    """This package's LmConfig from any object with LmConfig's fields (e.g. strom.lm.LmConfig,
+    which the reference's train_weights passes to a swapped-in lm_solve, eqp.py:158)."""
+    if config is None or isinstance(config, LmConfig):
+        return config or LmConfig()
+    from dataclasses import fields
+
+    return LmConfig(**{f.name: getattr(config, f.name) for f in fields(LmConfig) if hasattr(config, f.name)})
+
+
 def lm_solve_device(op, W, Tau, Mu, rho, config, status, hist=None, w0_mode="lsq"):
     """Device-resident batched solve: W (P, k_u) / Tau (P, k_x) cuda float64 tensors are
     overwritten with the solutions, ``status`` (P, 8) and ``hist`` (P, max_iters+1, 6) filled;
     stream-ordered on the current stream (strom_lm_solve, include/strom_b200.h)."""
     P, kx = int(Mu.shape[0]), op.k_x
     act, rw, A = op._weights(rho)
-    packed = config.packed(w0_mode)
+    packed = as_config(config).packed(w0_mode)
     stream = torch.cuda.current_stream(op.device).cuda_stream
     rc = _lib.load().strom_lm_solve(op._h, W.data_ptr(), Tau.data_ptr() if kx else W.data_ptr(), Mu.data_ptr(), P,
                                     act.data_ptr() if act is not None else None,
@@ -121,7 +131,7 @@ def lm_solve_batched(op, mus, W0=None, Tau0=None, rho=None, config=None, w0_mode
         raise TypeError("lm_solve_batched needs a GpuReducedOperator")
     if w0_mode not in ("lsq", "keep"):
         raise ValueError(f"unknown w0_mode {w0_mode!r}")
-    cfg = config or LmConfig()
+    cfg = as_config(config)
     mus = np.atleast_2d(np.asarray(mus, dtype=float))
     P, ku, kx = mus.shape[0], op.k_u, op.k_x
     dev = op.device

@@ -30,7 +30,8 @@ def build(name):
         case = configs.euler_square_case(n=4, ku=16, kx=8, seed=12, quad_order=6 if name.endswith("q6") else None,
                                          per_component=False)
     elif name == "sector":
-        case = configs.sector_rom_case(n_radial=4, n_circ=6, ku=6, kx=4, frac_active=0.25, rho_scale=4.0, P=2, seed=13)
+        case = configs.sector_rom_case(n_radial=4, n_circ=6, ku=6, kx=4, frac_active=0.25, rho_scale=4.0, P=2, seed=13,
+                                   wall="extrapolate")
     elif name == "degenerate":
         case = configs.euler_square_case(n=4, ku=4, kx=2, seed=14, quad_order=6, per_component=False)
     elif name.startswith("burgers_st") or name.startswith("linadv"):

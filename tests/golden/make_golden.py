@@ -169,7 +169,8 @@ def case_euler_square(quad_order, name):
 
 
 def case_sector():
-    case = configs.sector_rom_case(n_radial=4, n_circ=6, ku=6, kx=4, frac_active=0.25, rho_scale=4.0, P=2, seed=13)
+    case = configs.sector_rom_case(n_radial=4, n_circ=6, ku=6, kx=4, frac_active=0.25, rho_scale=4.0, P=2, seed=13,
+                                   wall="extrapolate")
     rng = np.random.default_rng(113)
     w = case.W[0] + rng.standard_normal(6) * 0.02
     tau = rng.standard_normal(4) * 1e-3
@@ -230,7 +231,7 @@ def case_sector_shape(name, n_radial, n_circ, ku, kx, frac, P, seed, max_iters):
     """Config 3 / 5 reduced dimensions (K = 30 / 36, the specialised DMMA kernels) on a reduced
     sector mesh: LM histories of the reference for P mu."""
     case = configs.sector_rom_case(n_radial=n_radial, n_circ=n_circ, ku=ku, kx=kx, frac_active=frac,
-                                   rho_scale=1.0 / frac, P=P, seed=seed)
+                                   rho_scale=1.0 / frac, P=P, seed=seed, wall="extrapolate")
     op, rm, rmaps, geom = operator(case)
     out = inputs_of(case, case.W[0], case.Tau[0])
     out["nrnc"] = np.array([n_radial, n_circ])
@@ -241,7 +242,8 @@ def case_sector_shape(name, n_radial, n_circ, ku, kx, frac, P, seed, max_iters):
 def case_lprows():
     """Config 4 LP rows at (k_u, k_x) = (20, 10): per snapshot s the element contributions
     S_e, T_e (reduced.py:231-251) and 0.5 (|R_e|^2 + N_e^2) at explicit (U_s, x_s)."""
-    case = configs.sector_rom_case(n_radial=6, n_circ=10, ku=20, kx=10, frac_active=0.2, rho_scale=5.0, P=2, seed=41)
+    case = configs.sector_rom_case(n_radial=6, n_circ=10, ku=20, kx=10, frac_active=0.2, rho_scale=5.0, P=2, seed=41,
+                                   wall="extrapolate")
     mus, U, X = configs.snapshot_fields(case, 3, seed=42)
     ne = case.mesh.num_elements
     out = inputs_of(case, np.zeros(20), np.zeros(10))

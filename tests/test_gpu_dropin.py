@@ -81,7 +81,14 @@ def test_reference_lm_solve_on_gpu_operator(S):
         runs.append(S["lm"].lm_solve(prob, S["lm"].LmConfig(max_iters=20)))  # the reference's own LM loop
     a, b = runs
     assert a.reason == b.reason and a.n_iters == b.n_iters and a.history.shape == b.history.shape
-    assert np.allclose(a.history, b.history, rtol=1e-8, atol=0.0, equal_nan=True)
+    # decisions (iteration, lambda, alpha) and J to 1e-8; the gradient norms |S|, |T| relative to
+    # their column scale (they are differences of O(1) terms; the state init drives |S| to rounding
+    # level, and the GPU's summation order moves them by ~1e-7 of the scale)
+    h, hr = b.history, a.history
+    assert np.array_equal(h[:, 0], hr[:, 0]) and np.array_equal(h[:, 5], hr[:, 5], equal_nan=True)
+    assert np.allclose(h[:, [1, 4]], hr[:, [1, 4]], rtol=1e-8, atol=0.0)
+    for col in (2, 3):
+        assert np.all(np.abs(h[:, col] - hr[:, col]) <= 1e-6 * np.max(np.abs(hr[:, col])))
     assert rel_err(b.w, a.w) < 1e-8 and abs(b.objective - a.objective) <= 1e-10 * abs(a.objective)
 
 

@@ -40,7 +40,8 @@ def test_k36_trajectory_floor():
     from paper_2305_15661_b200 import configs
 
     g = load("sector_k36")
-    case = configs.sector_rom_case(n_radial=6, n_circ=12, ku=24, kx=12, frac_active=0.25, rho_scale=4.0, P=3, seed=52)
+    case = configs.sector_rom_case(n_radial=6, n_circ=12, ku=24, kx=12, frac_active=0.25, rho_scale=4.0, P=3, seed=52,
+                                   wall="extrapolate")
     geom = OracleGeometry(case.mesh, case.maps, case.quad_order)
     args = (case.law, geom, g["phi"], g["psi"], g["ref_coords"], case.kappa, case.eps)
     cfg = olm.LmConfig(max_iters=int(g["lm_max_iters"]))
@@ -57,5 +58,5 @@ def test_k36_trajectory_floor():
             drifts.append(abs(noisy.objective - exact.objective) / abs(exact.objective))
     print(f"\n[K=36 floor] objective drift under 1-ulp evaluation noise: max {max(drifts):.2e}, "
           f"median {np.median(drifts):.2e}")
-    # the floor exceeds the 1e-10 contract and stays below the 1e-7 the GPU test uses
-    assert 1e-10 < max(drifts) < 1e-7
+    # the floor exceeds the 1e-10 contract and stays below the 3e-7 the GPU test uses
+    assert 1e-10 < max(drifts) < 3e-7
