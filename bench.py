@@ -471,8 +471,10 @@ def run_cfg5(args, dev, world, rank, local, group=None):
     rho = WeightVector(case.rho)
     cfg = LmConfig(max_iters=10)
 
+    st = {}
+
     def step():
-        return greedy_step(op, case.mus, [], rho, case.W[0], None, cfg, rank, world, group)
+        return greedy_step(op, case.mus, [], rho, case.W[0], None, cfg, rank, world, group, stats=st)
 
     step()
     torch.cuda.synchronize()
@@ -490,6 +492,9 @@ def run_cfg5(args, dev, world, rank, local, group=None):
     return {"metric": "greedy candidate evaluations/sec (ROM LM solve + full-mesh indicator, fp64)",
             "value": len(case.mus) / wall, "unit": "candidates/s", "higher_is_better": True, "scaling": "strong",
             "ms_per_step": 1e3 * wall, "steps": steps, "argmax": [float(v), int(i)],
+            "rank0_failed_candidates": st.get("failed"), "rank0_candidates": st.get("candidates"),
+            "failed_note": "a candidate fails (+inf, SPEC.md:492) when its reconstructed full mesh inverts an element "
+                           "(reference: DegenerateMappingError); with untrained seeded bases most do",
             "config": {"workload": "cfg5: 160,000-triangle sector, 1024 candidate mu ~ U[2,4], k_u=24, k_x=12, "
                                    "4,800 EQP elements (3%), LM max_iters=10, indicator ||R||_2 on the full mesh",
                        "parallelism": f"candidates interleaved over {world} rank(s) + all_gather argmax",

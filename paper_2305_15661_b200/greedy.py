@@ -72,8 +72,10 @@ def indicators(op, mus, W, Tau):
     return np.where(degen.cpu().numpy() > 0, np.inf, ind)
 
 
-def greedy_step(op, cand_mus, selected, rho, W0=None, Tau0=None, lm_config=None, rank=0, world=1, group=None):
-    """One greedy search over this rank's candidate shard -> global (indicator, index)."""
+def greedy_step(op, cand_mus, selected, rho, W0=None, Tau0=None, lm_config=None, rank=0, world=1, group=None,
+                stats=None):
+    """One greedy search over this rank's candidate shard -> global (indicator, index).
+    ``stats`` (dict, optional) receives this rank's candidate / failed-candidate counts."""
     from .lm import lm_solve_batched
 
     ids = shard(len(cand_mus), rank, world)
@@ -88,4 +90,6 @@ def greedy_step(op, cand_mus, selected, rho, W0=None, Tau0=None, lm_config=None,
     # solve that ended on a degenerate mapping (lm.py:150,231 catch DegenerateMappingError)
     failed = np.array([(not np.isfinite(r.objective)) or r.reason == "degenerate" for r in res])
     ind = np.where(failed, np.inf, ind)
+    if stats is not None:
+        stats.update(candidates=len(ids), failed=int(np.sum(~np.isfinite(ind))))
     return global_argmax(ind, ids, selected, group)

@@ -32,9 +32,11 @@ def snapshot_fields_device(case, ids, seed, device, jitter=0.05, amp=0.05, mach_
     """Config 4 training snapshots (state and mesh perturbations as in config 2) for the
     snapshot indices ``ids``, generated on ``device``: (mus (S, 1) host, U (S, N_u), X (S, N_x)).
 
-    Snapshot s uses its own generator (seed * 1_000_003 + s): freestream(Mach mu_s) times
-    (1 + U(-jitter, jitter)) per DG node and component, and the reference coordinates plus
-    four sinusoid modes of amplitude amp * h (configs.displacement)."""
+    Snapshot s uses its own generator (seed * 1_000_003 + s): freestream(Mach mu_s) perturbed
+    per DG node in its primitive variables, rho, u and p times (1 + U(-jitter, jitter)) and
+    v = u U(-jitter, jitter) (conservative per-component jitter makes the pressure negative at
+    Mach ~4), and the reference coordinates plus four sinusoid modes of amplitude amp * h
+    (configs.displacement)."""
     mesh = case.mesh
     ne, nb = mesh.num_elements, 6
     nodes = torch.as_tensor(mesh.nodes, dtype=torch.float64, device=device)
@@ -49,10 +51,10 @@ def snapshot_fields_device(case, ids, seed, device, jitter=0.05, amp=0.05, mach_
         mu = float(mach_range[0] + (mach_range[1] - mach_range[0]) * torch.rand(1, generator=g, device=device,
                                                                                   dtype=torch.float64))
         mus[j, 0] = mu
-        ff = torch.tensor([1.0, mu, 0.0, (1.0 / gamma) / (gamma - 1.0) + 0.5 * mu * mu], dtype=torch.float64,
-                          device=device)
-        fac = 1.0 + jitter * (2.0 * torch.rand((ne * nb, 4), generator=g, device=device, dtype=torch.float64) - 1.0)
-        U[j] = (fac * ff).reshape(-1)
+        d = jitter * (2.0 * torch.rand((ne * nb, 4), generator=g, device=device, dtype=torch.float64) - 1.0)
+        rho, u = 1.0 + d[:, 0], mu * (1.0 + d[:, 1])
+        v, p = mu * d[:, 2], (1.0 / gamma) * (1.0 + d[:, 3])
+        U[j] = torch.stack([rho, rho * u, rho * v, p / (gamma - 1.0) + 0.5 * rho * (u * u + v * v)], 1).reshape(-1)
         x = nodes.clone()
         for _ in range(4):
             k = torch.randint(1, 5, (2,), generator=g, device=device).double()
