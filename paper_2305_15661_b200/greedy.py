@@ -93,3 +93,113 @@ def greedy_step(op, cand_mus, selected, rho, W0=None, Tau0=None, lm_config=None,
     if stats is not None:
         stats.update(candidates=len(ids), failed=int(np.sum(~np.isfinite(ind))))
     return global_argmax(ind, ids, selected, group)
+
+
+# -- Algorithm 1 (SPEC.md greedy-driver, no reference code) ---------------
+class BasisInSpanError(ValueError):
+    """New column numerically inside the span of the basis (strom/reduced.py:20-22)."""
+
+
+class CandidateSetExhausted(RuntimeError):
+    """Every candidate parameter is already a training parameter (SPEC greedy_search errors)."""
+
+
+def gram_schmidt_append(basis, new_column, tol=1e-10):
+    """Append one column to an orthonormal basis: modified Gram-Schmidt with one
+    re-orthogonalisation pass, BasisInSpanError below ``tol`` times the column norm
+    (semantics of strom/reduced.py:88-113)."""
+    col = np.asarray(new_column, dtype=float).reshape(-1).copy()
+    nrm0 = np.linalg.norm(col)
+    if nrm0 == 0.0:
+        raise BasisInSpanError("zero column")
+    basis = np.asarray(basis, dtype=float)
+    if basis.size == 0:
+        return (col / nrm0)[:, None]
+    basis = basis.reshape(col.shape[0], -1)
+    v = col
+    for _ in range(2):
+        v = v - basis @ (basis.T @ v)
+    nrm = np.linalg.norm(v)
+    if nrm < tol * nrm0:
+        raise BasisInSpanError(f"column inside span (residual {nrm:.3e} vs norm {nrm0:.3e})")
+    return np.column_stack([basis, v / nrm])
+
+
+def seed_index(cand_mus):
+    """mu_1 = argmin ||mu - centroid|| over the candidate set, first index on ties (SPEC seed)."""
+    mus = np.atleast_2d(np.asarray(cand_mus, dtype=float))
+    d = np.linalg.norm(mus - mus.mean(axis=0), axis=1)
+    return int(np.flatnonzero(d == d.min())[0])
+
+
+class GreedyState:
+    """Training state of Algorithm 1 (SPEC GreedyState): selected candidate indices, bases,
+    weights, snapshots and one metrics record per iteration."""
+
+    def __init__(self, phi, psi, ref_coords, weights, selected, snapshots):
+        from .reduced import ReducedBases
+
+        self.bases = ReducedBases(phi, psi, ref_coords)
+        self.weights = weights
+        self.selected = list(selected)
+        self.snapshots = list(snapshots)
+        self.metrics = []
+
+    @property
+    def j(self):
+        return len(self.selected)
+
+
+def greedy_train(law, geom, cand_mus, hdm_snapshot, n_iter, dist_config, train_weights, lm_config=None, align=None,
+                 rank=0, world=1, group=None, device=None):
+    """Greedy training (Algorithm 1): seed, then per iteration greedy search (GPU, candidates
+    sharded over ranks), snapshot alignment, HDM snapshot, basis growth by Gram-Schmidt and
+    EQP weight retraining with the previous weights as the guess.
+
+    The full-space solves are callbacks — the HDM / tracking solves are outside this repo's
+    hot path: ``hdm_snapshot(mu, x_aligned) -> (U*, x*)`` and, optionally,
+    ``align(bases, mu) -> x_aligned`` (None: x = X, SPEC's no-alignment fallback).
+    ``train_weights(bases, guess, selected_mus) -> WeightVector`` is the EQP LP (e.g. the
+    reference's strom.eqp.train_weights with the GPU operator swapped in, dropin.install).
+    Seed (SPEC): mu_1 nearest the candidate centroid, Phi_1 = U*(mu_1)/||U*||,
+    Psi_1 = X/||X||, rho_1 trained from the all-ones guess.
+    """
+    import time
+
+    from .eqp import WeightVector
+    from .lm import LmConfig
+    from .reduced import GpuReducedOperator
+
+    cand_mus = np.atleast_2d(np.asarray(cand_mus, dtype=float))
+    X = np.asarray(geom.mesh.nodes, dtype=float).ravel()
+    i1 = seed_index(cand_mus)
+    U1, _ = hdm_snapshot(cand_mus[i1], X)
+    phi = gram_schmidt_append(np.zeros((len(U1), 0)), U1)
+    psi = gram_schmidt_append(np.zeros((len(X), 0)), X)
+    state = GreedyState(phi, psi, X, None, [i1], [(np.asarray(U1), X)])
+    t0 = time.perf_counter()
+    state.weights = train_weights(state.bases, WeightVector.ones(geom.mesh.num_elements), cand_mus[state.selected])
+    state.metrics.append({"j": 1, "mu": cand_mus[i1].tolist(), "T_rho": time.perf_counter() - t0,
+                          "active": int(len(state.weights.active))})
+    for _ in range(1, n_iter):
+        if len(state.selected) >= len(cand_mus):
+            raise CandidateSetExhausted("all candidate parameters are training parameters")
+        op = GpuReducedOperator(law, geom, state.bases, dist_config, device=device)
+        t0 = time.perf_counter()
+        w0 = state.bases.phi.T @ state.snapshots[-1][0]  # projection of the latest snapshot
+        v, i = greedy_step(op, cand_mus, state.selected, state.weights, w0, None, lm_config or LmConfig(), rank,
+                           world, group)
+        t_gs = time.perf_counter() - t0
+        if i < 0:
+            raise CandidateSetExhausted("no selectable candidate")
+        x_al = align(state.bases, cand_mus[i]) if align is not None else X
+        U, x = hdm_snapshot(cand_mus[i], x_al)
+        state.bases.phi = gram_schmidt_append(state.bases.phi, U)
+        state.bases.psi = gram_schmidt_append(state.bases.psi, np.asarray(x, dtype=float) - X)
+        state.selected.append(int(i))
+        state.snapshots.append((np.asarray(U), np.asarray(x)))
+        t0 = time.perf_counter()
+        state.weights = train_weights(state.bases, state.weights, cand_mus[state.selected])
+        state.metrics.append({"j": state.j, "mu": cand_mus[i].tolist(), "indicator": v, "T_gs": t_gs,
+                              "T_rho": time.perf_counter() - t0, "active": int(len(state.weights.active))})
+    return state

@@ -21,8 +21,10 @@ t0 = time.perf_counter()
 res = lm_solve_batched(op, case.mus, W0, None, rho, cfg)
 dt = time.perf_counter() - t0
 print(f"wall {dt*1e3:.2f} ms, iters {np.mean([r.n_iters for r in res]):.1f}")
-from torch.profiler import profile, ProfilerActivity
-with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-    lm_solve_batched(op, case.mus, W0, None, rho, cfg)
-    torch.cuda.synchronize()
-print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25))
+import ctypes
+from paper_2305_15661_b200 import _lib
+st = (ctypes.c_int32 * 3)()
+_lib.load().strom_lm_stats(op._h, st)
+print("rounds, derivative passes, objective passes:", list(st))
+# per-kernel times of the graph's kernel nodes: run under
+#   ncu --metrics gpu__time_duration.sum --csv python tools/prof_lm.py 3  (tools/launch_summary.py)
