@@ -49,15 +49,15 @@ def load():
         raise ImportError("reference strom not installed (baseline/_ref) and /root/reference absent")
     if d not in sys.path:
         sys.path.insert(0, d)
-    from strom import distortion, dual, geometry, lm, meshing, quadrature, reduced  # noqa: F401
+    from strom import conslaw, distortion, dual, geometry, lm, meshing, quadrature, reduced  # noqa: F401
     from strom import eqp
 
     from paper_2305_15661_b200 import laws as L, tables
 
     L.register_dual_backend(dual.Dual, dual)
     tables.install_degree6_rule(quadrature)
-    return dict(distortion=distortion, dual=dual, geometry=geometry, lm=lm, meshing=meshing, reduced=reduced,
-                eqp=eqp, path=d)
+    return dict(conslaw=conslaw, distortion=distortion, dual=dual, geometry=geometry, lm=lm, meshing=meshing,
+                reduced=reduced, eqp=eqp, path=d)
 
 
 def operator(case):

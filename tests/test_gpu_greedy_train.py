@@ -1,7 +1,8 @@
-"""Algorithm 1 orchestration on the GPU (greedy.greedy_train) with synthetic HDM snapshots:
-seed, greedy searches over the candidate set, Gram-Schmidt basis growth, weight retraining
-(the reference's train_weights with the GPU operator swapped in when the reference is
-installed), exhaustion error."""
+"""Algorithm 1 orchestration on the GPU (greedy.greedy_train) with synthetic HDM snapshots on
+the reference's Burgers space-time law: seed at the candidate centroid (SPEC example: the
+middle of the 3 x 3 grid on [3, 9] x [0.02, 0.075]), greedy searches over the candidate set,
+Gram-Schmidt basis growth, weight retraining (the reference's train_weights with the GPU
+operator swapped in when the reference is installed), exhaustion error."""
 
 import numpy as np
 import pytest
@@ -16,45 +17,46 @@ def test_greedy_train_bookkeeping():
         pytest.skip("no CUDA device")
     from paper_2305_15661_b200 import configs, laws as L
     from paper_2305_15661_b200.eqp import WeightVector
-    from paper_2305_15661_b200.greedy import CandidateSetExhausted, greedy_train, seed_index
+    from paper_2305_15661_b200.greedy import CandidateSetExhausted, greedy_train
     from paper_2305_15661_b200.lm import LmConfig
+    from paper_2305_15661_b200.mesh import build_box_mesh, get_geometry
 
-    case = configs.sector_rom_case(n_radial=3, n_circ=6, ku=2, kx=1, frac_active=0.5, rho_scale=2.0, P=1, seed=95,
-                                   wall="extrapolate")
-    geom, ne = case.geom, case.mesh.num_elements
-    cands = np.array([[2.0], [2.5], [3.0], [3.5], [4.0]])
-    rng = np.random.default_rng(1)
-    bump = 1.0 + 0.02 * rng.standard_normal(ne * 24)
+    mesh, maps = build_box_mesh(((0.0, 0.0), (2.0, 1.0)), 4, 3, degree_sol=2, n_comp=1)
+    law = L.burgers_spacetime()
+    geom, ne = get_geometry(mesh, maps), mesh.num_elements
+    cands = np.array([[a, b] for a in (3.0, 6.0, 9.0) for b in (0.02, 0.0475, 0.075)])
+    xy = np.repeat(mesh.nodes[mesh.elements[:, :3]].mean(axis=1), 6, axis=0)  # element centroids per DG node
 
-    def hdm_snapshot(mu, x):  # synthetic "HDM" state: freestream(mu) with a fixed perturbation
-        return np.tile(L.euler_freestream(float(mu[0])), ne * 6) * bump, x
+    def hdm_snapshot(mu, x):  # synthetic "HDM" state: a mu-dependent smooth field
+        return 1.0 + 0.1 * np.sin(mu[0] * xy[:, 0] + 40.0 * mu[1] * xy[:, 1]), x
 
-    def train(bases, guess, mus):  # all-ones weights keep the bookkeeping test independent of the LP
-        return WeightVector.ones(ne)
-
+    train = lambda bases, guess, mus: WeightVector.ones(ne)  # noqa: E731  (LP-independent bookkeeping)
     try:  # the reference's EQP LP with the GPU operator swapped in
         from oracle import strom_ref
+        from paper_2305_15661_b200 import dropin
 
         S = strom_ref.load()
-        from paper_2305_15661_b200 import dropin
 
         def train(bases, guess, mus):  # noqa: F811
             undo = dropin.install(lm=True)
             try:
                 cfg = S["eqp"].EqpTrainingConfig(delta=0.5, xi=np.asarray(mus))
                 rb = S["reduced"].ReducedBases(bases.phi, bases.psi, bases.ref_coords)
-                return S["eqp"].train_weights(case.law, case.mesh, case.maps, rb, guess, cfg, case.dist,
-                                              S["lm"].LmConfig(max_iters=5))
+                rmesh, rmaps = S["meshing"].build_structured_mesh(((0.0, 0.0), (2.0, 1.0)), 4, 3, degree_sol=2, n_comp=1)
+                sguess = S["eqp"].WeightVector(np.asarray(guess.rho))
+                return S["eqp"].train_weights(S["conslaw"].burgers_spacetime(), rmesh, rmaps, rb, sguess, cfg,
+                                              S["distortion"].DistortionConfig(1e-3), S["lm"].LmConfig(max_iters=5))
             finally:
                 undo()
     except ImportError:
         pass
 
-    st = greedy_train(case.law, geom, cands, hdm_snapshot, 3, case.dist, train, LmConfig(max_iters=5))
-    assert st.selected[0] == seed_index(cands) == 2
+    dist = configs.DistortionConfig(1e-3)
+    st = greedy_train(law, geom, cands, hdm_snapshot, 3, dist, train, LmConfig(max_iters=5))
+    assert np.allclose(cands[st.selected[0]], [6.0, 0.0475])  # seed: the centroid of the grid
     assert len(set(st.selected)) == 3 and st.bases.phi.shape[1] == 3 and st.bases.psi.shape[1] == 3
     assert np.allclose(st.bases.phi.T @ st.bases.phi, np.eye(3), atol=1e-12)
     assert np.allclose(st.bases.psi.T @ st.bases.psi, np.eye(3), atol=1e-12)
-    assert [m["j"] for m in st.metrics] == [1, 2, 3] and all(np.all(st.weights.rho >= 0.0) for _ in [0])
+    assert [m["j"] for m in st.metrics] == [1, 2, 3] and np.all(np.asarray(st.weights.rho) >= 0.0)
     with pytest.raises(CandidateSetExhausted):
-        greedy_train(case.law, geom, cands[:2], hdm_snapshot, 3, case.dist, train, LmConfig(max_iters=3))
+        greedy_train(law, geom, cands[:2], hdm_snapshot, 3, dist, train, LmConfig(max_iters=3))
