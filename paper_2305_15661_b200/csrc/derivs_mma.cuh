@@ -18,57 +18,18 @@
 namespace strom {
 
 constexpr int MTHREADS = 256;
-#ifndef STROM_RESID_MMA
-#define STROM_RESID_MMA 1  // R stage volume contraction on DMMA
-#endif
 #ifndef STROM_MMA_MAXNREG_WIDE
 #define STROM_MMA_MAXNREG_WIDE 240  // k_u > 16 runs 4 two-warp CTAs/SM (2 warps per SMSP): room for 240
-#endif
-#ifndef STROM_FACE3
-#define STROM_FACE3 0  // all three faces buffered (block sums, one barrier, projections): 4% slower on cfg2
-#endif
-#ifndef STROM_HREG
-#define STROM_HREG 1  // CT path, K <= 24: Gram accumulator in registers (fragment layout), to region A once
 #endif
 #ifndef STROM_HREG_WIDE
 #define STROM_HREG_WIDE 15  // k_u > 16 (240 registers): register Gram for up to 15 upper tiles (K <= 40)
 #endif
-#ifndef STROM_PREF
-#define STROM_PREF 0  // prefetch the projection B fragments into registers during the L stage (measured slower)
-#endif
-#ifndef STROM_PREF_E
-#define STROM_PREF_E 0  // own-projection B fragments loaded before the L stage
-#endif
-#ifndef STROM_XEARLY
-#define STROM_XEARLY 0  // dR/dx stage in the shadow of the L-GEMM DMMAs (own region): 2.7% slower (spills)
-#endif
-#ifndef STROM_L1PF
-#define STROM_L1PF 0  // L1 prefetch of the projection basis rows before the face stage (3% slower: spills)
-#endif
-#ifndef STROM_L_ROT
-#define STROM_L_ROT 1  // rotated conflict-free L stores (selects) vs plain stores (2-way conflicts)
-#endif
-#ifndef STROM_J_FLIP
-#define STROM_J_FLIP 0  // flipped conflict-free J fragment stores (selects): neutral vs plain stores
-#endif
-#ifndef STROM_DRX_ROT
-#define STROM_DRX_ROT 0  // rotated conflict-free dR/dx stores (selects) vs three plain stores
-#endif
-#ifndef STROM_PREF_NBR
-#define STROM_PREF_NBR 0  // L2 prefetch of the next unit's neighbor face-node rows
-#endif
-#ifndef STROM_PREF_JIT
-#define STROM_PREF_JIT 0  // each face's neighbor B fragments loaded at the top of its face step
-#endif
-#ifndef STROM_PHIBUF
-#define STROM_PHIBUF 0  // k_u = 16: next element basis block copied to smem by cp.async (measured 6% slower: spills)
-#endif
-#ifndef STROM_GFRAG
-#define STROM_GFRAG 1  // CT path: gradient partials from the J accumulators
-#endif
 #ifndef STROM_MMA_MAXNREG
-#define STROM_MMA_MAXNREG 168  // 3 warps per SMSP (12 per SM with 17 KB of smem per warp)
+#define STROM_MMA_MAXNREG 168  // 3 warps per SMSP (12 per SM with 15 KB of smem per warp)
 #endif
+// Measured and removed in round 2 (DESIGN.md §3 table): buffered three-face out-blocks,
+// register prefetch of the projection B fragments, cp.async staging of the next basis block,
+// the dR/dx stage in the L-GEMM shadow, L1 / L2 neighbor-row prefetch, flipped J stores.
 
 template <int NQ>
 struct MShape {
@@ -98,8 +59,8 @@ struct MShape {
   //   P/R : FX [field][NFSP] at LO           (face flux fields, read by the FD stage)
   //   F/J : one face's Lout [12][LDO] at LO  (projected right away)
   //   X/G : DRX [NU][LDX] at max(LA, NU LDJ) (CF, LOUT dead), Jt [NU][LDJ] at 0 (L dead)
-  static constexpr int LDL = 28, LDO = STROM_FACE3 ? 12 : 20;  // LDO == 12 mod 16: conflict-free too
-  static constexpr int NLO = STROM_FACE3 ? 3 : 1;               // out-block buffers (faces)
+  static constexpr int LDL = 28, LDO = 20;  // LDO == 4 mod 16: conflict-free half-warp fragment loads
+  static constexpr int NLO = 1;               // out-block buffer (one face at a time)
   // the two sides of BQ / CF sit 12 mod 16 doubles apart, so the 24 point lanes (12 per
   // side) of one store instruction hit 24 distinct banks
   static constexpr int BQS = 16 * NQC + 12, CFS = 16 * NFSP + 12;
@@ -124,16 +85,11 @@ struct MShape {
   // k_u > 16 gets the wide register budget (measured per pass: cfg3 -10%, cfg4 -3.5%, cfg5 -6.5%)
   __host__ __device__ static constexpr bool wide(int KUT) { return KUT > 16; }
   __host__ __device__ static constexpr bool hreg(int KUT, int KXT) {
-    return STROM_HREG && KUT > 0 && (KUT + KXT + 7) / 8 * ((KUT + KXT + 7) / 8 + 1) / 2 <= (wide(KUT) ? STROM_HREG_WIDE : 6);
+    return KUT > 0 && (KUT + KXT + 7) / 8 * ((KUT + KXT + 7) / 8 + 1) / 2 <= (wide(KUT) ? STROM_HREG_WIDE : 6);
   }
-  // the element's basis block Phi_e (24 rows of 8 16-byte chunks; chunk c of row r at
-  // c ^ 2(r & 3): conflict-free B-fragment loads, 2-way at most for the row-wise gather)
-  static constexpr int PHS = 16;
-  __host__ __device__ static constexpr bool phibuf(int KUT) { return STROM_PHIBUF && KUT == 16; }
-  __host__ __device__ static constexpr int warp_stride(int LDJ, int KP, int kx, bool hreg, bool phib = false) {
+  __host__ __device__ static constexpr int warp_stride(int LDJ, int KP, int kx, bool hreg) {
     const int a = LO + NLO * 12 * LDO, b = drx(LDJ) + NU * LDX;
-    const int s = RA + (a > b ? a : b) + (hreg ? 0 : hsize(KP)) + gtail(KP) + psr(kx) + (phib ? NU * PHS : 0) +
-                  (STROM_XEARLY ? NU * LDX : 0);
+    const int s = RA + (a > b ? a : b) + (hreg ? 0 : hsize(KP)) + gtail(KP) + psr(kx);
     return (s + 15) / 16 * 16 + 4;
   }
 };
@@ -189,7 +145,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   const int ku = CT ? KUT : r.ku, kx = CT ? KXT : r.kx, K = CT ? KT : r.K, KP = CT ? KPT : r.KP;
   const int LDJ = CT ? KPT + 4 : r.LDJ;
   // per-warp stride: a compile-time constant on the specialised path (cheap to rematerialise)
-  const int WSTR = CT ? SH::warp_stride(KPT + 4, KPT, KXT, SH::hreg(KUT, KXT), SH::phibuf(KUT)) : r.gx_warp_stride;
+  const int WSTR = CT ? SH::warp_stride(KPT + 4, KPT, KXT, SH::hreg(KUT, KXT)) : r.gx_warp_stride;
   double* const S = smem + (size_t)warp * WSTR;
   double* const RA = S + SH::RA;
   const int DRXo = SH::drx(LDJ);
@@ -199,20 +155,6 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   double* const HA = HREG ? S + SH::RA : GW - SH::hsize(KP);
   const int PRS = SH::prs(kx);
   double* const PR = (HREG ? GW : HA) - SH::psr(kx);  // Psi rows of the element's vertex coordinates
-  constexpr bool PHB = SH::phibuf(KUT);
-  double* const PHI = PR - NU * SH::PHS;  // Phi_e block (PHB)
-  double* const DRXE = (PHB ? PHI : PR) - NU * LDX;  // dR/dx rows (XEARLY)
-  // 16-byte async copies of element ue's 24 basis rows (KUT = 16: 8 chunks per row) into PHI
-  auto phi_async = [&](int ue) {
-#pragma unroll
-    for (int i = 0; i < NU * 8 / 32; ++i) {
-      const int q = lane + 32 * i, row = q >> 3, ch = q & 7;
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(PHI + row * SH::PHS + 2 * (ch ^ (2 * (row & 3))));
-      const double* src = r.phi + ((size_t)ue * NU + row) * 16 + 2 * ch;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
   constexpr int NT8T = CT ? (KUT + KXT + 7) / 8 : 1, NTRIT = NT8T * (NT8T + 1) / 2;
   double hacc[NTRIT][2];
 #pragma unroll
@@ -233,12 +175,13 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   for (int i = 0; i < 8; ++i) la.p[i] = r.lawp[i];
 #pragma unroll
   for (int i = 0; i < NMU; ++i) la.mu[i] = i < r.nmu ? r.mu[p * r.nmu + i] : 0.0;
-  // per-lane constant B fragments of the L GEMM: Phi[q][n'] at (q = 4ks + lane&3, n' = lane>>2)
+  // per-lane constant B fragments of the L GEMM: -Phi[q][n'] at (q = 4ks + lane&3, n' = lane>>2)
+  // (negated, so the accumulators come out as L = -sum_q Dq^T B_q Pq directly: exact)
   double phib[SH::NQ4 / 4];
 #pragma unroll
   for (int ks = 0; ks < SH::NQ4 / 4; ++ks) {
     const int q = 4 * ks + (lane & 3), np_ = lane >> 2;
-    phib[ks] = (q < NQ && np_ < NB) ? T.phi[q < NQ ? q : 0][np_ < NB ? np_ : 0] : 0.0;
+    phib[ks] = (q < NQ && np_ < NB) ? -T.phi[q < NQ ? q : 0][np_ < NB ? np_ : 0] : 0.0;
   }
   __syncthreads();
 
@@ -263,7 +206,6 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     const int idx0 = bx * nwarps + warp;
     if (idx0 < nunits && lane < 10) EI[lane] = index_word(r.active ? __ldg(r.active + idx0) : idx0, lane);
     __syncwarp();
-    if (PHB && idx0 < nunits) phi_async(EI[0]);
   }
   // per-lane gather roles (CT path): row lane (own row, or neighbor face 0 rows 0..7 for
   // lanes 24..31) and row lane + 32 (neighbor rows 8..35 for lanes 0..27)
@@ -319,22 +261,10 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         if (ok1) v1 = r.u0[(size_t)p * r.u0_stride + row1];
       }
       double2 b0[H], b1[H];
-      if (!PHB || lane >= NU) {
 #pragma unroll
-        for (int k2 = 0; k2 < H; ++k2) b0[k2] = ok0 ? __ldg(reinterpret_cast<const double2*>(src0) + k2) : make_double2(0.0, 0.0);
-      }
+      for (int k2 = 0; k2 < H; ++k2) b0[k2] = ok0 ? __ldg(reinterpret_cast<const double2*>(src0) + k2) : make_double2(0.0, 0.0);
 #pragma unroll
       for (int k2 = 0; k2 < H; ++k2) b1[k2] = ok1 ? __ldg(reinterpret_cast<const double2*>(src1) + k2) : make_double2(0.0, 0.0);
-      if (PHB) {  // own rows: the block copied in by cp.async during the previous element
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        __syncwarp();
-        if (lane < NU) {
-          const double2* ph2 = reinterpret_cast<const double2*>(PHI + lane * SH::PHS);
-          const int sw = 2 * (lane & 3);
-#pragma unroll
-          for (int k2 = 0; k2 < H; ++k2) b0[k2] = ph2[k2 ^ sw];
-        }
-      }
       const int lx = lane < 6 ? lane : 0;
       const int xrow = 2 * EI[1 + (lx >> 1)] + (lx & 1);
       double xv = r.xref[(size_t)p * r.x_stride + xrow];
@@ -654,38 +584,6 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       __syncwarp();
     }
     // ---- R: residual rows (volume / face split) and Tq ------------------------------
-#if !STROM_RESID_MMA
-    if (lane < NU) {
-      const int i = lane, n = i / M, c = i % M;
-      double tq[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const double f0 = RA[SH::FQ + (c * 2 + 0) * SH::NQC + q], f1 = RA[SH::FQ + (c * 2 + 1) * SH::NQC + q];
-        const double2 dd = *reinterpret_cast<const double2*>(s_dphi + (q * NB + n) * 2);
-        tq[0][0] = fma(dd.x, f0, tq[0][0]);
-        tq[0][1] = fma(dd.x, f1, tq[0][1]);
-        tq[1][0] = fma(dd.y, f0, tq[1][0]);
-        tq[1][1] = fma(dd.y, f1, tq[1][1]);
-      }
-      const double* adj = S + SH::MADJ;
-      const double rv = -(adj[0] * tq[0][0] + adj[1] * tq[0][1] + adj[2] * tq[1][0] + adj[3] * tq[1][1]);
-      double rf = 0.0;
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        const int j = face_local(f, n);
-        if (j >= 0)
-#pragma unroll
-          for (int s = 0; s < NS; ++s) rf = fma(T.trace[0][s][j], RA[SH::HS + c * NFSP + f * NS + s], rf);
-      }
-      S[SH::TQ + 0 * SH::TQS + i] = tq[0][0];
-      S[SH::TQ + 1 * SH::TQS + i] = tq[0][1];
-      S[SH::TQ + 2 * SH::TQS + i] = tq[1][0];
-      S[SH::TQ + 3 * SH::TQS + i] = tq[1][1];
-      S[SH::RV + i] = rv;
-      S[SH::RF + i] = rf;
-      S[SH::RT + i] = rv + rf;
-    }
-#else
     // Tq[(n,j)][(c,k)] = sum_q dphi[q][n][j] FQ[(c,k)][q] on DMMA: rows (n,j) in two 8-row
     // tiles, columns (c,k); the lane of row (n,j) holds c = lane&3, k = 0,1
     {
@@ -734,7 +632,6 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         S[SH::RT + i] = rv + rf;
       }
     }
-#endif
     // face responses to unit normal-vector perturbations (for the mesh tangents)
     if (lane < NFS) {
       const int fs = lane, f = fs / NS;
@@ -761,41 +658,6 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       }
     }
     // (no barrier: the L stage reads only BQ / CF; TQ / FD / R rows are read after later barriers)
-    // prefetch the projection's B fragments (basis rows of the element and of the
-    // neighbors' face nodes) so their load latency overlaps the L stage
-    double pfe[6][2], pfn[3][3][2];
-    const bool pref = STROM_PREF && ntu <= 2;
-    const bool prefe = (STROM_PREF || STROM_PREF_E) && ntu <= 2;
-    if (prefe) {
-      const double* phe = r.phi + (size_t)e * NU * ku;
-#pragma unroll
-      for (int ks = 0; ks < 6; ++ks)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          const int col = nt * 8 + (lane >> 2);
-          pfe[ks][nt] = (nt < ntu && col < ku) ? __ldg(phe + (size_t)(4 * ks + (lane & 3)) * ku + col) : 0.0;
-        }
-    }
-    if (pref) {
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        const bool interior = (fin[f] >> 3) == 0;
-        const int nf = fin[f] & 3;
-        const bool flip = (fin[f] >> 2) & 1;
-        const double* phn = r.phi + (size_t)(interior ? nbr[f] : 0) * NU * ku;
-#pragma unroll
-        for (int ks = 0; ks < 3; ++ks) {
-          const int jn = flip ? (ks == 0 ? 1 : (ks == 1 ? 0 : 2)) : ks;
-          const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            const int col = nt * 8 + (lane >> 2);
-            pfn[f][ks][nt] = (interior && nt < ntu && col < ku)
-                                 ? __ldg(phn + (size_t)(node * M + (lane & 3)) * ku + col) : 0.0;
-          }
-        }
-      }
-    }
     // next unit's index block: loaded here, stored to smem after the Jx stage
     const int wv = (nidx < nunits && lane < 10) ? index_word(nact, lane) : 0;
     // ---- X: local mesh Jacobian dR/dx (24 x 6) -------------------------------------------
@@ -826,23 +688,12 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         dr[2 * b + 1] += rx;  dr[2 * a + 1] -= rx;
         dr[2 * b + 0] -= ry;  dr[2 * a + 0] += ry;
       }
-#if STROM_DRX_ROT
-      {  // 16-byte pieces, order rotated by (i>>2)&1: conflict-free quarter-warp stores
-        double2* dst = reinterpret_cast<double2*>(drxb + i * LDX);
-        const bool rot = (i & 4) != 0;
-        const double2 pc[4] = {make_double2(dr[0], dr[1]), make_double2(dr[2], dr[3]), make_double2(dr[4], dr[5]),
-                               make_double2(0.0, 0.0)};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) dst[rot ? (t + 1) & 3 : t] = rot ? pc[(t + 1) & 3] : pc[t];
-      }
-#else
       {  // three 16-byte pieces (columns 6, 7 are never read: the Jx A fragments are predicated)
         double2* dst = reinterpret_cast<double2*>(drxb + i * LDX);
         dst[0] = make_double2(dr[0], dr[1]);
         dst[1] = make_double2(dr[2], dr[3]);
         dst[2] = make_double2(dr[4], dr[5]);
       }
-#endif
     }
     };
     // ---- L: volume local Jacobian on DMMA; X = Dq^T B_q fused into the A fragments ------
@@ -870,16 +721,12 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
           }
         }
       }
-      if (STROM_XEARLY) {  // independent scalar work while the L-GEMM DMMAs are in flight
-        __syncwarp();      // (FD / TQ rows of other lanes)
-        x_stage(DRXE);
-      }
       __syncwarp();  // BQ / CF reads of other lanes finished before L overwrites region A? (L lives after CF)
-      // write -L into L[(n,c)][(n',c')], n' = 2(lane&3) + {0,1}: the lane's 8 values are
+      // write L into L[(n,c)][(n',c')], n' = 2(lane&3) + {0,1}: the lane's 8 values are
       // contiguous (columns 8(lane&3) .. +7), written as four 16-byte pieces in an order
       // rotated by (lane&3)>>1 so every quarter-warp store hits 8 distinct bank groups
       if ((lane & 3) < 3) {
-        const bool rot = STROM_L_ROT && (lane & 2) != 0;
+        const bool rot = (lane & 2) != 0;
 #pragma unroll
         for (int mt = 0; mt < 3; ++mt) {
           double2* dst = reinterpret_cast<double2*>(RA + SH::LL + (mt * 8 + (lane >> 2)) * LDL + 8 * (lane & 3));
@@ -887,26 +734,14 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
           for (int t = 0; t < 4; ++t) {
             // piece pc = (t + rot) & 3 holds (h2 = pc >> 1, cp = 2 (pc & 1) + {0, 1})
             const int pa = t, pb = (t + 1) & 3;
-            const double xa = -lv[2 * (pa & 1)][mt][pa >> 1], ya = -lv[2 * (pa & 1) + 1][mt][pa >> 1];
-            const double xb = -lv[2 * (pb & 1)][mt][pb >> 1], yb = -lv[2 * (pb & 1) + 1][mt][pb >> 1];
-            if (STROM_L_ROT) dst[rot ? pb : pa] = make_double2(rot ? xb : xa, rot ? yb : ya);
-            else dst[pa] = make_double2(xa, ya);
+            const double xa = lv[2 * (pa & 1)][mt][pa >> 1], ya = lv[2 * (pa & 1) + 1][mt][pa >> 1];
+            const double xb = lv[2 * (pb & 1)][mt][pb >> 1], yb = lv[2 * (pb & 1) + 1][mt][pb >> 1];
+            dst[rot ? pb : pa] = make_double2(rot ? xb : xa, rot ? yb : ya);
           }
         }
       }
     }
     __syncwarp();
-    if (STROM_L1PF && CT) {  // projection B-fragment rows back into L1 (no registers held)
-      if (lane < NU) asm volatile("prefetch.global.L1 [%0];" ::"l"(r.phi + ((size_t)e * NU + lane) * ku));
-      for (int i = lane; i < NF * NF * M; i += 32) {
-        const int f = i / (NF * M), jj = (i / M) % NF, c = i % M;
-        if ((fin[f] >> 3) == 0) {
-          const int nf = fin[f] & 3;
-          const int node = jj == 0 ? nf : (jj == 1 ? (nf == 2 ? 0 : nf + 1) : 3 + nf);
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(r.phi + ((size_t)nbr[f] * NU + node * M + c) * ku));
-        }
-      }
-    }
     // face blocks, one face at a time: lanes 0-15 add the in-side block into L, lanes
     // 16-31 form Lout_f in a one-face buffer, then the warp projects it on the
     // neighbor's face-node basis rows straight into the J accumulators
@@ -917,84 +752,8 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       for (int mt = 0; mt < 3; ++mt) ju[nt][mt][0] = ju[nt][mt][1] = 0.0;
     const double* L = RA + SH::LL;
     double* Lo = RA + SH::LO;
-#if STROM_FACE3
-    // all faces' block sums first (in-blocks into L, out-blocks into three buffers), one
-    // barrier, then every face's projection on the neighbor's face-node rows
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
-      const int c = (lane & 15) >> 2, cp = lane & 3, side = lane >> 4;
-      double* Lof = Lo + f * 12 * LDO;
-      double cs[NS];
-#pragma unroll
-      for (int s = 0; s < NS; ++s) cs[s] = RA[SH::CF + side * SH::CFS + (c * M + cp) * NFSP + f * NS + s];
-#pragma unroll
-      for (int j = 0; j < NF; ++j)
-#pragma unroll
-        for (int jp = j; jp < NF; ++jp) {  // t2 is symmetric in (j, j'): one sum per pair
-          double v = 0.0;
-#pragma unroll
-          for (int s = 0; s < NS; ++s) v = fma(T.t2[j][jp][s], cs[s], v);
-          if (side == 0) {
-            RA[SH::LL + (fnode_of(PD, f, j) * M + c) * LDL + fnode_of(PD, f, jp) * M + cp] += v;
-            if (jp != j) RA[SH::LL + (fnode_of(PD, f, jp) * M + c) * LDL + fnode_of(PD, f, j) * M + cp] += v;
-          } else {
-            Lof[(j * M + c) * LDO + jp * M + cp] = v;
-            if (jp != j) Lof[(jp * M + c) * LDO + j * M + cp] = v;
-          }
-        }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int f = 0; f < 3; ++f) {
-      if ((fin[f] >> 3) == 0) {
-        const double* Lof = Lo + f * 12 * LDO;
-        const int nf = fin[f] & 3;
-        const bool flip = (fin[f] >> 2) & 1;
-        const double* phn = r.phi + (size_t)nbr[f] * NU * ku;
-#pragma unroll
-        for (int ks = 0; ks < 3; ++ks) {  // k = (j', c') = 4 ks + lane&3 -> j' = ks
-          const int jn = flip ? (ks == 0 ? 1 : (ks == 1 ? 0 : 2)) : ks;
-          const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
-          const int brow = node * M + (lane & 3);
-          double af[3];
-#pragma unroll
-          for (int mt = 0; mt < 3; ++mt) {
-            const int row = prow(mt, lane), n = row >> 2, c = row & 3;
-            const int j = face_local(f, n);
-            af[mt] = (mt != (f + 1) % 3 && j >= 0) ? Lof[(j * M + c) * LDO + 4 * ks + (lane & 3)] : 0.0;
-          }
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt) {
-            if (nt < ntu) {
-              const int col = nt * 8 + (lane >> 2);
-              const double b = col < ku ? __ldg(phn + (size_t)brow * ku + col) : 0.0;
-#pragma unroll
-              for (int mt = 0; mt < 3; ++mt)
-                if (mt != (f + 1) % 3) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
-            }
-          }
-        }
-      }
-    }
-#else
-#pragma unroll
-    for (int f = 0; f < 3; ++f) {
-      double pj[3][2];  // STROM_PREF_JIT: this face's neighbor B fragments, in flight during the block sums
-      if (STROM_PREF_JIT && ntu <= 2 && (fin[f] >> 3) == 0) {
-        const int nf = fin[f] & 3;
-        const bool flip = (fin[f] >> 2) & 1;
-        const double* phn = r.phi + (size_t)nbr[f] * NU * ku;
-#pragma unroll
-        for (int ks = 0; ks < 3; ++ks) {
-          const int jn = flip ? (ks == 0 ? 1 : (ks == 1 ? 0 : 2)) : ks;
-          const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            const int col = nt * 8 + (lane >> 2);
-            pj[ks][nt] = (nt < ntu && col < ku) ? __ldg(phn + (size_t)(node * M + (lane & 3)) * ku + col) : 0.0;
-          }
-        }
-      }
       {
         const int c = (lane & 15) >> 2, cp = lane & 3, side = lane >> 4;
         double cs[NS];
@@ -1038,8 +797,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
           for (int nt = 0; nt < 4; ++nt) {
             if (nt < ntu) {
               const int col = nt * 8 + (lane >> 2);
-              const double b = (STROM_PREF_JIT && ntu <= 2) ? pj[ks][nt < 2 ? nt : 0]
-                               : (pref ? pfn[f][ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phn + (size_t)brow * ku + col) : 0.0));
+              const double b = col < ku ? __ldg(phn + (size_t)brow * ku + col) : 0.0;
 #pragma unroll
               for (int mt = 0; mt < 3; ++mt)
                 if (mt != (f + 1) % 3) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
@@ -1049,7 +807,6 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       }
       __syncwarp();  // Lout_f consumed before the next face overwrites it
     }
-#endif
     // ---- J: own-state projection J_U += L Phi_e on DMMA ----------------------------------
     {
       const double* phe = r.phi + (size_t)e * NU * ku;
@@ -1063,8 +820,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         for (int nt = 0; nt < 4; ++nt) {
           if (nt < ntu) {
             const int col = nt * 8 + (lane >> 2);
-            const double b = PHB ? PHI[brow * SH::PHS + (((col >> 1) ^ (2 * (brow & 3))) << 1) + (col & 1)]
-                                 : (prefe ? pfe[ks][nt < 2 ? nt : 0] : (col < ku ? __ldg(phe + (size_t)brow * ku + col) : 0.0));
+            const double b = col < ku ? __ldg(phe + (size_t)brow * ku + col) : 0.0;
 #pragma unroll
             for (int mt = 0; mt < 3; ++mt) dmma(ju[nt][mt][0], ju[nt][mt][1], af[mt], b);
           }
@@ -1072,26 +828,22 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       }
     }
     __syncwarp();  // LOUT reads done before DRX overwrites it
-    if (!STROM_XEARLY) x_stage(RA + DRXo);
+    x_stage(RA + DRXo);
     __syncwarp();
     // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
     double* Jt = RA;
-    constexpr bool GFRAG = CT && STROM_GFRAG;  // gradient from the fragments
+    constexpr bool GFRAG = CT;  // gradient from the J accumulator fragments
     const bool gfrag = GFRAG && DERIVS;
     double rr[3];  // rho * R at the lane's three projection rows
 #pragma unroll
     for (int mt = 0; mt < 3; ++mt) rr[mt] = gfrag ? rho * S[SH::RT + prow(mt, lane)] : 0.0;
-    // fragment stores: the lane's two columns in an order flipped by jflip so the 16 lanes
-    // of a half-warp (rows c = 0..3 x column pairs k = 0..3, LDJ == 12 mod 16) never collide
-    const int jc = (lane >> 2) & 3, jk = lane & 3;
-    const int jflip = STROM_J_FLIP ? (jc == 3 ? 1 : ((jc == 1 || jc == 2) ? (jk >> 1) : 0)) : 0;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int mt = 0; mt < 3; ++mt)
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-          const int h2 = t ^ jflip;
+          const int h2 = t;
           const int col = nt * 8 + 2 * (lane & 3) + h2;
           const double v = h2 ? ju[nt][mt][1] : ju[nt][mt][0];
           if (nt < ntu && col < ku) Jt[prow(mt, lane) * LDJ + col] = v;
@@ -1109,7 +861,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         const int d = 4 * ks + (lane & 3);
         double af[3];
 #pragma unroll
-        for (int mt = 0; mt < 3; ++mt) af[mt] = d < 6 ? (STROM_XEARLY ? DRXE : RA + DRXo)[prow(mt, lane) * LDX + d] : 0.0;
+        for (int mt = 0; mt < 3; ++mt) af[mt] = d < 6 ? (RA + DRXo)[prow(mt, lane) * LDX + d] : 0.0;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           if (nt < ntx) {
@@ -1126,7 +878,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         for (int mt = 0; mt < 3; ++mt)
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
-            const int h2 = t ^ jflip;
+            const int h2 = t;
             const int col = nt * 8 + 2 * (lane & 3) + h2;
             const double v = h2 ? jx[nt][mt][1] : jx[nt][mt][0];
             if (col < kx) Jt[prow(mt, lane) * LDJ + ku + col] = v;
@@ -1149,25 +901,8 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       // (prefetching the neighbor rows, U0, Psi and coordinates too measured 4-9% slower)
       if (nidx < nunits) {
         if (lane < 10) EI[lane] = wv;
-        if (PHB) {
-          phi_async(nact);
-        } else {
-          const char* base = reinterpret_cast<const char*>(r.phi + (size_t)nact * NU * ku);
-          for (int off = lane * 128; off < NU * ku * 8; off += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
-          if (STROM_PREF_NBR) {  // the next unit's neighbor face-node rows (one 8*k_u-byte row per lane)
-            __syncwarp();
-            for (int i = lane; i < NF * NF * M; i += 32) {
-              const int f = i / (NF * M), jj = (i / M) % NF, c = i % M;
-              const int fi = EI[7 + f];
-              if ((fi >> 3) == 0) {
-                const int nf = fi & 3;
-                const int node = jj == 0 ? nf : (jj == 1 ? (nf == 2 ? 0 : nf + 1) : 3 + nf);
-                const double* row = r.phi + ((size_t)EI[4 + f] * NU + node * M + c) * ku;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
-              }
-            }
-          }
-        }
+        const char* base = reinterpret_cast<const char*>(r.phi + (size_t)nact * NU * ku);
+        for (int off = lane * 128; off < NU * ku * 8; off += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
       }
     }
     // ---- G: Gram and gradient, or per-element contributions --------------------------------
@@ -1289,7 +1024,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   if (!DERIVS) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) jacc += __shfl_xor_sync(0xffffffffu, jacc, o);
-  if constexpr (CT && STROM_GFRAG) {
+  if constexpr (CT) {
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1)
 #pragma unroll

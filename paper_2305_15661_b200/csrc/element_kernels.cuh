@@ -412,66 +412,6 @@ __global__ void __launch_bounds__(128) value_kernel(const __grid_constant__ Para
   }
 }
 
-// one warp per element, lane = parameter point (32 mu per warp): every basis row is a
-// broadcast load shared by the 32 mu; grid (element chunks, ceil(P / 32)); per-mu
-// partials per block (fixed-order sums)
-template <class LAW, int NB, int NQ, int NS>
-__global__ void __launch_bounds__(128) value_mu_kernel(const __grid_constant__ Params<NB, NQ, NS, Shape<LAW, NB, NQ, NS>::NF> prm) {
-  using SH = Shape<LAW, NB, NQ, NS>;
-  constexpr int NU = SH::NU;
-  const auto& T = prm.t;
-  const Run& r = prm.r;
-  __shared__ double Ws[KMAX][32], Ts[KXMAX][32], red[4][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // lane -> parameter row: consecutive rows, or the compacted list of enabled rows
-  auto row_of = [&](int l) -> int {
-    const int s = blockIdx.y * 32 + l;
-    return r.list ? (s < r.nlist ? r.list[s] : r.P) : s;
-  };
-  const int p0 = row_of(0);
-  const int pr = row_of(lane);
-  const bool pv = pr < r.P && (!r.mask || r.mask[pr]);
-  const int p = pv ? pr : p0;  // idle lanes shadow a valid point (no traps, results unused)
-  for (int t = threadIdx.x; t < KMAX * 32; t += blockDim.x) {
-    const int k = t / 32, l = t % 32, pp = row_of(l);
-    Ws[k][l] = (k < r.ku && pp < r.P) ? r.w[(size_t)pp * r.ku + k] : 0.0;
-  }
-  for (int t = threadIdx.x; t < KXMAX * 32; t += blockDim.x) {
-    const int a = t / 32, l = t % 32, pp = row_of(l);
-    Ts[a][l] = (a < r.kx && pp < r.P) ? r.tau[(size_t)pp * r.kx + a] : 0.0;
-  }
-  __syncthreads();
-  LawArgs la;
-  for (int i = 0; i < 8; ++i) la.p[i] = r.lawp[i];
-  for (int i = 0; i < NMU; ++i) la.mu[i] = (i < r.nmu && p < r.P) ? r.mu[p * r.nmu + i] : (i < r.nmu ? r.mu[i] : 0.0);
-  const int pp = p < r.P ? p : 0;
-  const int nunits = r.active ? r.A : r.ne;
-  double acc = 0.0;
-  for (int idx = blockIdx.x * 4 + warp; idx < nunits; idx += gridDim.x * 4) {
-    const int e = r.active ? r.active[idx] : idx;
-    const double rho = r.active ? r.rho[idx] : 1.0;
-    double R[NU], N;
-    bool deg;
-    value_unit<LAW, NB, NQ, NS>(T, r, la, e, pp, [&](int k) { return Ws[k][lane]; }, [&](int a) { return Ts[a][lane]; }, R, N, deg);
-    if (!pv) continue;
-    if (deg) flag_degenerate(r, p, e);
-    if (r.mode == MODE_RESIDUAL) {
-      double* o_ = r.out + ((size_t)p * r.ne + e) * NU;
-#pragma unroll
-      for (int i = 0; i < NU; ++i) o_[i] = R[i];
-    } else {
-      double r2 = 0.0;
-#pragma unroll
-      for (int i = 0; i < NU; ++i) r2 = fma(R[i], R[i], r2);
-      acc += r.mode == MODE_OBJECTIVE ? 0.5 * rho * (r2 + N * N) : r2;
-    }
-  }
-  if (r.mode == MODE_RESIDUAL) return;
-  red[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0 && pv) r.part[(size_t)p * gridDim.x + blockIdx.x] = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
-}
-
 // one warp per parameter row: lane-strided partials, fixed-order shuffle tree (deterministic)
 struct DynRows {  // device-sized launch of the pass being finalized (Run::dyn_*), count == null: static grid
   const int* count;
@@ -521,9 +461,18 @@ static __global__ void __launch_bounds__(1024) finalize_derivs_kernel(const doub
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int src = blockIdx.x * 32 + lane;
   double s = 0.0;
-  if (src < PSZ) {
+  if (src < PSZ) {  // four independent sums in flight per warp (fixed order: deterministic per launch shape)
     const double* q = part + (size_t)prow * gx * PSZ + src;
-    for (int b = w; b < gx; b += nw) s += q[(size_t)b * PSZ];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int b = w;
+    for (; b + 3 * nw < gx; b += 4 * nw) {
+      s0 += q[(size_t)b * PSZ];
+      s1 += q[(size_t)(b + nw) * PSZ];
+      s2 += q[(size_t)(b + 2 * nw) * PSZ];
+      s3 += q[(size_t)(b + 3 * nw) * PSZ];
+    }
+    for (; b < gx; b += nw) s0 += q[(size_t)b * PSZ];
+    s = (s0 + s1) + (s2 + s3);
   }
   red[w][lane] = s;
   __syncthreads();

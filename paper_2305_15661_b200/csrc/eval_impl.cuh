@@ -110,7 +110,7 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
   r.LDJ = r.KP + 4;  // == 4 mod 8 doubles: conflict-free half-warp fragment loads
   r.U = 1;
   r.unit_stride = 0;
-  r.gx_warp_stride = SH::warp_stride(r.LDJ, r.KP, r.kx, SH::hreg(KUT, KXT), SH::phibuf(KUT));
+  r.gx_warp_stride = SH::warp_stride(r.LDJ, r.KP, r.kx, SH::hreg(KUT, KXT));
   const int smem_cap = 227 * 1024;
   const size_t warp_bytes = (size_t)r.gx_warp_stride * sizeof(double);
   const int nwarps = std::min<int>(2, (int)(smem_cap / warp_bytes));  // 2-warp CTAs (measured fastest)

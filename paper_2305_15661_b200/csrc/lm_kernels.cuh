@@ -18,8 +18,14 @@
 
 namespace strom {
 
-constexpr int LM_B = 4;        // speculative objective trials per round
-constexpr int LM_THREADS = 64;
+#ifndef STROM_LM_B
+#define STROM_LM_B 4
+#endif
+#ifndef STROM_LM_THREADS
+#define STROM_LM_THREADS 64
+#endif
+constexpr int LM_B = STROM_LM_B;              // speculative objective trials per round
+constexpr int LM_THREADS = STROM_LM_THREADS;  // threads of the per-mu control block
 
 enum LmPhase {
   PH_START = 0, PH_SI_DERIV, PH_SI_BASEJ, PH_SI_LS, PH_MAIN_DERIV, PH_MAIN_ITER_READY, PH_MAIN_LS,
