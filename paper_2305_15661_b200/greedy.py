@@ -195,11 +195,19 @@ def greedy_train(law, geom, cand_mus, hdm_snapshot, n_iter, dist_config, train_w
         x_al = align(state.bases, cand_mus[i]) if align is not None else X
         U, x = hdm_snapshot(cand_mus[i], x_al)
         state.bases.phi = gram_schmidt_append(state.bases.phi, U)
-        state.bases.psi = gram_schmidt_append(state.bases.psi, np.asarray(x, dtype=float) - X)
+        try:  # an unaligned snapshot (x* = X, SPEC's alignment fallback) adds no mesh motion
+            state.bases.psi = gram_schmidt_append(state.bases.psi, np.asarray(x, dtype=float) - X)
+            psi_grown = True
+        except BasisInSpanError:
+            import warnings
+
+            warnings.warn(f"mesh snapshot at mu={cand_mus[i].tolist()} adds no new motion; Psi not grown")
+            psi_grown = False
         state.selected.append(int(i))
         state.snapshots.append((np.asarray(U), np.asarray(x)))
         t0 = time.perf_counter()
         state.weights = train_weights(state.bases, state.weights, cand_mus[state.selected])
         state.metrics.append({"j": state.j, "mu": cand_mus[i].tolist(), "indicator": v, "T_gs": t_gs,
-                              "T_rho": time.perf_counter() - t0, "active": int(len(state.weights.active))})
+                              "T_rho": time.perf_counter() - t0, "active": int(len(state.weights.active)),
+                              "psi_grown": psi_grown})
     return state

@@ -27,8 +27,11 @@ def test_greedy_train_bookkeeping():
     cands = np.array([[a, b] for a in (3.0, 6.0, 9.0) for b in (0.02, 0.0475, 0.075)])
     xy = np.repeat(mesh.nodes[mesh.elements[:, :3]].mean(axis=1), 6, axis=0)  # element centroids per DG node
 
-    def hdm_snapshot(mu, x):  # synthetic "HDM" state: a mu-dependent smooth field
-        return 1.0 + 0.1 * np.sin(mu[0] * xy[:, 0] + 40.0 * mu[1] * xy[:, 1]), x
+    nodes = mesh.nodes
+
+    def hdm_snapshot(mu, x):  # synthetic "HDM" state and an aligned mesh: mu-dependent smooth fields
+        d = 1e-3 * np.stack([np.sin(mu[0] * nodes[:, 1]), np.cos(40.0 * mu[1] * nodes[:, 0])], 1)
+        return 1.0 + 0.1 * np.sin(mu[0] * xy[:, 0] + 40.0 * mu[1] * xy[:, 1]), x + d.ravel()
 
     train = lambda bases, guess, mus: WeightVector.ones(ne)  # noqa: E731  (LP-independent bookkeeping)
     try:  # the reference's EQP LP with the GPU operator swapped in
@@ -58,5 +61,6 @@ def test_greedy_train_bookkeeping():
     assert np.allclose(st.bases.phi.T @ st.bases.phi, np.eye(3), atol=1e-12)
     assert np.allclose(st.bases.psi.T @ st.bases.psi, np.eye(3), atol=1e-12)
     assert [m["j"] for m in st.metrics] == [1, 2, 3] and np.all(np.asarray(st.weights.rho) >= 0.0)
+    assert all(m["psi_grown"] for m in st.metrics[1:])
     with pytest.raises(CandidateSetExhausted):
         greedy_train(law, geom, cands[:2], hdm_snapshot, 3, dist, train, LmConfig(max_iters=3))
