@@ -67,7 +67,23 @@ def bytes_per_pass(ne, nv, nu, ku, kx):
     return 8 * (Nu * ku + Nu + Nx * kx + 2 * Nx + ne) + ne * 3 * (4 + 4 + 1)
 
 
-def fp64_peak():
+def fp64_peak(gpu=0):
+    """FP64 roofline denominator: the DFMA / DMMA issue-bound loops of tools/fp64_peak.cu run
+    on this GPU in this run (clocks sampled while they run), else the round-1 measurement."""
+    tool = os.path.join(ROOT, "tools", "fp64_peak")
+    if os.path.exists(tool):
+        clk = Clocks(gpu)
+        try:
+            out = subprocess.run([tool], capture_output=True, text=True, timeout=120).stdout
+            d = json.loads(out.strip().splitlines()[-1])
+        except (OSError, ValueError, IndexError, subprocess.SubprocessError):
+            d = None
+        c = clk.stop()
+        if d and d.get("err") == "no error":
+            dfma = max(v for k, v in d.items() if k.startswith("dfma_tflops"))
+            dmma = max(v for k, v in d.items() if k.startswith("dmma_tflops"))
+            return max(dfma, dmma), (f"measured in this run by tools/fp64_peak.cu: DFMA {dfma:.2f}, DMMA {dmma:.2f} "
+                                     f"TFLOP/s at {c.get('sm_mhz')} MHz (reasons {c.get('reasons')})")
     path = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
     with open(path) as fh:
         d = json.load(fh)
@@ -636,7 +652,7 @@ def run_mine(args):
     F = flops_per_element(nq, 6, 4, ns, 3, 6, ku, kx)
     per_launch_flops = F * (hi - lo)
     kern_avg_s = kern_ms / max(1, nl.value) / 1e3
-    peak, peak_src = fp64_peak()
+    peak, peak_src = fp64_peak(local)
     achieved = per_launch_flops / kern_avg_s / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "derivs_traffic_r01.json")
