@@ -617,7 +617,7 @@ def run_mine(args):
             op.derivatives(coords, case.mus[0])
         e2e_s = time.perf_counter() - t0
         e2e_value = ne * args.steps / e2e_s
-        e2e_io = (8 * (ku + kx + op.n_mu), 8 * (1 + K + K * K) + 4)
+        e2e_io = (8 * (ku + kx + op.n_mu), 8 * (1 + K + K * K) + 8)  # inputs; outputs + degenerate counter slot
     else:
         # each rank: the public derivatives call on its element range (host in, host out), then
         # the 1+K+K^2 sums all-reduced over NCCL and read back; wall time, max over ranks

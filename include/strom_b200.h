@@ -109,6 +109,17 @@ int strom_eval(strom_handle* h, int32_t mode, const double* w, const double* tau
                int32_t P, const int32_t* active, const double* rho, int32_t A, double* out,
                int32_t* degen, void* stream, int32_t sync);
 
+/* The same evaluation through HOST buffers: w (P, ku), tau (P, kx), mu (P, n_mu) and out
+ * (out_n doubles, the mode's size) are host pointers; active / rho stay device pointers.
+ * Inputs go through a pinned staging buffer owned by the handle with one H2D copy, the
+ * result and the per-row degenerate counters (degen_out, host, or NULL) come back with one
+ * D2H copy and one stream synchronisation; returns 1 (ids available through
+ * strom_degenerate_elements) when an element is degenerate.  This is the single-point
+ * public API's path (ReducedOperator.objective / derivatives, reduced.py:172-229). */
+int strom_eval_host(strom_handle* h, int32_t mode, const double* w, const double* tau, const double* mu,
+                    int32_t P, const int32_t* active, const double* rho, int32_t A, double* out, int64_t out_n,
+                    int32_t* degen_out, void* stream);
+
 /* Element ids flagged degenerate by the last eval for parameter p (host
  * buffer `ids`, capacity cap); returns the count written, sorted ascending. */
 int strom_degenerate_elements(strom_handle* h, int32_t p, int32_t* ids, int32_t cap);

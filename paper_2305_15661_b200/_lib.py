@@ -28,7 +28,8 @@ class DistDesc(C.Structure):
     _fields_ = [("kappa", C.c_double), ("eps", C.c_double)]
 
 
-EXPORTS = ("strom_create", "strom_set_bases", "strom_set_offsets", "strom_reserve", "strom_eval", "strom_degenerate_elements",
+EXPORTS = ("strom_create", "strom_set_bases", "strom_set_offsets", "strom_reserve", "strom_eval", "strom_eval_host",
+           "strom_degenerate_elements",
            "strom_lm_solve", "strom_lm_stats", "strom_profile", "strom_profile_ms", "strom_last_error", "strom_destroy")
 
 _lib = None
@@ -53,6 +54,7 @@ def load(path=SO_PATH):
     lib.strom_reserve.argtypes = [vp, i32, i32]
     lib.strom_set_offsets.argtypes = [vp, vp, C.c_int64, vp, C.c_int64]
     lib.strom_eval.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp, i32]
+    lib.strom_eval_host.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, i32, vp, C.c_int64, vp, vp]
     lib.strom_degenerate_elements.argtypes = [vp, i32, vp, i32]
     lib.strom_lm_solve.argtypes = [vp, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp, vp]
     lib.strom_lm_stats.argtypes = [vp, vp]

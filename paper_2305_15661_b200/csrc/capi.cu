@@ -216,6 +216,53 @@ extern "C" int strom_eval(strom_handle* h, int32_t mode, const double* w, const 
   return 0;
 }
 
+// One evaluation through HOST buffers (the public single-point API): the inputs are staged in
+// pinned memory, copied with one asynchronous H2D, evaluated, and the result and the per-row
+// degenerate counters come back with one D2H and one stream synchronisation.
+extern "C" int strom_eval_host(strom_handle* h, int32_t mode, const double* w, const double* tau, const double* mu,
+                               int32_t P, const int32_t* active, const double* rho, int32_t A, double* out,
+                               int64_t out_n, int32_t* degen_out, void* stream) {
+  if (!h || !out || out_n < 0 || P < 1) return fail(-1, "strom_eval_host: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nmu = h->law.n_mu;
+  const size_t n_in = (size_t)P * (h->ku + h->kx + nmu);
+  const size_t need = n_in + (size_t)out_n + (size_t)P;  // doubles: inputs, outputs, counters (as doubles)
+  if (need > h->stage_cap) {
+    if (h->stage_h) cudaFreeHost(h->stage_h);
+    if (h->stage_d) cudaFree(h->stage_d);
+    h->stage_h = nullptr;
+    h->stage_d = nullptr;
+    h->stage_cap = 0;
+    CK(cudaMallocHost(&h->stage_h, need * sizeof(double)));
+    CK(cudaMalloc(&h->stage_d, need * sizeof(double)));
+    h->stage_cap = need;
+  }
+  double* hin = h->stage_h;
+  double* din = h->stage_d;
+  const size_t nw = (size_t)P * h->ku, nt = (size_t)P * h->kx, nm = (size_t)P * nmu;
+  if (nw) memcpy(hin, w, nw * sizeof(double));
+  if (nt) memcpy(hin + nw, tau, nt * sizeof(double));
+  if (nm) memcpy(hin + nw + nt, mu, nm * sizeof(double));
+  CK(cudaMemcpyAsync(din, hin, n_in * sizeof(double), cudaMemcpyHostToDevice, st));
+  double* dout = din + n_in;
+  int32_t* ddeg = reinterpret_cast<int32_t*>(dout + out_n);
+  int rc = strom_eval(h, mode, nw ? din : nullptr, nt ? din + nw : nullptr, nm ? din + nw + nt : nullptr, P, active,
+                      rho, A, dout, ddeg, st, 0);
+  if (rc < 0) return rc;
+  double* hout = hin + n_in;
+  CK(cudaMemcpyAsync(hout, dout, ((size_t)out_n + P) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  memcpy(out, hout, (size_t)out_n * sizeof(double));
+  const int32_t* hdeg = reinterpret_cast<const int32_t*>(hout + out_n);
+  bool any = false;
+  for (int p = 0; p < P; ++p) any |= hdeg[p] > 0;
+  if (degen_out) memcpy(degen_out, hdeg, P * sizeof(int32_t));
+  if (!any) return 0;
+  // degenerate elements: re-run synchronously for their ids (rare path)
+  return strom_eval(h, mode, nw ? din : nullptr, nt ? din + nw : nullptr, nm ? din + nw + nt : nullptr, P, active, rho,
+                    A, dout, nullptr, st, 1);
+}
+
 extern "C" int strom_degenerate_elements(strom_handle* h, int32_t p, int32_t* ids, int32_t cap) {
   if (!h || p < 0 || p >= (int)h->last_degen.size()) return 0;
   const auto& v = h->last_degen[p];
@@ -236,6 +283,8 @@ extern "C" void strom_destroy(strom_handle* h) {
   if (h->degen_scratch) cudaFree(h->degen_scratch);
   lm_graph_free(h);
   lm_free(h->lm);
+  if (h->stage_h) cudaFreeHost(h->stage_h);
+  if (h->stage_d) cudaFree(h->stage_d);
   if (h->lm_stream) cudaStreamDestroy(h->lm_stream);
   for (auto& e : h->ev) cudaEventDestroy(e);
   delete h;

@@ -78,6 +78,9 @@ struct strom_handle {
   std::vector<std::vector<int>> last_degen;
   int num_sms = 148;
   bool has_wall = false;  // slip-wall faces (BC_REFLECT) in the mesh
+  double* stage_h = nullptr;  // pinned staging of strom_eval_host
+  double* stage_d = nullptr;  // its device twin
+  size_t stage_cap = 0;       // doubles
   strom::LmWork lm;
   cudaStream_t lm_stream = nullptr;  // private capture stream of the LM graph
   cudaGraph_t lm_graph = nullptr;    // the last built LM graph, reused while its key matches

@@ -129,6 +129,8 @@ def lm_solve_batched(op, mus, W0=None, Tau0=None, rho=None, config=None, w0_mode
     """Solve P reduced problems (one per row of ``mus``) on the GPU at once."""
     if not isinstance(op, GpuReducedOperator):
         raise TypeError("lm_solve_batched needs a GpuReducedOperator")
+    if getattr(op, "_pad", 0):
+        raise NotImplementedError("the batched GPU LM needs k_u >= 1 (the reference's tau-only LM is not ported)")
     if w0_mode not in ("lsq", "keep"):
         raise ValueError(f"unknown w0_mode {w0_mode!r}")
     cfg = as_config(config)

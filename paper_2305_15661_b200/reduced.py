@@ -156,9 +156,13 @@ class GpuReducedOperator:
             _lib.check(lib.strom_create(_lib.C.byref(md), _lib.C.byref(ld), _lib.C.byref(qd), _lib.C.byref(dd),
                                         self.device.index, _lib.C.byref(h)), "strom_create")
             self._h = h
-            self.k_u, self.k_x = bases.k_u, bases.k_x
+            # k_u = 0 (no state basis, reduced.py:197-199): the device runs one zero column,
+            # which contributes exact zeros, and the public methods strip it
+            self._pad = 1 if bases.k_u == 0 else 0
+            self.k_u, self.k_x = bases.k_u + self._pad, bases.k_x
             nu_g = self.dm.ne * self.dm.nu
-            self.phi = _as_f64(np.asarray(bases.phi).reshape(nu_g, self.k_u), self.device)
+            self.phi = _as_f64(np.zeros((nu_g, 1)) if self._pad else np.asarray(bases.phi).reshape(nu_g, self.k_u),
+                               self.device)
             self.psi = _as_f64(np.asarray(bases.psi).reshape(2 * self.dm.nv, self.k_x), self.device)
             self.ref_coords = _as_f64(bases.ref_coords, self.device)
             self.u0 = None if state_offset is None else _as_f64(state_offset, self.device)
@@ -224,45 +228,38 @@ class GpuReducedOperator:
         self.stats["elements_evaluated"] += A * P
         return out, rc
 
-    def _staging(self, key, n, dtype=torch.float64, pinned=True):
-        """Reused host (pinned) / device buffers of the one-point public calls."""
-        cache = self.__dict__.setdefault("_stage", {})
-        t = cache.get((key, pinned))
-        if t is None or t.numel() < n:
-            t = (torch.empty(max(n, 1), dtype=dtype, pin_memory=True) if pinned
-                 else torch.empty(max(n, 1), dtype=dtype, device=self.device))
-            cache[(key, pinned)] = t
-        return t[:n]
-
     def _single(self, mode, coords, mu, rho):
-        """One parameter point through the public API: inputs staged in pinned memory, one
-        asynchronous H2D copy, the evaluation, results and the degenerate flag read back
-        with one stream synchronisation (the element ids only on the rare degenerate path)."""
+        """One parameter point through the public API: one C call (strom_eval_host) stages the
+        host inputs in pinned memory, copies them with one H2D, evaluates, and returns the result
+        and the degenerate flag with one D2H and one stream synchronisation (the element ids
+        only on the rare degenerate path)."""
         ku, kx = self.k_u, self.k_x
-        n_in = ku + kx + self.n_mu
-        hin = self._staging("in", n_in)
-        a = hin.numpy()
-        a[:ku] = np.asarray(coords.w, dtype=float).reshape(-1)
-        a[ku:ku + kx] = np.asarray(coords.tau, dtype=float).reshape(-1)
-        a[ku + kx:] = self._mu(mu)
-        d = self._staging("in", n_in, pinned=False)
-        d.copy_(hin, non_blocking=True)
-        W, Tau, Mu = d[:ku].view(1, ku), d[ku:ku + kx].view(1, kx), d[ku + kx:].view(1, self.n_mu)
-        degen = self._staging("deg", 1, torch.int32, pinned=False)
-        out, _ = self.eval_batched(mode, W, Tau, Mu, rho, degen=degen)
-        hout = self._staging("out", out.numel())
-        hout.copy_(out, non_blocking=True)
-        hdeg = self._staging("deg", 1, torch.int32)
-        hdeg.copy_(degen, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
-        if int(hdeg[0]) > 0:  # degenerate elements: re-run synchronously for their ids
-            _, rc = self.eval_batched(mode, W, Tau, Mu, rho, sync=True)
-            if rc == 1:
-                n = self._lib.strom_degenerate_elements(self._h, 0, None, 0)
-                ids = np.zeros(max(n, 1), dtype=np.int32)
-                self._lib.strom_degenerate_elements(self._h, 0, ids.ctypes.data, n)
-                raise degenerate_error(ids[:n].astype(np.int64))
-        return hout.numpy().copy()
+        w = np.zeros(ku) if self._pad else np.ascontiguousarray(coords.w, dtype=np.float64).reshape(-1)
+        tau = np.ascontiguousarray(coords.tau, dtype=np.float64).reshape(-1)
+        mu_v = np.ascontiguousarray(self._mu(mu), dtype=np.float64)
+        if w.size != ku or tau.size != kx:
+            raise ValueError(f"coordinates have sizes ({w.size}, {tau.size}), expected ({ku - self._pad}, {kx})")
+        act, rw, A = self._weights(rho)
+        K, ne = ku + kx, self.dm.ne
+        n_out = {
+            _lib.OBJECTIVE: 1, _lib.RESNORM2: 1, _lib.DERIVS: 1 + K + K * K, _lib.CONTRIB: ne * K,
+            _lib.CONTRIB_SPLIT: ne * 2 * K, _lib.RESIDUAL: ne * self.dm.nu, _lib.CONTRIB_LPROWS: (K + 1) * ne,
+        }[mode]
+        out = np.empty(n_out)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        rc = self._lib.strom_eval_host(self._h, mode, w.ctypes.data if ku else None, tau.ctypes.data if kx else None,
+                                       mu_v.ctypes.data, 1, act.data_ptr() if act is not None else None,
+                                       rw.data_ptr() if rw is not None else None, A, out.ctypes.data, n_out, None,
+                                       stream)
+        _lib.check(rc, "strom_eval_host")
+        self.stats["kernel_calls"] += 1
+        self.stats["elements_evaluated"] += A
+        if rc == 1:
+            n = self._lib.strom_degenerate_elements(self._h, 0, None, 0)
+            ids = np.zeros(max(n, 1), dtype=np.int32)
+            self._lib.strom_degenerate_elements(self._h, 0, ids.ctypes.data, n)
+            raise degenerate_error(ids[:n].astype(np.int64))
+        return out
 
     # -- reference API -------------------------------------------------------------
     def objective(self, coords, mu, rho=None):
@@ -272,20 +269,20 @@ class GpuReducedOperator:
         return float(self._single(_lib.OBJECTIVE, coords, mu, rho)[0])
 
     def _derivs(self, coords, mu, rho):
-        ku, kx = self.k_u, self.k_x
+        ku, kx, a = self.k_u, self.k_x, self._pad  # device columns [a, ku) are the API's state columns
         if rho is not None and self._weights(rho)[2] == 0:
             self.stats["kernel_calls"] += 1
-            return 0.0, np.zeros(ku), np.zeros(kx), np.zeros((ku, ku)), np.zeros((ku, kx)), np.zeros((kx, kx))
-        if ku == 0:
-            raise NotImplementedError("derivatives with k_u = 0 are not supported on the GPU path")
+            n = ku - a
+            return 0.0, np.zeros(n), np.zeros(kx), np.zeros((n, n)), np.zeros((n, kx)), np.zeros((kx, kx))
         o = self._single(_lib.DERIVS, coords, mu, rho)
         K = ku + kx
         H = o[1 + K:].reshape(K, K)
-        return float(o[0]), o[1:1 + ku].copy(), o[1 + ku:1 + K].copy(), H[:ku, :ku].copy(), H[:ku, ku:].copy(), H[ku:, ku:].copy()
+        return (float(o[0]), o[1 + a:1 + ku].copy(), o[1 + ku:1 + K].copy(), H[a:ku, a:ku].copy(), H[a:ku, ku:].copy(),
+                H[ku:, ku:].copy())
 
     def residuals(self, coords, mu, rho=None):
         """First-order optimality residuals (S, T) (reduced.py:195-207)."""
-        ku, kx = self.k_u, self.k_x
+        ku, kx = self.k_u - self._pad, self.k_x
         if self.geom.mesh.num_elements == 0 or (ku == 0 and kx == 0):
             return np.zeros(ku), np.zeros(kx)
         _, S, T, _, _, _ = self._derivs(coords, mu, rho)
@@ -297,12 +294,12 @@ class GpuReducedOperator:
 
     def elemental_contributions(self, coords, mu, split=False):
         """Per-element contributions over all elements (reduced.py:231-251)."""
-        ku, kx, ne = self.k_u, self.k_x, self.dm.ne
+        ku, kx, ne, a = self.k_u, self.k_x, self.dm.ne, self._pad
         if not split:
             o = self._single(_lib.CONTRIB, coords, mu, None).reshape(ne, ku + kx)
-            return o[:, :ku].copy(), o[:, ku:].copy()
+            return o[:, a:ku].copy(), o[:, ku:].copy()
         o = self._single(_lib.CONTRIB_SPLIT, coords, mu, None).reshape(ne, 2 * (ku + kx))
-        return (o[:, :ku].copy(), o[:, ku:2 * ku].copy(), o[:, 2 * ku:2 * ku + kx].copy(), o[:, 2 * ku + kx:].copy())
+        return (o[:, a:ku].copy(), o[:, ku + a:2 * ku].copy(), o[:, 2 * ku:2 * ku + kx].copy(), o[:, 2 * ku + kx:].copy())
 
     # -- extensions ----------------------------------------------------------------
     def global_residual(self, coords, mu):
@@ -338,7 +335,16 @@ class GpuReducedOperator:
         K = self.k_u + self.k_x
         ne = self.dm.ne
         shape = {"lprows": (S, K + 1, ne), "split": (S, ne, 2 * K), "total": (S, ne, K)}[layout]
-        return res.view(shape)
+        res = res.view(shape)
+        if self._pad:  # strip the zero state column of a k_u = 0 operator
+            ku = self.k_u
+            if layout == "lprows":
+                res = res[:, 1:]
+            elif layout == "total":
+                res = res[:, :, 1:]
+            else:
+                res = torch.cat([res[:, :, 1:ku], res[:, :, ku + 1:]], dim=2)
+        return res
 
     def residual_norm(self, coords, mu):
         """||R||_2 of the full-mesh residual (greedy error indicator)."""

@@ -90,3 +90,31 @@ def test_gpu_empty_active_set():
     assert op.objective(c, case.mus[0], rho) == 0.0
     J, S, T, Hww, Hwt, Htt = op.derivatives(c, case.mus[0], rho)
     assert J == 0.0 and not np.any(S) and not np.any(Htt)
+
+
+def test_gpu_ku_zero_matches_oracle():
+    """k_u = 0 (no state basis; reduced.py:197-199): derivatives, residuals and contributions
+    carry the tau part only — checked against the oracle on an explicit-state case."""
+    import oracle.dual  # noqa: F401
+    from oracle.element import OracleGeometry, OracleReducedOperator
+    from paper_2305_15661_b200 import configs
+    from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases, ReducedCoords
+
+    case = configs.euler_square_case(n=4, ku=16, kx=8, seed=12)
+    phi0 = np.zeros((case.phi.shape[0], 0))
+    op = GpuReducedOperator(case.law, case.geom, ReducedBases(phi0, case.psi, case.ref_coords), case.dist,
+                            state_offset=case.state_offset)
+    ref = OracleReducedOperator(case.law, OracleGeometry(case.mesh, case.maps, case.quad_order), phi0, case.psi,
+                                case.ref_coords, case.kappa, case.eps, state_offset=case.state_offset)
+    tau = 1e-3 * np.random.default_rng(3).standard_normal(8)
+    c, mu = ReducedCoords(np.zeros(0), tau), case.mus[0]
+    got, want = op.derivatives(c, mu), ref.derivatives(np.zeros(0), tau, mu, None)
+    assert got[1].shape == (0,) and got[3].shape == (0, 0) and got[4].shape == (0, 8)
+    for k in (0, 2, 5):
+        assert rel_err(got[k], want[k]) < TOL
+    S, T = op.residuals(c, mu)
+    assert S.shape == (0,) and rel_err(T, want[2]) < TOL
+    Se, Te = op.elemental_contributions(c, mu)
+    Se_r, Te_r = ref.elemental_contributions(np.zeros(0), tau, mu)
+    assert Se.shape == (case.mesh.num_elements, 0) and rel_err(Te, Te_r) < TOL
+    assert rel_err(op.objective(c, mu), ref.objective(np.zeros(0), tau, mu)) < TOL
