@@ -655,7 +655,7 @@ def run_mine(args):
     peak, peak_src = fp64_peak(local)
     achieved = per_launch_flops / kern_avg_s / 1e12
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "derivs_traffic_r01.json")
+    tp = os.path.join(ROOT, "profiles", "derivs_traffic_r02.json")
     if os.path.exists(tp) and n == 256:  # the ncu capture is of the full config-2 pass
         with open(tp) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch") * (hi - lo) / ne

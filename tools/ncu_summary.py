@@ -17,12 +17,20 @@ WANT = [
     "sass__inst_executed_local_loads", "sass__inst_executed_local_stores", "lts__t_bytes.sum",
     "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_tensor_op_dmma.sum",
     "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__ops_path_tensor_src_fp64.avg.pct_of_peak_sustained_elapsed", "sass__inst_executed_register_spilling",
+    "l1tex__t_sectors_pipe_lsu_mem_local_op_ld_lookup_hit.sum", "l1tex__t_sectors_pipe_lsu_mem_local_op_ld_lookup_miss.sum",
 ]
 STALLS = "smsp__average_warp_latency_issue_stalled_"
 
 
 def summary(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """rep: an .ncu-rep file, or the csv of `ncu -i rep --page raw --csv`."""
+    if rep.endswith(".csv"):
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, out = rows[0], rows[1], []
     for vals in rows[2:]:
