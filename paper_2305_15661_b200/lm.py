@@ -167,3 +167,10 @@ def lm_solve(problem, config=None, w0_mode="lsq"):
     res = lm_solve_batched(op, [problem.mu], w0[None], tau0[None], problem.rho, config, w0_mode,
                            raise_degenerate=True)
     return res[0]
+
+
+def history_csv(history, path):
+    """Mirror of strom.lm.history_csv (lm.py:67-70): rows (iter, J, |S|, |T|, lambda, alpha)."""
+    from .io import history_csv as _h
+
+    _h(history, path)
