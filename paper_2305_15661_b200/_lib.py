@@ -6,7 +6,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("STROM_SO") or os.path.join(HERE, "_strom_b200.so")
 
-OBJECTIVE, DERIVS, CONTRIB, CONTRIB_SPLIT, RESIDUAL, RESNORM2, CONTRIB_LPROWS = range(7)
+OBJECTIVE, DERIVS, CONTRIB, CONTRIB_SPLIT, RESIDUAL, RESNORM2, CONTRIB_LPROWS, ELEMJAC = range(8)
 
 
 class MeshDesc(C.Structure):

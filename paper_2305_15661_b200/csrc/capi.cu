@@ -194,13 +194,15 @@ extern "C" int strom_eval(strom_handle* h, int32_t mode, const double* w, const 
                           int32_t P, const int32_t* active, const double* rho, int32_t A, double* out,
                           int32_t* degen, void* stream, int32_t sync) {
   if (!h) return fail(-1, "null handle");
-  if (mode < 0 || mode > MODE_CONTRIB_LPROWS) return fail(-1, "bad mode");
+  if (mode < 0 || mode > MODE_ELEMJAC) return fail(-1, "bad mode");
+  if (mode == MODE_ELEMJAC && (h->law.n_comp != 4 || h->p != 2 || P != 1))
+    return fail(-1, "element Jacobians: 4-component laws with p = 2, one parameter point");
   if (P < 1) return fail(-1, "P must be >= 1");
   if (!out) return fail(-1, "null output");
   if (!h->xref) return fail(-1, "bases not set");
   if ((h->ku && !w) || (h->kx && !tau) || (h->law.n_mu && !mu)) return fail(-1, "null coordinates");
   if (active && (!rho || A < 0)) return fail(-1, "active set needs weights");
-  if (active && (mode == MODE_CONTRIB || mode == MODE_CONTRIB_SPLIT || mode == MODE_CONTRIB_LPROWS))
+  if (active && (mode == MODE_CONTRIB || mode == MODE_CONTRIB_SPLIT || mode == MODE_CONTRIB_LPROWS || mode == MODE_ELEMJAC))
     return fail(-1, "element contributions are evaluated over all elements");
   cudaStream_t st = (cudaStream_t)stream;
   if (!degen) {

@@ -141,6 +141,10 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   }
   constexpr bool CT = KUT > 0;
   const bool DERIVS = DM >= 0 ? DM == 1 : r.mode == MODE_DERIVS;  // compile-time on the specialised path
+  // element Jacobian blocks (full-space assembly, dg.py:197-272; generic instantiation only):
+  // out[e] = [res (NU) | dR/dU_e (NU x NU) | dR/dU_nbr (NU x 3 NU) | dR/dx_e (NU x 6)]
+  const bool EJ = DM < 0 && r.mode == MODE_ELEMJAC;
+  constexpr int EJ_SELF = 24, EJ_NBR = EJ_SELF + 24 * 24, EJ_X = EJ_NBR + 24 * 72, EJ_SZ = EJ_X + 24 * 6;
   constexpr int KT = KUT + KXT, KPT = (KT + 7) / 8 * 8;
   const int ku = CT ? KUT : r.ku, kx = CT ? KXT : r.kx, K = CT ? KT : r.K, KP = CT ? KPT : r.KP;
   const int LDJ = CT ? KPT + 4 : r.LDJ;
@@ -752,6 +756,9 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       for (int mt = 0; mt < 3; ++mt) ju[nt][mt][0] = ju[nt][mt][1] = 0.0;
     const double* L = RA + SH::LL;
     double* Lo = RA + SH::LO;
+    double* const ej = EJ ? r.out + (size_t)e * EJ_SZ : nullptr;
+    if (EJ)  // neighbor blocks: zero first (boundary faces and off-face columns stay 0)
+      for (int i = lane; i < 24 * 72; i += 32) ej[EJ_NBR + i] = 0.0;
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
       {
@@ -776,6 +783,16 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
           }
       }
       __syncwarp();
+      if (EJ && (fin[f] >> 3) == 0) {  // Lout_f -> dR_e/dU_nbr(f) at the neighbor's face-node columns
+        const int nf = fin[f] & 3;
+        const bool flip = (fin[f] >> 2) & 1;
+        for (int i = lane; i < 144; i += 32) {
+          const int row = i / 12, kk = i % 12, j = row / M, c = row % M, ks = kk / M, cp = kk % M;
+          const int jn = flip ? (ks == 0 ? 1 : (ks == 1 ? 0 : 2)) : ks;
+          const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
+          ej[EJ_NBR + (fnode_of(PD, f, j) * M + c) * 72 + f * NU + node * M + cp] = Lo[(j * M + c) * LDO + kk];
+        }
+      }
       if ((fin[f] >> 3) == 0) {
         const int nf = fin[f] & 3;
         const bool flip = (fin[f] >> 2) & 1;
@@ -807,6 +824,8 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       }
       __syncwarp();  // Lout_f consumed before the next face overwrites it
     }
+    if (EJ)  // L (volume + face in-blocks) = dR_e/dU_e
+      for (int i = lane; i < NU * NU; i += 32) ej[EJ_SELF + i] = L[(i / NU) * LDL + i % NU];
     // ---- J: own-state projection J_U += L Phi_e on DMMA ----------------------------------
     {
       const double* phe = r.phi + (size_t)e * NU * ku;
@@ -830,6 +849,10 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     __syncwarp();  // LOUT reads done before DRX overwrites it
     x_stage(RA + DRXo);
     __syncwarp();
+    if (EJ) {  // dR_e/dx_e (local coordinates 2 g + i) and the residual
+      for (int i = lane; i < NU * 6; i += 32) ej[EJ_X + i] = RA[DRXo + (i / 6) * LDX + i % 6];
+      if (lane < NU) ej[lane] = S[SH::RT + lane];
+    }
     // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
     double* Jt = RA;
     constexpr bool GFRAG = CT;  // gradient from the J accumulator fragments
@@ -991,7 +1014,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         const double ri = lane < NU ? S[SH::RT + lane] : (lane == NU ? S[SH::MN] : 0.0);
         jacc = fma(rho * ri, ri, jacc);
       }
-    } else {
+    } else if (!EJ) {
       const int extra = r.mode == MODE_CONTRIB_LPROWS ? 1 : 0;
       const int nk = r.mode == MODE_CONTRIB_SPLIT ? 2 * K : K + extra;
       for (int k2 = lane; k2 < nk; k2 += 32) {

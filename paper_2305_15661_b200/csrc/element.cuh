@@ -13,7 +13,7 @@ constexpr int DERIV_THREADS = 128;
 
 enum Mode {
   MODE_OBJECTIVE = 0, MODE_DERIVS = 1, MODE_CONTRIB = 2, MODE_CONTRIB_SPLIT = 3,
-  MODE_RESIDUAL = 4, MODE_RESNORM2 = 5, MODE_CONTRIB_LPROWS = 6
+  MODE_RESIDUAL = 4, MODE_RESNORM2 = 5, MODE_CONTRIB_LPROWS = 6, MODE_ELEMJAC = 7
 };
 
 // reference-element constants; lives in the kernel parameter (constant) bank

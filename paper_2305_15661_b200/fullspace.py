@@ -1,0 +1,77 @@
+"""Full-space assembly on the GPU (first part): ``assemble_global`` with the
+sparse Jacobians dR/dU and dR/dx (strom/dg.py:228-272).
+
+The element blocks — residual, dR_e/dU_e, dR_e/dU_nbr and dR_e/dx_e, i.e. what
+``elemental_residual(..., want_jacobians=True)`` returns (dg.py:197-225) — come from the K1
+element kernel in its STROM_ELEMJAC mode (the same local Jacobians the reduced path projects,
+written out instead of projected); the scatter into CSR uses the reference's own index
+construction.  4-component laws (Euler) with p = 2; other laws raise.  The enriched test
+space (``assemble_enriched``), the HDM Newton solve and full-space tracking are not built.
+"""
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from .reduced import EJ_SIZE, GpuReducedOperator, ReducedBases
+
+
+class _NoDistortion:
+    kappa, eps = 1.0, 1e-8
+
+
+def element_jacobians(law, geom, U, x, mu, device=None):
+    """(res (ne, 24), jac_self (ne, 24, 24), jac_neigh (ne, 24, 72), jac_coord (ne, 24, 6)) at
+    the global state U and coordinates x (dg.py:197-225, batched over all elements)."""
+    import torch
+
+    mesh, maps = geom.mesh, geom.maps
+    if maps.n_comp != 4 or maps.degree_sol != 2:
+        raise NotImplementedError("GPU element Jacobians: 4-component laws with p = 2")
+    U = np.asarray(U, dtype=float).reshape(-1)
+    x = np.asarray(x, dtype=float).reshape(-1)
+    bases = ReducedBases(np.zeros((U.size, 0)), np.zeros((x.size, 0)), x)
+    op = GpuReducedOperator(law, geom, bases, _NoDistortion(), device=device, state_offset=U)
+    W = torch.zeros((1, op.k_u), dtype=torch.float64, device=op.device)
+    Tau = torch.zeros((1, 1), dtype=torch.float64, device=op.device)
+    Mu = torch.as_tensor(op._mu(mu)[None]).to(op.device)
+    out, rc = op.eval_batched(_lib.ELEMJAC, W, Tau, Mu, None, sync=True)
+    if rc == 1:  # g <= 0 somewhere: raised after the whole batch, as dg.py:177-178
+        from .reduced import degenerate_error
+
+        n = op._lib.strom_degenerate_elements(op._h, 0, None, 0)
+        ids = np.zeros(max(n, 1), dtype=np.int32)
+        op._lib.strom_degenerate_elements(op._h, 0, ids.ctypes.data, n)
+        raise degenerate_error(ids[:n].astype(np.int64))
+    o = out.view(mesh.num_elements, EJ_SIZE).cpu().numpy()
+    return (o[:, :24], o[:, 24:600].reshape(-1, 24, 24), o[:, 600:2328].reshape(-1, 24, 72),
+            o[:, 2328:].reshape(-1, 24, 6))
+
+
+def assemble_global(law, mesh, maps, U, x, mu, want_jacobians=True, geom=None, device=None):
+    """Residual and CSR Jacobians dR/dU (N_u x N_u), dR/dx (N_u x N_x): strom/dg.py:228-272."""
+    from .mesh import get_geometry
+
+    geom = geom or get_geometry(mesh, maps)
+    if not want_jacobians:
+        bases = ReducedBases(np.zeros((np.size(U), 0)), np.zeros((np.size(x), 0)), np.asarray(x, float).ravel())
+        op = GpuReducedOperator(law, geom, bases, _NoDistortion(), device=device, state_offset=np.asarray(U, float))
+        from .reduced import ReducedCoords
+
+        return op.global_residual(ReducedCoords(np.zeros(0), np.zeros(0)), mu), None, None
+    res, jac_self, jac_neigh, jac_coord = element_jacobians(law, geom, U, x, mu, device)
+    R = res.reshape(-1)
+    rows = maps.state_map[:, :, None]
+    r1 = np.broadcast_to(rows, jac_self.shape).ravel()
+    c1 = np.broadcast_to(maps.state_map[:, None, :], jac_self.shape).ravel()
+    nmap = maps.neighbor_map
+    valid = nmap >= 0
+    r2 = np.broadcast_to(rows, jac_neigh.shape).ravel()
+    c2 = np.broadcast_to(np.clip(nmap, 0, None)[:, None, :], jac_neigh.shape).ravel()
+    d2 = (jac_neigh * valid[:, None, :]).ravel()
+    dRdU = sp.coo_matrix((np.concatenate([jac_self.ravel(), d2]), (np.concatenate([r1, r2]), np.concatenate([c1, c2]))),
+                         shape=(maps.n_global_state, maps.n_global_state)).tocsr()
+    r3 = np.broadcast_to(rows, jac_coord.shape).ravel()
+    c3 = np.broadcast_to(maps.coord_map[:, None, :], jac_coord.shape).ravel()
+    dRdx = sp.coo_matrix((jac_coord.ravel(), (r3, c3)), shape=(maps.n_global_state, maps.n_global_coord)).tocsr()
+    return R, dRdU, dRdx

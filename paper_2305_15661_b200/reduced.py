@@ -87,6 +87,9 @@ def reconstruct(bases, coords):
     return U, x
 
 
+EJ_SIZE = 24 + 24 * 24 + 24 * 72 + 24 * 6  # STROM_ELEMJAC record per element (include/strom_b200.h)
+
+
 def _as_f64(a, device):
     return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).to(device)
 
@@ -214,6 +217,7 @@ class GpuReducedOperator:
             _lib.OBJECTIVE: P, _lib.RESNORM2: P, _lib.DERIVS: P * (1 + K + K * K),
             _lib.CONTRIB: P * ne * K, _lib.CONTRIB_SPLIT: P * ne * 2 * K,
             _lib.RESIDUAL: P * ne * self.dm.nu, _lib.CONTRIB_LPROWS: P * (K + 1) * ne,
+            _lib.ELEMJAC: P * ne * EJ_SIZE,
         }[mode]
         if out is None:
             out = torch.empty(size, dtype=torch.float64, device=self.device)
@@ -244,6 +248,7 @@ class GpuReducedOperator:
         n_out = {
             _lib.OBJECTIVE: 1, _lib.RESNORM2: 1, _lib.DERIVS: 1 + K + K * K, _lib.CONTRIB: ne * K,
             _lib.CONTRIB_SPLIT: ne * 2 * K, _lib.RESIDUAL: ne * self.dm.nu, _lib.CONTRIB_LPROWS: (K + 1) * ne,
+            _lib.ELEMJAC: ne * EJ_SIZE,
         }[mode]
         out = np.empty(n_out)
         stream = torch.cuda.current_stream(self.device).cuda_stream

@@ -1,0 +1,75 @@
+"""GPU full-space assembly (fullspace.assemble_global, dg.py:228-272) vs the reference's element
+Jacobian goldens (dg.py:197-225, stored by make_golden.py) and vs the oracle's dual-number
+assembly over every element."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle.dual as D
+from oracle.element import OracleGeometry, element_eval
+
+from cases import build, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def fields(case, g):
+    U = case.phi @ g["w"] + (case.state_offset if case.state_offset is not None else 0.0)
+    x = case.ref_coords + case.psi @ g["tau"]
+    return U, x
+
+
+@pytest.mark.parametrize("name", ["euler_square_q6", "euler_square_default", "sector"])
+def test_element_jacobians_match_reference_goldens(name):
+    from paper_2305_15661_b200.fullspace import element_jacobians
+
+    case, g = build(name)
+    U, x = fields(case, g)
+    res, js, jn, jx = element_jacobians(case.law, case.geom, U, x, case.mus[0])
+    elems = sorted({int(k[4:].split("_")[0]) for k in g if k.startswith("elem") and k.endswith("_res")})
+    assert elems
+    for e in elems:
+        scale = np.max(np.abs(g[f"elem{e}_jself"]))
+        assert rel_err(res[e], g[f"elem{e}_res"]) < 1e-10
+        assert rel_err(js[e], g[f"elem{e}_jself"]) < 1e-10
+        assert rel_err(jn[e], g[f"elem{e}_jneigh"], scale) < 1e-10  # off-face reference entries are ~1e-16
+        assert rel_err(jx[e], g[f"elem{e}_jcoord"]) < 1e-10
+
+
+def test_assemble_global_matches_oracle():
+    from paper_2305_15661_b200.fullspace import assemble_global
+
+    case, g = build("sector")
+    U, x = fields(case, g)
+    mu = case.mus[0]
+    R, dRdU, dRdx = assemble_global(case.law, case.mesh, case.maps, U, x, mu, geom=case.geom)
+    # oracle: every element seeded with identity tangents [U_e | U_nbr | x_e] (dg.py:184-195)
+    geom = OracleGeometry(case.mesh, case.maps, case.quad_order)
+    els = np.arange(case.mesh.num_elements)
+    Ue, Un = geom.gather_state(U, els)
+    xe = geom.gather_coords(x, els)
+    nu, ng = 24, 3
+    T = 4 * nu + 2 * ng
+    out = element_eval(case.law, geom, els, D.seed_identity(Ue, 0, T), D.seed_identity(Un, nu, T),
+                       D.seed_identity(xe, 4 * nu, T), mu)
+    tan = out.res.tan
+    maps = case.maps
+    Ju = np.zeros((maps.n_global_state, maps.n_global_state))
+    Jx = np.zeros((maps.n_global_state, maps.n_global_coord))
+    sm, nm, cm = maps.state_map, maps.neighbor_map, maps.coord_map
+    for e in els:
+        np.add.at(Ju, (sm[e][:, None], sm[e][None, :]), tan[e][:, :nu])
+        ok = nm[e] >= 0
+        np.add.at(Ju, (sm[e][:, None], nm[e][ok][None, :]), tan[e][:, nu:4 * nu][:, ok])
+        np.add.at(Jx, (sm[e][:, None], cm[e][None, :]), tan[e][:, 4 * nu:])
+    assert rel_err(R, out.res.val.reshape(-1)) < 1e-10
+    assert rel_err(dRdU.toarray(), Ju) < 1e-10 and rel_err(dRdx.toarray(), Jx) < 1e-10
+    assert dRdU.shape == (maps.n_global_state, maps.n_global_state)
