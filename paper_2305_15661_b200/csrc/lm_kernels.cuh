@@ -550,7 +550,10 @@ static __device__ int block_compact(const int* flags, int n, int* list, int* wsu
 // LM_MAXWAIT rounds in a row): the mu meet at their derivative evaluations, so each K1 pass
 // is a full batch (cfg3: 92 -> ~40 passes per batch); deferred requests stay posted and the
 // mu waits, so no mu's iterates change.  In graph mode the IF / WHILE conditions are set here.
-constexpr int LM_MAXWAIT = 3;
+#ifndef STROM_LM_MAXWAIT
+#define STROM_LM_MAXWAIT 3
+#endif
+constexpr int LM_MAXWAIT = STROM_LM_MAXWAIT;
 
 static __global__ void __launch_bounds__(1024) lm_compact_kernel(LmRun R, cudaGraphConditionalHandle h_while,
                                                                  cudaGraphConditionalHandle h_d,
