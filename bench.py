@@ -10,8 +10,11 @@ all elements, rho = 1) — ``ReducedOperator.derivatives`` (strom/reduced.py:
 209-229).
 
 The same JSON line carries "gn": the second half of BASELINE.json's metric,
-ROM Gauss-Newton solves/s on config 3 (40k-triangle half-cylinder sector,
-k_u=20, k_x=10, 800 EQP elements, 64 mu per batch, LM max_iters=30).
+ROM Gauss-Newton solves/s on config 3 (40k-triangle half-cylinder sector with
+a slip wall, k_u=20, k_x=10, 800 EQP elements, 64 mu per batch, LM
+max_iters=30), and "cfg4" / "cfg5": the sharded training configs (EQP LP rows
+of 64 snapshots over 400k triangles; one 1,024-candidate greedy step).  The
+timed config-2 step is replayed as one CUDA graph (``--no-graph``: eager).
 
 Arms:
   default            this repo's CUDA path; ``value`` = elements/s with inputs
@@ -27,9 +30,10 @@ Arms:
                      config-2-generator elements per process, and stock
                      ``lm_solve`` on config-3 mu for "gn"; the oracle port
                      (oracle/) only if the install is missing.
-Multi-GPU (torchrun): elements are split into contiguous ranges, each rank
-reduces its range and the 1+K+K^2 sums are all-reduced over NCCL
-(strong scaling; max-over-ranks device time).
+Multi-GPU (torchrun): config 2's elements are split into contiguous ranges,
+each rank reduces its range and the 1+K+K^2 sums are all-reduced over NCCL
+(strong scaling; max-over-ranks device time); config 3 runs one 64-mu batch per
+rank (weak); configs 4 / 5 shard snapshots / candidates (sharded.py, greedy.py).
 """
 
 import argparse
@@ -578,24 +582,50 @@ def run_mine(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # the step (counter memsets, K1, finalize, and the NCCL all-reduce for N > 1) captured once
+    # as a CUDA graph and replayed: no per-kernel launch gaps (eager with --no-graph or when the
+    # capture is not possible, e.g. the gloo functional runs)
+    graph, graph_note = None, "eager launches"
+    if not args.no_graph and (world == 1 or dist.get_backend() == "nccl"):
+        try:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                step()
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
+            torch.cuda.synchronize()
+            graph_note = "one CUDA graph per step (memsets, K1, finalize" + (", NCCL all-reduce)" if world > 1 else ")")
+        except Exception as exc:  # noqa: BLE001
+            graph, graph_note = None, f"eager launches (graph capture failed: {type(exc).__name__})"
+    run = graph.replay if graph is not None else step
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = Clocks(local)
     lib = _lib.load()
-    lib.strom_profile(op._h, 1)
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(st)
     for _ in range(args.steps):
-        step()
+        run()
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    clocks = clk.stop()
+    # K1 kernel time: events around every K1 launch of the same number of eager steps
+    lib.strom_profile(op._h, 1)
+    for _ in range(args.steps):
+        op.eval_batched(_lib.DERIVS, W, Tau, Mu, rho, out=out, degen=degen)
     nl = _lib.C.c_int32()
     kern_ms = lib.strom_profile_ms(op._h, _lib.C.byref(nl))
     lib.strom_profile(op._h, 0)
-    clocks = clk.stop()
     if world > 1:
         t = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -670,7 +700,7 @@ def run_mine(args):
                      "flops_per_element": F, "flops_per_launch": per_launch_flops,
                      "kernel_ms_avg": kern_avg_s * 1e3, "peak_source": peak_src,
                      "hbm_bytes_per_launch": bytes_per_pass(ne, case.mesh.num_nodes, nu, ku, kx) * (hi - lo) / ne},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": 2 * args.steps, "step_launch": graph_note,
         "clocks": clocks,
     }
     if e2e_value is not None:
@@ -700,6 +730,7 @@ def main():
     ap.add_argument("--no-gn", action="store_true", help="skip the config-3 Gauss-Newton solves/s measurement")
     ap.add_argument("--gn-steps", type=int, default=20, help="timed 64-mu LM batches of the GN measurement")
     ap.add_argument("--no-sharded", action="store_true", help="skip the config-4 / config-5 sharded measurements")
+    ap.add_argument("--no-graph", action="store_true", help="time the config-2 step with eager launches")
     ap.add_argument("--cfg-steps", type=int, default=3, help="timed steps of the config-4 / config-5 measurements")
     args = ap.parse_args()
     if args.warmup < 3:

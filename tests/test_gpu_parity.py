@@ -118,3 +118,10 @@ def test_gpu_ku_zero_matches_oracle():
     Se_r, Te_r = ref.elemental_contributions(np.zeros(0), tau, mu)
     assert Se.shape == (case.mesh.num_elements, 0) and rel_err(Te, Te_r) < TOL
     assert rel_err(op.objective(c, mu), ref.objective(np.zeros(0), tau, mu)) < TOL
+
+
+def test_graft_smoke_entry():
+    """The driver's smoke() (one small derivatives pass on cuda:0 checked against the oracle)."""
+    import __graft_entry__
+
+    __graft_entry__.smoke()
