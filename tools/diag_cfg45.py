@@ -33,6 +33,9 @@ if which == "4":
 else:
     P = int(sys.argv[2]) if len(sys.argv) > 2 else 64
     case = configs.cfg5_rom(P)
+    if len(sys.argv) > 3:  # distortion weight override
+        case.kappa = float(sys.argv[3])
+        print("kappa", case.kappa)
     op = GpuReducedOperator(case.law, case.geom, ReducedBases(case.phi, case.psi, case.ref_coords), case.dist)
     res = lm_solve_batched(op, case.mus, case.W[0], None, WeightVector(case.rho), LmConfig(max_iters=10))
     W = np.stack([r.w for r in res]); T = np.stack([r.tau for r in res])
