@@ -84,3 +84,27 @@ def test_gpu_lm_converges_on_consistent_problem():
     for r in res:
         assert np.isfinite(r.objective)
         assert r.reason in ("first-order", "max-iters", "line-search-failure")
+
+
+@pytest.mark.parametrize("max_backtracks", [0, 1, 3])
+def test_gpu_lm_backtrack_budget_matches_oracle(max_backtracks):
+    """LmConfig.max_backtracks, including 0 (no trial at all: lambda escalates until the cap,
+    then line-search-failure, lm.py:226-241), follows the oracle's LM decisions."""
+    import oracle.dual  # noqa: F401
+    from oracle import lm as olm
+    from oracle.element import OracleGeometry, OracleReducedOperator
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.lm import LmConfig, lm_solve_batched
+
+    case, g = build("strip")
+    op = gpu_op(case)
+    res = lm_solve_batched(op, case.mus[:2], None, None, WeightVector(case.rho),
+                           LmConfig(max_iters=6, max_backtracks=max_backtracks))
+    ora = OracleReducedOperator(case.law, OracleGeometry(case.mesh, case.maps, case.quad_order), case.phi, case.psi,
+                                case.ref_coords, case.kappa, case.eps)
+    for i, r in enumerate(res):
+        want = olm.lm_solve(olm.OracleProblem(ora, case.mus[i], case.rho),
+                            olm.LmConfig(max_iters=6, max_backtracks=max_backtracks))
+        assert r.reason == want.reason and r.n_iters == want.n_iters
+        assert len(r.history) == len(want.history)
+        assert np.allclose(r.history[:, [0, 4, 5]], want.history[:, [0, 4, 5]], rtol=1e-8, equal_nan=True)

@@ -33,7 +33,7 @@ if which == "4":
 else:
     P = int(sys.argv[2]) if len(sys.argv) > 2 else 64
     case = configs.cfg5_rom(P)
-    if len(sys.argv) > 3:  # distortion weight override
+    if len(sys.argv) > 3:  # distortion weight override (cfg5_rom default: 1.0)
         case.kappa = float(sys.argv[3])
         print("kappa", case.kappa)
     op = GpuReducedOperator(case.law, case.geom, ReducedBases(case.phi, case.psi, case.ref_coords), case.dist)
