@@ -130,7 +130,7 @@ def test_greedy_step_single_rank():
         assert v == ref[best] or abs(v - ref[best]) <= 1e-10 * abs(ref[best])
 
 
-@pytest.mark.parametrize("ku,kx", [(20, 10), (24, 12), (32, 8), (5, 3)])
+@pytest.mark.parametrize("ku,kx", [(20, 10), (24, 12), (32, 8), (5, 3), (24, 16)])
 def test_reduced_dimensions_match_oracle(ku, kx):
     """Config 3 / 5 reduced dimensions (K = 30, 36) and odd / maximal k_u on the
     DMMA kernel (n-tile padding, 10 and 15 Gram tiles) vs the oracle."""
@@ -208,3 +208,29 @@ def test_value_many_points_matches_oracle_and_single_point_path():
     for p in range(P):
         one = op.objective(ReducedCoords(W[p], Tau[p]), mus[p], rho)
         assert abs(obj[p] - one) <= 1e-12 * abs(one)
+
+
+def test_batched_points_equal_single_calls():
+    """eval_batched over many parameter points (K2 multi-point kernel, K1 batched pass) gives the
+    single-point public API's values for every point (objective, derivatives)."""
+    from paper_2305_15661_b200 import _lib
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.reduced import ReducedCoords
+
+    case = small_sector()
+    op = gpu_op(case)
+    rng = np.random.default_rng(9)
+    P = 70
+    W = case.W[0] + 0.02 * rng.standard_normal((P, 6))
+    Tau = 1e-3 * rng.standard_normal((P, 4))
+    mus = rng.uniform(2.0, 4.0, (P, 1))
+    rho = WeightVector(case.rho)
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    obj, _ = op.eval_batched(_lib.OBJECTIVE, dev(W), dev(Tau), dev(mus), rho)
+    der, _ = op.eval_batched(_lib.DERIVS, dev(W), dev(Tau), dev(mus), rho)
+    obj, der = obj.cpu().numpy(), der.cpu().numpy().reshape(P, -1)
+    for p in range(0, P, 7):
+        c = ReducedCoords(W[p], Tau[p])
+        assert rel_err(obj[p], op.objective(c, mus[p], rho)) < 1e-12
+        J, S, T, Hww, Hwt, Htt = op.derivatives(c, mus[p], rho)
+        assert rel_err(der[p, 0], J) < 1e-12 and rel_err(der[p, 1:7], S) < 1e-12
