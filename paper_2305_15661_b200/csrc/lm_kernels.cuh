@@ -22,7 +22,7 @@ namespace strom {
 #define STROM_LM_B 4
 #endif
 #ifndef STROM_LM_THREADS
-#define STROM_LM_THREADS 64
+#define STROM_LM_THREADS 256
 #endif
 constexpr int LM_B = STROM_LM_B;              // speculative objective trials per round
 constexpr int LM_THREADS = STROM_LM_THREADS;  // threads of the per-mu control block
@@ -99,7 +99,11 @@ __device__ __forceinline__ double nrm2(const double* v, int n) {
 // LDL^T solve of the n x n symmetric system in A (row-major, overwritten) for
 // x = A^{-1} b; all threads of the block participate.  Returns false when a
 // pivot is zero / non-finite or the solution is non-finite.
-static __device__ bool ldlt_solve(double* A, int n, double* b, double* x, int* flag) {
+// tri[q] = (ii << 8) | kk for the row-major lower triangle q = ii (ii + 1) / 2 + kk, kk <= ii
+// (the enumeration is the same prefix for every triangle size, so one table serves every step)
+constexpr int LM_TRI = KMAX * (KMAX + 1) / 2;
+
+static __device__ bool ldlt_solve(double* A, int n, double* b, double* x, int* flag, const unsigned short* tri) {
   const int t = threadIdx.x, nt = blockDim.x;
   if (t == 0) *flag = 1;
   __syncthreads();
@@ -116,11 +120,7 @@ static __device__ bool ldlt_solve(double* A, int n, double* b, double* x, int* f
     // (per entry the same j-ascending update sequence as the row-wise loop)
     const int m = n - j - 1, cnt = m * (m + 1) / 2;
     for (int q = t; q < cnt; q += nt) {
-      // q -> (ii, kk) with 0 <= kk <= ii < m, row-major over the lower triangle
-      int ii = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
-      while (ii * (ii + 1) / 2 > q) --ii;
-      while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
-      const int kk = q - ii * (ii + 1) / 2;
+      const int ii = tri[q] >> 8, kk = tri[q] & 255;  // (ii, kk), 0 <= kk <= ii < m
       const int i = j + 1 + ii, k = j + 1 + kk;
       A[i * n + k] -= (A[i * n + j] * d) * A[k * n + j];
     }
@@ -421,6 +421,13 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
   __shared__ int s_act, s_flag;
   __shared__ LmState s;
   __shared__ int s_hold;
+  __shared__ unsigned short s_tri[LM_TRI];
+  for (int q = threadIdx.x; q < K * (K + 1) / 2; q += blockDim.x) {
+    int ii = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+    while (ii * (ii + 1) / 2 > q) --ii;
+    while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
+    s_tri[q] = (unsigned short)((ii << 8) | (q - ii * (ii + 1) / 2));
+  }
   const int par = R.ctl->round & 1;
   int* const counters = R.ctl->cnt[par];
   if (blockIdx.x == 0 && threadIdx.x < 4) R.ctl->cnt[par ^ 1][threadIdx.x] = 0;  // next round's set
@@ -487,7 +494,7 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
     }
     for (int i = t; i < n; i += nt) rhs[i] = -c_S[i];
     __syncthreads();
-    const bool ok = ldlt_solve(A, n, rhs, x, &s_flag);
+    const bool ok = ldlt_solve(A, n, rhs, x, &s_flag, s_tri);
     if (t == 0) s_act = lm_after_solve(Rl, p, s, act, ok, x, A, rhs);
     __syncthreads();
   }
