@@ -58,6 +58,7 @@ struct LmCtl {
   int dcount, ocount; // rows of this round's derivatives / objective passes (dlist / olist)
   int nd, no;         // passes run (statistics)
   int overflow;       // max_rounds reached with unfinished solves
+  int ticket;         // control blocks finished this round (the last one ends the round)
 };
 
 struct LmRun {
@@ -412,7 +413,14 @@ static __device__ int lm_after_solve(const LmRun& R, int p, LmState& s, int act,
 }
 
 // one control round; blockDim = LM_THREADS, dynamic smem (K*K + 2K) doubles
-static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) {
+static __device__ void lm_round_end(const LmRun& R, cudaGraphConditionalHandle h_while, cudaGraphConditionalHandle h_d,
+                                    cudaGraphConditionalHandle h_o, int graph);
+static __device__ void lm_control_body(const LmRun& R, int p, LmState& s, double* A, double* rhs, double* x,
+                                       const unsigned short* s_tri, int* counters, int* s_act_p, int* s_flag_p);
+
+static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R, cudaGraphConditionalHandle h_while,
+                                                                       cudaGraphConditionalHandle h_d,
+                                                                       cudaGraphConditionalHandle h_o, int graph) {
   extern __shared__ double sm[];
   const int p = blockIdx.x, K = R.K;
   double* A = sm;
@@ -450,8 +458,27 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
       if (R.req_d[p]) atomicAdd(&counters[1], 1);
       if (R.req_o[p * LM_B]) atomicAdd(&counters[2], 1);
     }
-    return;
+  } else {
+    lm_control_body(R, p, s, A, rhs, x, s_tri, counters, &s_act, &s_flag);
   }
+  // the last block to finish ends the round (compaction, pass decisions, graph conditions)
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&R.ctl->ticket, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    lm_round_end(R, h_while, h_d, h_o, graph);
+  }
+}
+
+static __device__ void lm_control_body(const LmRun& R, int p, LmState& s, double* A, double* rhs, double* x,
+                                       const unsigned short* s_tri, int* counters, int* s_act_p, int* s_flag_p) {
+  const int K = R.K;
+  int& s_act = *s_act_p;
   // the mu's vectors live in shared memory for the round: the state machine (thread 0)
   // then works on shared copies; loads / stores of the global arrays are block-parallel
   __shared__ double c_w[32], c_tau[KXMAX], c_dw[KMAX], c_S[KMAX], c_best[KMAX];
@@ -494,7 +521,7 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
     }
     for (int i = t; i < n; i += nt) rhs[i] = -c_S[i];
     __syncthreads();
-    const bool ok = ldlt_solve(A, n, rhs, x, &s_flag, s_tri);
+    const bool ok = ldlt_solve(A, n, rhs, x, s_flag_p, s_tri);
     if (t == 0) s_act = lm_after_solve(Rl, p, s, act, ok, x, A, rhs);
     __syncthreads();
   }
@@ -520,13 +547,14 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R) 
   }
 }
 
-// ascending compaction of flags[0 .. n) into list (one block, deterministic); returns the
-// count to every thread
+// ascending compaction of flags[0 .. n) into list (one block, deterministic; the flags were
+// written by other blocks of the same launch, so they are read past L1); returns the count to
+// every thread
 static __device__ int block_compact(const int* flags, int n, int* list, int* wsum) {
   const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
   const int per = (n + blockDim.x - 1) / blockDim.x, lo = t * per;
   int c = 0;
-  for (int i = lo; i < lo + per && i < n; ++i) c += flags[i] != 0;
+  for (int i = lo; i < lo + per && i < n; ++i) c += __ldcg(flags + i) != 0;  // written by other blocks
   int x = c;  // inclusive warp scan
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, x, o);
@@ -545,13 +573,13 @@ static __device__ int block_compact(const int* flags, int n, int* list, int* wsu
   __syncthreads();
   int pos = x - c + (wp > 0 ? wsum[wp - 1] : 0);
   for (int i = lo; i < lo + per && i < n; ++i)
-    if (flags[i]) list[pos++] = i;
+    if (__ldcg(flags + i)) list[pos++] = i;
   const int total = wsum[(blockDim.x >> 5) - 1];
   __syncthreads();
   return total;
 }
 
-// End of a control round (one block): compact the requested derivative / objective rows and
+// End of a control round (the last control block to finish): compact the requested derivative / objective rows and
 // decide on the device what the round launches.  A derivatives pass waits until every
 // unfinished mu asks for one (or no objective trials are pending, or it was deferred
 // LM_MAXWAIT rounds in a row): the mu meet at their derivative evaluations, so each K1 pass
@@ -562,16 +590,15 @@ static __device__ int block_compact(const int* flags, int n, int* list, int* wsu
 #endif
 constexpr int LM_MAXWAIT = STROM_LM_MAXWAIT;
 
-static __global__ void __launch_bounds__(1024) lm_compact_kernel(LmRun R, cudaGraphConditionalHandle h_while,
-                                                                 cudaGraphConditionalHandle h_d,
-                                                                 cudaGraphConditionalHandle h_o, int graph) {
+static __device__ void lm_round_end(const LmRun& R, cudaGraphConditionalHandle h_while, cudaGraphConditionalHandle h_d,
+                                    cudaGraphConditionalHandle h_o, int graph) {
   __shared__ int wsum[32];
   LmCtl& C = *R.ctl;
   const int* cnt = C.cnt[C.round & 1];
   const int nobj = block_compact(R.req_o, R.P * LM_B, R.olist, wsum);
   const int nder = block_compact(R.req_d, R.P, R.dlist, wsum);
   if (threadIdx.x != 0) return;
-  const int n_active = cnt[0], n_d = cnt[1], n_o = cnt[2];
+  const int n_active = __ldcg(cnt), n_d = __ldcg(cnt + 1), n_o = __ldcg(cnt + 2);  // atomics of every block
   const bool run_d = n_d > 0 && (n_o == 0 || n_d >= n_active || C.waited >= LM_MAXWAIT);
   const bool run_o = n_o > 0;
   C.waited = (n_d > 0 && !run_d) ? C.waited + 1 : 0;
@@ -582,6 +609,7 @@ static __global__ void __launch_bounds__(1024) lm_compact_kernel(LmRun R, cudaGr
   C.dcount = nder;
   C.ocount = nobj;
   C.round += 1;
+  C.ticket = 0;
   const bool more = n_active > 0 && C.round < R.max_rounds;
   if (n_active > 0 && !more) C.overflow = 1;
   *R.degen_fill = 0;
