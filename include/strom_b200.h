@@ -75,9 +75,10 @@ enum {
   STROM_RESIDUAL = 4,       /* out[P][N_u]: global residual vector        dg.py:238-240     */
   STROM_RESNORM2 = 5,       /* out[P]: sum_e |R_e|^2 over the element set (greedy indicator) */
   STROM_CONTRIB_LPROWS = 6, /* out[P][K+1][ne]: S_e,T_e and 0.5(|R_e|^2+N_e^2) as LP rows (config 4) */
-  STROM_ELEMJAC = 7         /* out[ne][24 + 24*24 + 24*72 + 24*6]: res, dR/dU_e, dR/dU_nbr (3 faces x 24),
-                               dR/dx_e per element at U = U0, x = x_ref (P = 1; 4-component laws, p = 2)
-                               dg.py:197-225, the blocks assemble_global scatters (dg.py:241-272) */
+  STROM_ELEMJAC = 7         /* out[ne][24 + 24*24 + 24*72 + 24*6 + 7]: res, dR/dU_e, dR/dU_nbr (3 faces x 24),
+                               dR/dx_e, N_e, dN_e/dx_e per element at U = U0, x = x_ref (P = 1;
+                               4-component laws, p = 2): dg.py:197-225 and distortion.py:64-92, the
+                               blocks assemble_global / assemble_distortion scatter */
 };
 
 int strom_create(const strom_mesh_desc* mesh, const strom_law_desc* law, const strom_quad_desc* quad,

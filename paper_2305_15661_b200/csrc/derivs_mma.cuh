@@ -142,9 +142,10 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   constexpr bool CT = KUT > 0;
   const bool DERIVS = DM >= 0 ? DM == 1 : r.mode == MODE_DERIVS;  // compile-time on the specialised path
   // element Jacobian blocks (full-space assembly, dg.py:197-272; generic instantiation only):
-  // out[e] = [res (NU) | dR/dU_e (NU x NU) | dR/dU_nbr (NU x 3 NU) | dR/dx_e (NU x 6)]
+  // out[e] = [res (NU) | dR/dU_e (NU x NU) | dR/dU_nbr (NU x 3 NU) | dR/dx_e (NU x 6) | N_e | dN_e/dx_e (6)]
   const bool EJ = DM < 0 && r.mode == MODE_ELEMJAC;
-  constexpr int EJ_SELF = 24, EJ_NBR = EJ_SELF + 24 * 24, EJ_X = EJ_NBR + 24 * 72, EJ_SZ = EJ_X + 24 * 6;
+  constexpr int EJ_SELF = 24, EJ_NBR = EJ_SELF + 24 * 24, EJ_X = EJ_NBR + 24 * 72, EJ_D = EJ_X + 24 * 6,
+                EJ_SZ = EJ_D + 7;
   constexpr int KT = KUT + KXT, KPT = (KT + 7) / 8 * 8;
   const int ku = CT ? KUT : r.ku, kx = CT ? KXT : r.kx, K = CT ? KT : r.K, KP = CT ? KPT : r.KP;
   const int LDJ = CT ? KPT + 4 : r.LDJ;
@@ -852,6 +853,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     if (EJ) {  // dR_e/dx_e (local coordinates 2 g + i) and the residual
       for (int i = lane; i < NU * 6; i += 32) ej[EJ_X + i] = RA[DRXo + (i / 6) * LDX + i % 6];
       if (lane < NU) ej[lane] = S[SH::RT + lane];
+      if (lane < 7) ej[EJ_D + lane] = lane == 0 ? S[SH::MN] : S[SH::DNX + lane - 1];  // distortion.py:64-92
     }
     // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
     double* Jt = RA;

@@ -20,9 +20,8 @@ class _NoDistortion:
     kappa, eps = 1.0, 1e-8
 
 
-def element_jacobians(law, geom, U, x, mu, device=None):
-    """(res (ne, 24), jac_self (ne, 24, 24), jac_neigh (ne, 24, 72), jac_coord (ne, 24, 6)) at
-    the global state U and coordinates x (dg.py:197-225, batched over all elements)."""
+def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenerate=True):
+    """(ne, EJ_SIZE) STROM_ELEMJAC records at the global state U and coordinates x."""
     import torch
 
     mesh, maps = geom.mesh, geom.maps
@@ -31,21 +30,48 @@ def element_jacobians(law, geom, U, x, mu, device=None):
     U = np.asarray(U, dtype=float).reshape(-1)
     x = np.asarray(x, dtype=float).reshape(-1)
     bases = ReducedBases(np.zeros((U.size, 0)), np.zeros((x.size, 0)), x)
-    op = GpuReducedOperator(law, geom, bases, _NoDistortion(), device=device, state_offset=U)
+    op = GpuReducedOperator(law, geom, bases, dist or _NoDistortion(), device=device, state_offset=U)
     W = torch.zeros((1, op.k_u), dtype=torch.float64, device=op.device)
     Tau = torch.zeros((1, 1), dtype=torch.float64, device=op.device)
     Mu = torch.as_tensor(op._mu(mu)[None]).to(op.device)
     out, rc = op.eval_batched(_lib.ELEMJAC, W, Tau, Mu, None, sync=True)
-    if rc == 1:  # g <= 0 somewhere: raised after the whole batch, as dg.py:177-178
+    if rc == 1 and raise_degenerate:  # g <= 0 somewhere: raised after the whole batch, as dg.py:177-178
         from .reduced import degenerate_error
 
         n = op._lib.strom_degenerate_elements(op._h, 0, None, 0)
         ids = np.zeros(max(n, 1), dtype=np.int32)
         op._lib.strom_degenerate_elements(op._h, 0, ids.ctypes.data, n)
         raise degenerate_error(ids[:n].astype(np.int64))
-    o = out.view(mesh.num_elements, EJ_SIZE).cpu().numpy()
+    return out.view(mesh.num_elements, EJ_SIZE).cpu().numpy()
+
+
+def element_jacobians(law, geom, U, x, mu, device=None):
+    """(res (ne, 24), jac_self (ne, 24, 24), jac_neigh (ne, 24, 72), jac_coord (ne, 24, 6)) at
+    the global state U and coordinates x (dg.py:197-225, batched over all elements)."""
+    o = _element_records(law, geom, U, x, mu, device=device)
     return (o[:, :24], o[:, 24:600].reshape(-1, 24, 24), o[:, 600:2328].reshape(-1, 24, 72),
-            o[:, 2328:].reshape(-1, 24, 6))
+            o[:, 2328:2472].reshape(-1, 24, 6))
+
+
+def assemble_distortion(mesh, maps, x, config, want_jacobian=True, geom=None, device=None):
+    """Elemental distortion residuals N (ne,) and the CSR gradient dN/dx (ne, N_x):
+    strom/distortion.py:71-92 (never raises: eps floors the Jacobian determinant)."""
+    from . import laws as L
+    from .mesh import get_geometry
+
+    geom = geom or get_geometry(mesh, maps)
+    if maps.n_comp != 4 or maps.degree_sol != 2:
+        raise NotImplementedError("GPU distortion assembly runs on the p = 2, 4-component element kernel")
+    U = np.tile(L.euler_freestream(2.0), mesh.num_elements * 6)  # the state does not enter N
+    law = L.euler(tags={t: "extrapolate" for t in mesh.boundary_tags})
+    o = _element_records(law, geom, U, x, np.array([2.0]), dist=config, device=device, raise_degenerate=False)
+    N = o[:, 2472].copy()
+    if not want_jacobian:
+        return N, None
+    rows = np.repeat(np.arange(mesh.num_elements), 6)
+    jac = sp.coo_matrix((o[:, 2473:2479].ravel(), (rows, maps.coord_map.ravel())),
+                        shape=(mesh.num_elements, maps.n_global_coord)).tocsr()
+    return N, jac
 
 
 def assemble_global(law, mesh, maps, U, x, mu, want_jacobians=True, geom=None, device=None):

@@ -87,7 +87,7 @@ def reconstruct(bases, coords):
     return U, x
 
 
-EJ_SIZE = 24 + 24 * 24 + 24 * 72 + 24 * 6  # STROM_ELEMJAC record per element (include/strom_b200.h)
+EJ_SIZE = 24 + 24 * 24 + 24 * 72 + 24 * 6 + 7  # STROM_ELEMJAC record per element (include/strom_b200.h)
 
 
 def _as_f64(a, device):

@@ -73,3 +73,25 @@ def test_assemble_global_matches_oracle():
     assert rel_err(R, out.res.val.reshape(-1)) < 1e-10
     assert rel_err(dRdU.toarray(), Ju) < 1e-10 and rel_err(dRdx.toarray(), Jx) < 1e-10
     assert dRdU.shape == (maps.n_global_state, maps.n_global_state)
+
+
+def test_assemble_distortion_matches_oracle():
+    """fullspace.assemble_distortion (distortion.py:71-92) vs the oracle's dual-number
+    distortion residuals and their coordinate gradients."""
+    from oracle.element import distortion_eval
+    from paper_2305_15661_b200.configs import DistortionConfig
+    from paper_2305_15661_b200.fullspace import assemble_distortion
+
+    case, g = build("sector")
+    _, x = fields(case, g)
+    cfg = DistortionConfig(case.kappa, case.eps)
+    N, jac = assemble_distortion(case.mesh, case.maps, x, cfg, geom=case.geom)
+    geom = OracleGeometry(case.mesh, case.maps, case.quad_order)
+    els = np.arange(case.mesh.num_elements)
+    xe = geom.gather_coords(x, els)
+    out = distortion_eval(geom, els, D.seed_identity(xe, 0, 6), case.kappa, case.eps)
+    assert rel_err(N, D.val(out)) < 1e-10
+    want = np.zeros((len(els), case.maps.n_global_coord))
+    for e in els:
+        np.add.at(want, (e, case.maps.coord_map[e]), out.tan[e])
+    assert rel_err(jac.toarray(), want) < 1e-10
