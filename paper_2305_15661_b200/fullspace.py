@@ -1,12 +1,13 @@
-"""Full-space assembly on the GPU (first part): ``assemble_global`` with the
-sparse Jacobians dR/dU and dR/dx (strom/dg.py:228-272).
+"""Full-space assembly on the GPU: ``assemble_global`` with the sparse
+Jacobians dR/dU and dR/dx (strom/dg.py:228-272), ``assemble_distortion``
+(distortion.py:71-92) and the HDM Newton / PTC solve ``solve_hdm`` (dg.py:343-400) on top.
 
 The element blocks — residual, dR_e/dU_e, dR_e/dU_nbr and dR_e/dx_e, i.e. what
 ``elemental_residual(..., want_jacobians=True)`` returns (dg.py:197-225) — come from the K1
 element kernel in its STROM_ELEMJAC mode (the same local Jacobians the reduced path projects,
 written out instead of projected); the scatter into CSR uses the reference's own index
 construction.  4-component laws (Euler) with p = 2; other laws raise.  The enriched test
-space (``assemble_enriched``), the HDM Newton solve and full-space tracking are not built.
+space (``assemble_enriched``) and full-space tracking are not built.
 """
 
 import numpy as np
@@ -101,3 +102,87 @@ def assemble_global(law, mesh, maps, U, x, mu, want_jacobians=True, geom=None, d
     c3 = np.broadcast_to(maps.coord_map[:, None, :], jac_coord.shape).ravel()
     dRdx = sp.coo_matrix((jac_coord.ravel(), (r3, c3)), shape=(maps.n_global_state, maps.n_global_coord)).tocsr()
     return R, dRdU, dRdx
+
+
+class HdmSolveError(RuntimeError):
+    """Mirror of strom.dg.HdmSolveError (dg.py:336-340)."""
+
+    def __init__(self, message, residual_norm, state):
+        super().__init__(message)
+        self.residual_norm = residual_norm
+        self.state = state
+
+
+def state_positions(geom, x):
+    """Positions of all solution nodes under the mapping coefficients x (geometry.py:156-160;
+    straight elements: barycentric combinations of the deformed vertices)."""
+    from .tables import lagrange_nodes
+
+    mesh, maps = geom.mesh, geom.maps
+    xi = lagrange_nodes(maps.degree_sol)  # (nb, 2) reference nodes
+    bary = np.stack([1.0 - xi[:, 0] - xi[:, 1], xi[:, 0], xi[:, 1]], axis=1)  # P1 shape functions
+    x_e = np.asarray(x, dtype=float)[maps.coord_map].reshape(mesh.num_elements, -1, 2)[:, :3]
+    return np.einsum("ng,egi->eni", bary, x_e)
+
+
+def initial_state(law, mesh, maps, x, mu, geom=None):
+    """Law-provided initial guess sampled at the deformed solution nodes (dg.py:329-333)."""
+    from .mesh import get_geometry
+
+    pos = state_positions(geom or get_geometry(mesh, maps), x)
+    return np.asarray(law.initial_state(pos, mu), dtype=float).reshape(-1)
+
+
+def solve_hdm(law, mesh, maps, x, mu, U_init=None, tol=1e-10, max_iters=80, geom=None, device=None):
+    """Damped Newton / pseudo-transient-continuation solve of the DG system on a frozen mesh
+    (dg.py:343-400): the residual and its sparse Jacobian are assembled on the GPU, the
+    linear systems factored with SuperLU on the host like the reference.  Returns the state
+    vector; raises HdmSolveError when it does not converge."""
+    import scipy.sparse.linalg as spla
+
+    from .mesh import get_geometry
+    from .reduced import DegenerateMappingError
+
+    geom = geom or get_geometry(mesh, maps)
+    U = initial_state(law, mesh, maps, x, mu, geom) if U_init is None else np.asarray(U_init, dtype=float).copy()
+    R, J, _ = assemble_global(law, mesh, maps, U, x, mu, geom=geom, device=device)
+    rnorm0 = np.linalg.norm(R)
+    target = tol * max(1.0, rnorm0)
+    rnorm = rnorm0
+    ptc = 0.0  # inverse pseudo-timestep; 0 = plain Newton
+    ident = sp.identity(maps.n_global_state, format="csr")
+    for _ in range(max_iters):
+        if rnorm <= target:
+            return U
+        A = J + ptc * ident if ptc > 0.0 else J
+        try:
+            dU = spla.splu(A.tocsc()).solve(-R)
+        except RuntimeError:
+            ptc = max(10.0 * ptc, 1e-4 * rnorm)
+            continue
+        alpha, best = 1.0, None
+        for _ in range(30):
+            try:
+                Rt, _, _ = assemble_global(law, mesh, maps, U + alpha * dU, x, mu, want_jacobians=False, geom=geom,
+                                           device=device)
+                nt = np.linalg.norm(Rt)
+            except DegenerateMappingError:
+                nt = np.inf
+            if nt < (1.0 - 1e-4 * alpha) * rnorm or nt <= target:
+                best = (alpha, nt)
+                break
+            alpha *= 0.5
+        if best is None:  # line search stalled: engage / strengthen pseudo-transient damping
+            ptc = max(4.0 * ptc, 1e-3 * max(rnorm, 1.0))
+            continue
+        U = U + best[0] * dU
+        rnorm = best[1]
+        if ptc > 0.0:  # relax damping as the residual drops
+            ptc = ptc / 4.0 if best[0] == 1.0 else ptc
+            if ptc < 1e-12 * max(rnorm, 1.0):
+                ptc = 0.0
+        R, J, _ = assemble_global(law, mesh, maps, U, x, mu, geom=geom, device=device)
+        rnorm = np.linalg.norm(R)
+    if rnorm <= target:
+        return U
+    raise HdmSolveError(f"HDM solve did not converge: |R| = {rnorm:.3e} (target {target:.3e})", rnorm, U)

@@ -95,3 +95,33 @@ def test_assemble_distortion_matches_oracle():
     for e in els:
         np.add.at(want, (e, case.maps.coord_map[e]), out.tan[e])
     assert rel_err(jac.toarray(), want) < 1e-10
+
+
+def test_solve_hdm_converges_and_matches_reference():
+    """fullspace.solve_hdm (dg.py:343-400 on GPU-assembled Jacobians) converges to the target and
+    to the reference's own solve_hdm state (stock code path, when the reference is installed)."""
+    from paper_2305_15661_b200 import configs, laws as L
+    from paper_2305_15661_b200.fullspace import assemble_global, solve_hdm
+
+    case = configs.sector_rom_case(n_radial=3, n_circ=6, ku=2, kx=1, frac_active=0.5, rho_scale=2.0, P=1, seed=95,
+                                   wall="extrapolate")
+    mu = np.array([3.0])
+    rng = np.random.default_rng(2)
+    U0 = np.tile(L.euler_freestream(3.0), case.mesh.num_elements * 6) * (1.0 + 0.02 * rng.standard_normal(
+        case.mesh.num_elements * 24))
+    x = case.ref_coords
+    U = solve_hdm(case.law, case.mesh, case.maps, x, mu, U_init=U0, geom=case.geom)
+    R0 = assemble_global(case.law, case.mesh, case.maps, U0, x, mu, want_jacobians=False, geom=case.geom)[0]
+    R = assemble_global(case.law, case.mesh, case.maps, U, x, mu, want_jacobians=False, geom=case.geom)[0]
+    assert np.linalg.norm(R) <= 1e-10 * max(1.0, np.linalg.norm(R0))
+    try:
+        from oracle import strom_ref
+
+        S = strom_ref.load()
+    except ImportError:
+        return
+    import strom.dg as sdg
+
+    rop = strom_ref.operator(case)  # the reference geometry (12-point rule) for this mesh
+    st = sdg.solve_hdm(case.law, rop.geom.mesh, rop.geom.maps, x, mu, U_init=U0)
+    assert rel_err(U, st.values) < 1e-8
