@@ -411,55 +411,25 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         fp[c][0] = __shfl_sync(0xffffffffu, f2[c][0], partner);
         fp[c][1] = __shfl_sync(0xffffffffu, f2[c][1], partner);
       }
-      if constexpr (LAW::ROE) {  // Roe (GPU-only extension): D = |A_roe(nh)| (u_out - u_in)
+      if constexpr (LAW::ROE) {  // Roe (GPU-only extension): the LLF-free part here, D in the Roe pass
         if (lane < 2 * NFS) {
-          // D and its Jacobian along this lane's own state (and, side 0, along nh): forward mode
-          Dn<6> ua[M], ub[M], nd[2];
-#pragma unroll
-          for (int c = 0; c < M; ++c) {
-            ua[c] = side ? cst<6>(up[c]) : seed<6>(us[c], c);
-            ub[c] = side ? seed<6>(us[c], c) : cst<6>(up[c]);
-          }
-          nd[0] = seed<6>(nh[0], M);
-          nd[1] = seed<6>(nh[1], M + 1);
-          Dn<6> Dd[M];
-          roe_diss(ua, ub, nd, la.p[0], la.p[1], Dd);
-          const bool dz = bc == 1;  // extrapolated exterior: u_out == u_in, D == 0 identically
-          const bool ext0 = side == 1 && bc >= 1 && !wall;
           double* FXp = RA + SH::FX;
           if (side == 0) {
 #pragma unroll
             for (int c = 0; c < M; ++c) {
-              const double dv = dz ? 0.0 : Dd[c].v;
               const double fni = f2[c][0] * nu[0] + f2[c][1] * nu[1], fno = fp[c][0] * nu[0] + fp[c][1] * nu[1];
-              RA[SH::HS + c * NFSP + fs] = wsq * (0.5 * (fni + fno) - 0.5 * len * dv);
+              RA[SH::HS + c * NFSP + fs] = wsq * (0.5 * (fni + fno));
               FXp[(2 * c + 0) * NFSP + fs] = 0.5 * wsq * (f2[c][0] + fp[c][0]);
               FXp[(2 * c + 1) * NFSP + fs] = 0.5 * wsq * (f2[c][1] + fp[c][1]);
-              FXp[(2 * M + c) * NFSP + fs] = 0.5 * wsq * dv;  // the FD stage's "du" slot carries D
             }
             FXp[(3 * M + 0) * NFSP + fs] = 1.0;  // "lam" = 1, its normal gradient 0: coef = dlen
             FXp[(3 * M + 1) * NFSP + fs] = 0.0;
             FXp[(3 * M + 2) * NFSP + fs] = 0.0;
-            // D's own normal dependence: -wsq len / 2 (dD/dnh . dnh) per unit normal perturbation,
-            // pre-written into the FD slots (the FD stage adds the flux and |nu| terms)
-            const double il = 1.0 / len;
-#pragma unroll
-            for (int dir = 0; dir < 2; ++dir) {
-              const double dlen = nh[dir];
-              const double dn0 = ((dir == 0 ? 1.0 : 0.0) - nh[0] * dlen) * il, dn1 = ((dir == 1 ? 1.0 : 0.0) - nh[1] * dlen) * il;
-#pragma unroll
-              for (int c = 0; c < M; ++c)
-                S[SH::FD + (c * 2 + dir) * NFSP + fs] =
-                    dz ? 0.0 : -0.5 * wsq * len * (Dd[c].d[M] * dn0 + Dd[c].d[M + 1] * dn1);
-            }
           }
-          // C_side = wsq (A_side / 2 - len / 2 dD/du_side)
 #pragma unroll
           for (int c = 0; c < M; ++c)
 #pragma unroll
-            for (int cp = 0; cp < M; ++cp)
-              RA[SH::CF + side * SH::CFS + (c * M + cp) * NFSP + fs] =
-                  A[c][cp] + ((ext0 || dz) ? 0.0 : -0.5 * wsq * len * Dd[c].d[cp]);
+            for (int cp = 0; cp < M; ++cp) RA[SH::CF + side * SH::CFS + (c * M + cp) * NFSP + fs] = A[c][cp];
 #pragma unroll
           for (int c = 0; c < M; ++c) {
             if (side == 0) {
@@ -546,6 +516,95 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       }
     }
     __syncwarp();
+    if constexpr (LAW::ROE) {  // ---- Roe pass: D = |A_roe(nh)| (u_out - u_in) and its Jacobians
+      // outside the P stage (fewer live values): lane = side * 12 + fs recomputes both traces,
+      // forward mode along its own state (Dn<4>) and, on side 0, along the face normal (Dn<2>)
+      if (lane < 2 * NFS) {
+        const int side = lane >= NFS ? 1 : 0, fs = lane - side * NFS, f = fs / NS, s = fs % NS;
+        const int fi = fin[f], bc = fi >> 3;
+        const bool wall = bc == BC_REFLECT, dz = bc == 1, ext0 = side == 1 && bc >= 1 && !wall;
+        const double* nh = S + SH::MNHAT + 2 * f;
+        const double len = S[SH::MNLEN + f], wsq = T.ws[s];
+        double ui[M] = {0.0, 0.0, 0.0, 0.0}, uo[M] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < NF; ++j)
+#pragma unroll
+          for (int c = 0; c < M; ++c) ui[c] = fma(T.trace[0][s][j], S[SH::UE + fnode_of(PD, f, j) * M + c], ui[c]);
+        if (bc == 0) {
+          const int sp = ((fi >> 2) & 1) ? NS - 1 - s : s;
+#pragma unroll
+          for (int j = 0; j < NF; ++j)
+#pragma unroll
+            for (int c = 0; c < M; ++c) uo[c] = fma(T.trace[0][sp][j], S[SH::UNF + (f * NF + j) * M + c], uo[c]);
+        } else if (bc == 1) {
+#pragma unroll
+          for (int c = 0; c < M; ++c) uo[c] = ui[c];
+        } else if (wall) {
+          reflect_state(ui, nh, uo);
+        } else {
+          LAW::ghost(bc - 2, la, uo);
+        }
+        if (!dz) {
+          // dD/du_side in two passes of two seeded components each (Dn<2>: fewer live values)
+          double Dv[M];
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            Dn<2> ua[M], ub[M], nd[2];
+#pragma unroll
+            for (int c = 0; c < M; ++c) {
+              const bool seeded = (c >> 1) == half;
+              ua[c] = (side == 0 && seeded) ? seed<2>(ui[c], c & 1) : cst<2>(ui[c]);
+              ub[c] = (side == 1 && seeded) ? seed<2>(uo[c], c & 1) : cst<2>(uo[c]);
+            }
+            nd[0] = cst<2>(nh[0]);
+            nd[1] = cst<2>(nh[1]);
+            Dn<2> Dd[M];
+            roe_diss(ua, ub, nd, la.p[0], la.p[1], Dd);
+#pragma unroll
+            for (int c = 0; c < M; ++c) Dv[c] = Dd[c].v;
+            if (!ext0)
+#pragma unroll
+              for (int c = 0; c < M; ++c)
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+                  RA[SH::CF + side * SH::CFS + (c * M + 2 * half + k) * NFSP + fs] -= 0.5 * wsq * len * Dd[c].d[k];
+          }
+          if (side == 0) {
+#pragma unroll
+            for (int c = 0; c < M; ++c) {
+              RA[SH::HS + c * NFSP + fs] -= wsq * 0.5 * len * Dv[c];
+              RA[SH::FX + (2 * M + c) * NFSP + fs] = 0.5 * wsq * Dv[c];  // the FD stage's "du" slot carries D
+            }
+            // D's own normal dependence: -wsq len / 2 (dD/dnh . dnh) per unit normal perturbation,
+            // pre-written into the FD slots (the FD stage adds the flux and |nu| terms)
+            Dn<2> ua2[M], ub2[M], nd2[2];
+#pragma unroll
+            for (int c = 0; c < M; ++c) { ua2[c] = cst<2>(ui[c]); ub2[c] = cst<2>(uo[c]); }
+            nd2[0] = seed<2>(nh[0], 0);
+            nd2[1] = seed<2>(nh[1], 1);
+            Dn<2> Dn2[M];
+            roe_diss(ua2, ub2, nd2, la.p[0], la.p[1], Dn2);
+            const double il = 1.0 / len;
+#pragma unroll
+            for (int dir = 0; dir < 2; ++dir) {
+              const double dlen = nh[dir];
+              const double dn0 = ((dir == 0 ? 1.0 : 0.0) - nh[0] * dlen) * il, dn1 = ((dir == 1 ? 1.0 : 0.0) - nh[1] * dlen) * il;
+#pragma unroll
+              for (int c = 0; c < M; ++c)
+                S[SH::FD + (c * 2 + dir) * NFSP + fs] = -0.5 * wsq * len * (Dn2[c].d[0] * dn0 + Dn2[c].d[1] * dn1);
+            }
+          }
+        } else if (side == 0) {  // extrapolated exterior: D == 0 identically
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            RA[SH::FX + (2 * M + c) * NFSP + fs] = 0.0;
+            S[SH::FD + (c * 2 + 0) * NFSP + fs] = 0.0;
+            S[SH::FD + (c * 2 + 1) * NFSP + fs] = 0.0;
+          }
+        }
+      }
+      __syncwarp();
+    }
     // ---- slip walls: fold the exterior block into C_in through u_g = R(nh) u_in, and the
     // ghost's normal dependence into the FD slots (warp-uniform: elements without walls skip)
     if (LAW::WALLS && ((fin[0] >> 3) == BC_REFLECT || (fin[1] >> 3) == BC_REFLECT || (fin[2] >> 3) == BC_REFLECT)) {
