@@ -108,3 +108,27 @@ def test_gpu_lm_backtrack_budget_matches_oracle(max_backtracks):
         assert r.reason == want.reason and r.n_iters == want.n_iters
         assert len(r.history) == len(want.history)
         assert np.allclose(r.history[:, [0, 4, 5]], want.history[:, [0, 4, 5]], rtol=1e-8, equal_nan=True)
+
+
+def test_gpu_lm_graph_reuse_is_deterministic():
+    """The cached LM graph gives bit-identical results on reuse, after a shape change forces a
+    rebuild, and after the bases change (epoch) — and the statistics come back."""
+    import ctypes
+
+    from paper_2305_15661_b200 import _lib
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.lm import LmConfig, lm_solve_batched
+
+    case, g = build("sector")
+    op = gpu_op(case)
+    rho = WeightVector(case.rho)
+    cfg = LmConfig(max_iters=10)
+    a = lm_solve_batched(op, case.mus, case.W[0], None, rho, cfg)
+    b = lm_solve_batched(op, case.mus, case.W[0], None, rho, cfg)  # graph reused
+    lm_solve_batched(op, case.mus[:1], case.W[0], None, rho, cfg)  # different P: rebuilt
+    c = lm_solve_batched(op, case.mus, case.W[0], None, rho, cfg)  # rebuilt again
+    for x, y, z in zip(a, b, c):
+        assert np.array_equal(x.w, y.w) and np.array_equal(x.w, z.w) and x.n_iters == y.n_iters == z.n_iters
+    st = (ctypes.c_int32 * 3)()
+    _lib.check(_lib.load().strom_lm_stats(op._h, st), "strom_lm_stats")
+    assert st[0] > 0 and st[1] > 0 and st[2] > 0
