@@ -2,7 +2,9 @@
 
 Follows, line by line in meaning (not in text):
   * per-element tabulations        strom/geometry.py:40-139
-  * element_eval                   strom/dg.py:82-181
+  * element_eval                   strom/dg.py:82-181 (incl. the richer test space, dg.py:92-102)
+  * Geometry.test_space            strom/geometry.py:162-196
+  * assemble_enriched              strom/dg.py:275-326
   * seed_elemental / elemental_residual  strom/dg.py:184-225
   * assemble_global (value path)   strom/dg.py:228-240
   * distortion_integral/_eval      strom/distortion.py:33-68
@@ -80,6 +82,24 @@ class OracleGeometry:
         self.phi_opp = opp[np.where(nbr >= 0, nface, 0), flip.astype(np.int64)]
         self.extras = {}
 
+    def test_space(self, degree):
+        """Tabulations of a richer nodal test space (strom/geometry.py:162-196): weighted
+        reference gradients (ne, nq, n_t, 2), weighted values, weighted face traces."""
+        key = ("test_space", degree)
+        if key not in self.extras:
+            vr, fr = triangle_rule(self.quad_order), interval_rule(self.quad_order)
+            phi_t, dphi_t = lagrange_basis(degree, vr.points)
+            det = self.det_ref
+            wdphi0 = np.einsum("qnk,ekj->eqnj", dphi_t, self.inv_jac_ref) * (self.wq[None, :, None, None] * det[:, None, None, None])
+            wphi = phi_t[None] * (self.wq[None, :, None] * det[:, None, None])
+            verts = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]])
+            s = fr.points
+            face = np.stack([lagrange_basis(degree, (1.0 - s)[:, None] * verts[a] + s[:, None] * verts[b])[0]
+                             for a, b in LOCAL_EDGES])
+            wphi_face = self.ws[None, None, :, None] * self.face_length[:, :, None, None] * face[None]
+            self.extras[key] = EnrichedTabs(degree, phi_t.shape[1], wdphi0, wphi, wphi_face)
+        return self.extras[key]
+
     def gather_state(self, U, els):
         nb, m = self.n_basis, self.n_comp
         U = np.asarray(U)
@@ -90,6 +110,15 @@ class OracleGeometry:
 
     def gather_coords(self, x, els):
         return np.asarray(x)[self.maps.coord_map[els]].reshape(len(els), self.n_geo, 2)
+
+
+@dataclass
+class EnrichedTabs:
+    degree: int
+    n_basis: int
+    wdphi0: np.ndarray
+    wphi: np.ndarray
+    wphi_face: np.ndarray
 
 
 def _det(G):
@@ -108,10 +137,13 @@ class KernelOut:
     res_face: object
 
 
-def element_eval(law, geom, els, Ue, Un, xe, mu, check_degenerate=True):
-    """Batched elemental DG residual (strom/dg.py:82-181)."""
+def element_eval(law, geom, els, Ue, Un, xe, mu, check_degenerate=True, test=None):
+    """Batched elemental DG residual (strom/dg.py:82-181); ``test`` swaps the test-side
+    tabulations for a richer nodal space, the trial side untouched (dg.py:92-102)."""
     els = np.asarray(els)
-    B, m, nb = len(els), geom.n_comp, geom.n_basis
+    B, m, nb = len(els), geom.n_comp, geom.n_basis if test is None else test.n_basis
+    wdphi0, wphi, wphi_face = (geom.wdphi0, geom.wphi, geom.wphi_face) if test is None else (
+        test.wdphi0, test.wphi, test.wphi_face)
     bad = set()
     # volume (dg.py:105-125)
     Jx = D.einsum("qgj,bgi->bqij", geom.gdphi, xe)
@@ -126,7 +158,7 @@ def element_eval(law, geom, els, Ue, Un, xe, mu, check_degenerate=True):
     f = law.flux(u, None, mu)
     F = D.einsum("bqci,bqji->bqcj", f, adj)
     S = D.expand(g, 1) * law.source(pos, u, None, mu)
-    res_vol = -(D.einsum("bqnj,bqcj->bnc", geom.wdphi0[els], F) + D.einsum("bqn,bqc->bnc", geom.wphi[els], S))
+    res_vol = -(D.einsum("bqnj,bqcj->bnc", wdphi0[els], F) + D.einsum("bqn,bqc->bnc", wphi[els], S))
     # faces (dg.py:127-175)
     tag_name = {tid: name for name, tid in geom.mesh.boundary_tags.items()}
     res_face = None
@@ -186,13 +218,27 @@ def element_eval(law, geom, els, Ue, Un, xe, mu, check_degenerate=True):
                     ws_out[wall] = ws_in[wall]
             lam = D.maximum(ws_in, ws_out)
             H = 0.5 * fn - 0.5 * D.expand(lam * sigma, 1) * (u_out - u_in)
-        c = D.einsum("bsn,bsc->bnc", geom.wphi_face[els, fi], H)
+        c = D.einsum("bsn,bsc->bnc", wphi_face[els, fi], H)
         res_face = c if res_face is None else res_face + c
     if bad:
         raise DegenerateMappingError(sorted(bad))
     res_vol = D.reshape(res_vol, (B, nb * m))
     res_face = D.reshape(res_face, (B, nb * m))
     return KernelOut(res_vol + res_face, res_vol, res_face)
+
+
+def enriched_blocks(law, geom, U, x, mu, test_degree=None):
+    """Enriched residual rows and their element tangent blocks [U_e | U_nbr | x_e] over every
+    element: the quantities strom/dg.py:275-326 scatters (res (ne, n_t m), tan (ne, n_t m, T))."""
+    test = geom.test_space(geom.maps.degree_sol + 1 if test_degree is None else test_degree)
+    els = np.arange(geom.mesh.num_elements)
+    Ue, Un = geom.gather_state(U, els)
+    xe = geom.gather_coords(x, els)
+    nu = geom.n_basis * geom.n_comp
+    T = 4 * nu + 2 * geom.n_geo
+    out = element_eval(law, geom, els, D.seed_identity(Ue, 0, T), D.seed_identity(Un, nu, T),
+                       D.seed_identity(xe, 4 * nu, T), mu, test=test)
+    return out.res.val, out.res.tan
 
 
 def reflect_state(u, nhat):

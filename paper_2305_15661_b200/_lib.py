@@ -6,7 +6,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("STROM_SO") or os.path.join(HERE, "_strom_b200.so")
 
-OBJECTIVE, DERIVS, CONTRIB, CONTRIB_SPLIT, RESIDUAL, RESNORM2, CONTRIB_LPROWS, ELEMJAC = range(8)
+OBJECTIVE, DERIVS, CONTRIB, CONTRIB_SPLIT, RESIDUAL, RESNORM2, CONTRIB_LPROWS, ELEMJAC, ELEMJAC_ENRICHED = range(9)
 
 
 class MeshDesc(C.Structure):
@@ -28,7 +28,7 @@ class DistDesc(C.Structure):
     _fields_ = [("kappa", C.c_double), ("eps", C.c_double)]
 
 
-EXPORTS = ("strom_create", "strom_set_bases", "strom_set_offsets", "strom_reserve", "strom_eval", "strom_eval_host",
+EXPORTS = ("strom_create", "strom_set_bases", "strom_set_offsets", "strom_set_test_space", "strom_reserve", "strom_eval", "strom_eval_host",
            "strom_degenerate_elements",
            "strom_lm_solve", "strom_lm_stats", "strom_profile", "strom_profile_ms", "strom_last_error", "strom_destroy")
 
@@ -52,6 +52,7 @@ def load(path=SO_PATH):
                                  C.POINTER(DistDesc), C.c_int, C.POINTER(vp)]
     lib.strom_set_bases.argtypes = [vp, vp, i32, vp, i32, vp, vp]
     lib.strom_reserve.argtypes = [vp, i32, i32]
+    lib.strom_set_test_space.argtypes = [vp, i32, vp, vp]
     lib.strom_set_offsets.argtypes = [vp, vp, C.c_int64, vp, C.c_int64]
     lib.strom_eval.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp, i32]
     lib.strom_eval_host.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, i32, vp, C.c_int64, vp, vp]

@@ -159,6 +159,20 @@ extern "C" int strom_set_offsets(strom_handle* h, const double* state_offset, in
   return 0;
 }
 
+extern "C" int strom_set_test_space(strom_handle* h, int32_t nbt, const double* dphi, const double* trace) {
+  if (!h) return fail(-1, "null handle");
+  if (nbt < 1 || nbt > 64 || !dphi || !trace) return fail(-1, "strom_set_test_space: bad arguments");
+  CK(cudaSetDevice(h->device));
+  if (h->test_tab) cudaFree(h->test_tab);
+  h->test_tab = nullptr;
+  const size_t nd = (size_t)h->nq * nbt * 2, nt = (size_t)3 * h->ns * nbt;
+  CK(cudaMalloc(&h->test_tab, (nd + nt) * sizeof(double)));
+  CK(cudaMemcpy(h->test_tab, dphi, nd * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->test_tab + nd, trace, nt * sizeof(double), cudaMemcpyHostToDevice));
+  h->test_nb = nbt;
+  return 0;
+}
+
 extern "C" int strom_reserve(strom_handle* h, int32_t max_P, int32_t max_active) {
   if (!h) return fail(-1, "null handle");
   const int K = h->ku + h->kx, KP = std::max(8, (K + 7) / 8 * 8);
@@ -194,15 +208,17 @@ extern "C" int strom_eval(strom_handle* h, int32_t mode, const double* w, const 
                           int32_t P, const int32_t* active, const double* rho, int32_t A, double* out,
                           int32_t* degen, void* stream, int32_t sync) {
   if (!h) return fail(-1, "null handle");
-  if (mode < 0 || mode > MODE_ELEMJAC) return fail(-1, "bad mode");
-  if (mode == MODE_ELEMJAC && (h->law.n_comp != 4 || h->p != 2 || P != 1))
+  if (mode < 0 || mode > MODE_ELEMJAC_ENRICHED) return fail(-1, "bad mode");
+  const bool ejmode = mode == MODE_ELEMJAC || mode == MODE_ELEMJAC_ENRICHED;
+  if (ejmode && (h->law.n_comp != 4 || h->p != 2 || P != 1))
     return fail(-1, "element Jacobians: 4-component laws with p = 2, one parameter point");
+  if (mode == MODE_ELEMJAC_ENRICHED && !h->test_tab) return fail(-1, "enriched element Jacobians: test space not set");
   if (P < 1) return fail(-1, "P must be >= 1");
   if (!out) return fail(-1, "null output");
   if (!h->xref) return fail(-1, "bases not set");
   if ((h->ku && !w) || (h->kx && !tau) || (h->law.n_mu && !mu)) return fail(-1, "null coordinates");
   if (active && (!rho || A < 0)) return fail(-1, "active set needs weights");
-  if (active && (mode == MODE_CONTRIB || mode == MODE_CONTRIB_SPLIT || mode == MODE_CONTRIB_LPROWS || mode == MODE_ELEMJAC))
+  if (active && (mode == MODE_CONTRIB || mode == MODE_CONTRIB_SPLIT || mode == MODE_CONTRIB_LPROWS || ejmode))
     return fail(-1, "element contributions are evaluated over all elements");
   cudaStream_t st = (cudaStream_t)stream;
   if (!degen) {
@@ -279,6 +295,7 @@ extern "C" void strom_destroy(strom_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->eta_ref) cudaFree(h->eta_ref);
+  if (h->test_tab) cudaFree(h->test_tab);
   if (h->part) cudaFree(h->part);
   if (h->degen_list) cudaFree(h->degen_list);
   if (h->degen_fill) cudaFree(h->degen_fill);

@@ -143,7 +143,11 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   const bool DERIVS = DM >= 0 ? DM == 1 : r.mode == MODE_DERIVS;  // compile-time on the specialised path
   // element Jacobian blocks (full-space assembly, dg.py:197-272; generic instantiation only):
   // out[e] = [res (NU) | dR/dU_e (NU x NU) | dR/dU_nbr (NU x 3 NU) | dR/dx_e (NU x 6) | N_e | dN_e/dx_e (6)]
-  const bool EJ = DM < 0 && r.mode == MODE_ELEMJAC;
+  const bool EJ = DM < 0 && (r.mode == MODE_ELEMJAC || r.mode == MODE_ELEMJAC_ENRICHED);
+  // enriched test space (dg.py:275-326): the same pointwise records contracted with the
+  // degree p+1 test tabulations, out[e] = [res (NT) | dR/dU_e (NT x NU) | dR/dU_nbr (NT x 3 NU) |
+  // dR/dx_e (NT x 6) | N_e | dN_e/dx_e (6)], NT = n_test * M
+  const bool EJT = EJ && r.mode == MODE_ELEMJAC_ENRICHED;
   constexpr int EJ_SELF = 24, EJ_NBR = EJ_SELF + 24 * 24, EJ_X = EJ_NBR + 24 * 72, EJ_D = EJ_X + 24 * 6,
                 EJ_SZ = EJ_D + 7;
   constexpr int KT = KUT + KXT, KPT = (KT + 7) / 8 * 8;
@@ -720,6 +724,87 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
               pre + FXp[(2 * c) * NFSP] * dnu0 + FXp[(2 * c + 1) * NFSP] * dnu1 - FXp[(2 * M + c) * NFSP] * coef;
         }
       }
+    }
+    if (EJT) {
+      __syncwarp();  // FD slots written above
+      const int NBT = r.test_nb, NT = NBT * M;
+      const double* __restrict__ tdphi = r.test_tab;              // [NQ][NBT][2]
+      const double* __restrict__ ttr = r.test_tab + NQ * NBT * 2;  // [3][NS][NBT]
+      double* const eo = r.out + (size_t)e * (NT * (1 + 4 * NU + 6) + 7);
+      const double* adj = S + SH::MADJ;
+      for (int i = lane; i < NT; i += 32) {  // residual row (n, c) and its six mesh derivatives
+        const int n = i / M, c = i % M;
+        double t00 = 0.0, t01 = 0.0, t10 = 0.0, t11 = 0.0;  // t[j][k] = sum_q dphi_t[q][n][j] w_q f[c][k]
+        for (int q = 0; q < NQ; ++q) {
+          const double d0 = tdphi[(q * NBT + n) * 2], d1 = tdphi[(q * NBT + n) * 2 + 1];
+          const double f0 = RA[SH::FQ + (c * 2 + 0) * SH::NQC + q], f1 = RA[SH::FQ + (c * 2 + 1) * SH::NQC + q];
+          t00 = fma(d0, f0, t00); t01 = fma(d0, f1, t01); t10 = fma(d1, f0, t10); t11 = fma(d1, f1, t11);
+        }
+        const double rv = -((adj[0] * t00 + adj[1] * t01) + (adj[2] * t10 + adj[3] * t11));
+        double dr[6];
+#pragma unroll
+        for (int d = 0; d < 6; ++d) {
+          const int gv = d >> 1, ic = d & 1;
+          const double c0 = (gv == 1) - (gv == 0), c1 = (gv == 2) - (gv == 0);
+          dr[d] = ic == 0 ? (c1 * t01 - c0 * t11) : -(c1 * t00 - c0 * t10);
+        }
+        double rf = 0.0;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          double rx = 0.0, ry = 0.0;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const double tr = ttr[(f * NS + s) * NBT + n];
+            rf = fma(tr, RA[SH::HS + c * NFSP + f * NS + s], rf);
+            rx = fma(tr, S[SH::FD + (c * 2 + 0) * NFSP + f * NS + s], rx);
+            ry = fma(tr, S[SH::FD + (c * 2 + 1) * NFSP + f * NS + s], ry);
+          }
+          const int a = f, b = (f + 1) % 3;
+          dr[2 * b + 1] += rx;  dr[2 * a + 1] -= rx;
+          dr[2 * b + 0] -= ry;  dr[2 * a + 0] += ry;
+        }
+        eo[i] = rv + rf;
+#pragma unroll
+        for (int d = 0; d < 6; ++d) eo[(size_t)NT * (1 + 4 * NU) + i * 6 + d] = dr[d];
+      }
+      for (int i = lane; i < NT * NU; i += 32) {  // dR/dU_e
+        const int row = i / NU, col = i % NU, n = row / M, c = row % M, np_ = col / M, cp = col % M;
+        double v = 0.0;
+        for (int q = 0; q < NQ; ++q) {
+          const double a = fma(tdphi[(q * NBT + n) * 2], RA[SH::BQ + (cp * M + c) * SH::NQC + q],
+                               tdphi[(q * NBT + n) * 2 + 1] * RA[SH::BQ + SH::BQS + (cp * M + c) * SH::NQC + q]);
+          v = fma(-a, T.phi[q][np_], v);
+        }
+        for (int f = 0; f < 3; ++f) {
+          const int jp = face_local(f, np_);
+          if (jp < 0) continue;
+          for (int s = 0; s < NS; ++s)
+            v = fma(ttr[(f * NS + s) * NBT + n] * T.trace[0][s][jp], RA[SH::CF + (c * M + cp) * NFSP + f * NS + s], v);
+        }
+        eo[NT + i] = v;
+      }
+      for (int i = lane; i < NT * 3 * NU; i += 32) {  // dR/dU_nbr: the neighbor's face-node columns
+        const int row = i / (3 * NU), col = i % (3 * NU), n = row / M, c = row % M;
+        const int f = col / NU, node = (col % NU) / M, cp = col % M;
+        const int fi = EI[7 + f];
+        double v = 0.0;
+        if ((fi >> 3) == 0) {
+          const int nf = fi & 3;
+          const int jn = node == nf ? 0 : (node == (nf + 1) % 3 ? 1 : (node == 3 + nf ? 2 : -1));
+          if (jn >= 0)
+            for (int s = 0; s < NS; ++s) {
+              const int sp = ((fi >> 2) & 1) ? NS - 1 - s : s;
+              v = fma(ttr[(f * NS + s) * NBT + n] * T.trace[0][sp][jn],
+                      RA[SH::CF + SH::CFS + (c * M + cp) * NFSP + f * NS + s], v);
+            }
+        }
+        eo[NT + NT * NU + i] = v;
+      }
+      if (lane < 7) eo[(size_t)NT * (1 + 4 * NU + 6) + lane] = lane == 0 ? S[SH::MN] : S[SH::DNX + lane - 1];
+      __syncwarp();
+      if (nidx < nunits && lane < 10) EI[lane] = index_word(nact, lane);
+      __syncwarp();
+      continue;
     }
     // (no barrier: the L stage reads only BQ / CF; TQ / FD / R rows are read after later barriers)
     // next unit's index block: loaded here, stored to smem after the Jx stage

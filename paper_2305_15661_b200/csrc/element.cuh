@@ -13,7 +13,8 @@ constexpr int DERIV_THREADS = 128;
 
 enum Mode {
   MODE_OBJECTIVE = 0, MODE_DERIVS = 1, MODE_CONTRIB = 2, MODE_CONTRIB_SPLIT = 3,
-  MODE_RESIDUAL = 4, MODE_RESNORM2 = 5, MODE_CONTRIB_LPROWS = 6, MODE_ELEMJAC = 7
+  MODE_RESIDUAL = 4, MODE_RESNORM2 = 5, MODE_CONTRIB_LPROWS = 6, MODE_ELEMJAC = 7,
+  MODE_ELEMJAC_ENRICHED = 8
 };
 
 // reference-element constants; lives in the kernel parameter (constant) bank
@@ -72,6 +73,10 @@ struct Run {
   int gx;         // blocks per parameter
   int unit_stride;  // doubles per unit in shared memory
   int gx_warp_stride;  // doubles per warp in shared memory (warp kernel)
+  // enriched test space (MODE_ELEMJAC_ENRICHED): [NQ][nbt][2] reference gradients, then
+  // [3][NS][nbt] face traces of the degree p+1 nodal basis (geometry.py:162-196)
+  const double* __restrict__ test_tab;
+  int test_nb;
   double kappa, eps;
   double lawp[8];
 };

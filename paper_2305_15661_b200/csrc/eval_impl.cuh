@@ -141,6 +141,9 @@ static int launch_mma_t(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>&
 template <class LAW, int NQ>
 static int launch_mma(strom_handle* h, const EvalArgs& a, Params<6, NQ, 4, 3>& prm, int nunits) {
   // compile-time reduced dimensions for the BASELINE configs (addressing folds to immediates)
+  // element-Jacobian records come from the generic instantiation (the specialised ones carry
+  // only the projected modes)
+  if (a.mode == MODE_ELEMJAC || a.mode == MODE_ELEMJAC_ENRICHED) return launch_mma_t<LAW, NQ, 0, 0>(h, a, prm, nunits);
   if (h->ku == 16 && h->kx == 8) return launch_mma_t<LAW, NQ, 16, 8>(h, a, prm, nunits);
   if (h->ku == 20 && h->kx == 10) return launch_mma_t<LAW, NQ, 20, 10>(h, a, prm, nunits);
   if (h->ku == 24 && h->kx == 12) return launch_mma_t<LAW, NQ, 24, 12>(h, a, prm, nunits);
@@ -169,6 +172,7 @@ static int eval_impl(strom_handle* h, const EvalArgs& a) {
   r.mode = a.mode;
   r.mask = a.mask;
   r.kappa = h->kappa; r.eps = h->eps;
+  if (a.mode == MODE_ELEMJAC_ENRICHED) { r.test_tab = h->test_tab; r.test_nb = h->test_nb; }
   for (int i = 0; i < 8; ++i) r.lawp[i] = h->law.params[i];
   const int nunits = a.active ? a.A : h->ne;
   if (nunits == 0) {

@@ -77,6 +77,8 @@ struct strom_handle {
   int degen_scratch_cap = 0;
   std::vector<std::vector<int>> last_degen;
   int num_sms = 148;
+  double* test_tab = nullptr;  // enriched test-space tabulation (device, owned), strom_set_test_space
+  int test_nb = 0;
   bool has_wall = false;  // slip-wall faces (BC_REFLECT) in the mesh
   double* stage_h = nullptr;  // pinned staging of strom_eval_host
   double* stage_d = nullptr;  // its device twin

@@ -6,8 +6,10 @@ The element blocks — residual, dR_e/dU_e, dR_e/dU_nbr and dR_e/dx_e, i.e. what
 ``elemental_residual(..., want_jacobians=True)`` returns (dg.py:197-225) — come from the K1
 element kernel in its STROM_ELEMJAC mode (the same local Jacobians the reduced path projects,
 written out instead of projected); the scatter into CSR uses the reference's own index
-construction.  4-component laws (Euler) with p = 2; other laws raise.  The enriched test
-space (``assemble_enriched``) and full-space tracking are not built.
+construction.  ``assemble_enriched`` (dg.py:275-326) tests the same weak form against the
+degree p+1 nodal space: K1's STROM_ELEMJAC_ENRICHED mode contracts its pointwise flux /
+Jacobian records with the test tabulations bound by ``strom_set_test_space``.  4-component
+laws (Euler) with p = 2; other laws raise.  Full-space tracking on top: ``tracking.py``.
 """
 
 import numpy as np
@@ -21,8 +23,24 @@ class _NoDistortion:
     kappa, eps = 1.0, 1e-8
 
 
-def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenerate=True):
-    """(ne, EJ_SIZE) STROM_ELEMJAC records at the global state U and coordinates x."""
+def test_space_tables(tabs, degree):
+    """Reference gradients (nq, n_test, 2) and face traces (3, ns, n_test) of the degree
+    ``degree`` nodal basis at the element tables' volume / face points (geometry.py:162-196)."""
+    from .tables import LOCAL_EDGES, lagrange_basis, triangle_rule
+
+    verts = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]])
+    _, dphi_t = lagrange_basis(degree, triangle_rule(tabs.quad_order).points)
+    s = np.asarray(tabs.s)
+    trace_t = np.stack([lagrange_basis(degree, (1.0 - s)[:, None] * verts[a] + s[:, None] * verts[b])[0]
+                        for a, b in LOCAL_EDGES])
+    return np.ascontiguousarray(dphi_t), np.ascontiguousarray(trace_t)
+
+
+def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenerate=True, test_degree=None,
+                     columns=None):
+    """(ne, EJ_SIZE) STROM_ELEMJAC records at the global state U and coordinates x; with
+    ``test_degree`` the STROM_ELEMJAC_ENRICHED records (ne, NT (1 + 24 + 72 + 6) + 7).
+    ``columns`` (slice) limits what is copied back to the host."""
     import torch
 
     mesh, maps = geom.mesh, geom.maps
@@ -35,7 +53,15 @@ def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenera
     W = torch.zeros((1, op.k_u), dtype=torch.float64, device=op.device)
     Tau = torch.zeros((1, 1), dtype=torch.float64, device=op.device)
     Mu = torch.as_tensor(op._mu(mu)[None]).to(op.device)
-    out, rc = op.eval_batched(_lib.ELEMJAC, W, Tau, Mu, None, sync=True)
+    mode, rec = _lib.ELEMJAC, EJ_SIZE
+    if test_degree is not None:
+        dphi_t, trace_t = test_space_tables(op.dm.tabs, test_degree)
+        nbt = dphi_t.shape[1]
+        _lib.check(op._lib.strom_set_test_space(op._h, nbt, dphi_t.ctypes.data, trace_t.ctypes.data),
+                   "strom_set_test_space")
+        mode, rec = _lib.ELEMJAC_ENRICHED, 4 * nbt * (1 + 24 + 72 + 6) + 7
+    out = torch.empty(mesh.num_elements * rec, dtype=torch.float64, device=op.device)
+    out, rc = op.eval_batched(mode, W, Tau, Mu, None, out=out, sync=True)
     if rc == 1 and raise_degenerate:  # g <= 0 somewhere: raised after the whole batch, as dg.py:177-178
         from .reduced import degenerate_error
 
@@ -43,7 +69,8 @@ def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenera
         ids = np.zeros(max(n, 1), dtype=np.int32)
         op._lib.strom_degenerate_elements(op._h, 0, ids.ctypes.data, n)
         raise degenerate_error(ids[:n].astype(np.int64))
-    return out.view(mesh.num_elements, EJ_SIZE).cpu().numpy()
+    out = out.view(mesh.num_elements, rec)
+    return (out if columns is None else out[:, columns].contiguous()).cpu().numpy()
 
 
 def element_jacobians(law, geom, U, x, mu, device=None):
@@ -88,7 +115,12 @@ def assemble_global(law, mesh, maps, U, x, mu, want_jacobians=True, geom=None, d
         return op.global_residual(ReducedCoords(np.zeros(0), np.zeros(0)), mu), None, None
     res, jac_self, jac_neigh, jac_coord = element_jacobians(law, geom, U, x, mu, device)
     R = res.reshape(-1)
-    rows = maps.state_map[:, :, None]
+    dRdU, dRdx = _scatter_csr(maps, maps.state_map[:, :, None], jac_self, jac_neigh, jac_coord, maps.n_global_state)
+    return R, dRdU, dRdx
+
+
+def _scatter_csr(maps, rows, jac_self, jac_neigh, jac_coord, n_rows):
+    """CSR dR/dU and dR/dx from element blocks (the index construction of dg.py:246-271)."""
     r1 = np.broadcast_to(rows, jac_self.shape).ravel()
     c1 = np.broadcast_to(maps.state_map[:, None, :], jac_self.shape).ravel()
     nmap = maps.neighbor_map
@@ -97,11 +129,53 @@ def assemble_global(law, mesh, maps, U, x, mu, want_jacobians=True, geom=None, d
     c2 = np.broadcast_to(np.clip(nmap, 0, None)[:, None, :], jac_neigh.shape).ravel()
     d2 = (jac_neigh * valid[:, None, :]).ravel()
     dRdU = sp.coo_matrix((np.concatenate([jac_self.ravel(), d2]), (np.concatenate([r1, r2]), np.concatenate([c1, c2]))),
-                         shape=(maps.n_global_state, maps.n_global_state)).tocsr()
+                         shape=(n_rows, maps.n_global_state)).tocsr()
     r3 = np.broadcast_to(rows, jac_coord.shape).ravel()
     c3 = np.broadcast_to(maps.coord_map[:, None, :], jac_coord.shape).ravel()
-    dRdx = sp.coo_matrix((jac_coord.ravel(), (r3, c3)), shape=(maps.n_global_state, maps.n_global_coord)).tocsr()
-    return R, dRdU, dRdx
+    dRdx = sp.coo_matrix((jac_coord.ravel(), (r3, c3)), shape=(n_rows, maps.n_global_coord)).tocsr()
+    return dRdU, dRdx
+
+
+def enriched_records(law, geom, U, x, mu, test_degree=None, dist=None, want_jacobians=True, device=None,
+                     raise_degenerate=True):
+    """Element blocks of the enriched residual in one K1 pass: (res (ne, NT), jac_self
+    (ne, NT, 24), jac_neigh (ne, NT, 72), jac_coord (ne, NT, 6), N (ne,), dN (ne, 6)); the
+    Jacobian blocks are None (and never copied back) when ``want_jacobians`` is false."""
+    from .tables import lagrange_nodes
+
+    maps = geom.maps
+    deg = maps.degree_sol + 1 if test_degree is None else test_degree
+    NT = lagrange_nodes(deg).shape[0] * maps.n_comp
+    rec = NT * (1 + 24 + 72 + 6)
+    if not want_jacobians:  # residual rows and the distortion scalar only
+        import torch  # noqa: F401
+
+        cols = np.r_[0:NT, rec:rec + 7]
+        o = _element_records(law, geom, U, x, mu, dist=dist, device=device, raise_degenerate=raise_degenerate,
+                             test_degree=deg, columns=cols)
+        return o[:, :NT], None, None, None, o[:, NT], o[:, NT + 1:]
+    o = _element_records(law, geom, U, x, mu, dist=dist, device=device, raise_degenerate=raise_degenerate,
+                         test_degree=deg)
+    a, b, c = NT, NT + NT * 24, NT + NT * 96
+    return (o[:, :a], o[:, a:b].reshape(-1, NT, 24), o[:, b:c].reshape(-1, NT, 72), o[:, c:rec].reshape(-1, NT, 6),
+            o[:, rec], o[:, rec + 1:rec + 7])
+
+
+def assemble_enriched(law, mesh, maps, U, x, mu, test_degree=None, want_jacobians=True, geom=None, device=None):
+    """Residual tested against the degree p+1 nodal space, with CSR dRbar/dU (ne n_t x N_u)
+    and dRbar/dx (ne n_t x N_x): strom/dg.py:275-326 (rows element-major)."""
+    from .mesh import get_geometry
+
+    geom = geom or get_geometry(mesh, maps)
+    res, js, jn, jc, _, _ = enriched_records(law, geom, U, x, mu, test_degree, want_jacobians=want_jacobians,
+                                             device=device)
+    Rbar = res.reshape(-1).copy()
+    if not want_jacobians:
+        return Rbar, None, None
+    ne, n_t = res.shape
+    rows = (np.arange(ne)[:, None] * n_t + np.arange(n_t)[None, :]).astype(np.int64)[:, :, None]
+    dRdU, dRdx = _scatter_csr(maps, rows, js, jn, jc, ne * n_t)
+    return Rbar, dRdU, dRdx
 
 
 class HdmSolveError(RuntimeError):

@@ -158,11 +158,167 @@ def lm_solve_batched(op, mus, W0=None, Tau0=None, rho=None, config=None, w0_mode
     return out
 
 
+# -- protocol path: any problem with (nw, ntau, initial_guess, objective, derivatives) ----------
+# The full-space tracking / alignment problems (tracking.TrackingProblem) have sparse blocks
+# with thousands of unknowns; their residuals and Jacobians are assembled on the GPU, the
+# damped normal equations are factored on the host (SuperLU), as strom/lm.py:77-126 does.
+
+
+def _trial_objective(problem, w, tau):
+    from .reduced import DegenerateMappingError
+
+    try:
+        return problem.objective(w, tau)
+    except DegenerateMappingError:
+        return np.inf
+
+
+def _normal_step(H_ww, H_wt, H_tt, S, T, lam):
+    """(dw, dtau) of the normal equations damped on the deformation block only
+    (lm.py:77-126); numpy.linalg.LinAlgError when singular."""
+    import scipy.linalg
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+
+    nw, nt = len(S), len(T)
+    if nw + nt == 0:
+        return np.zeros(0), np.zeros(0)
+    rhs = -np.concatenate([S, T])
+    if any(sp.issparse(M) for M in (H_ww, H_wt, H_tt) if M is not None):
+        damped = None if nt == 0 else sp.csr_matrix(H_tt) + lam * sp.identity(nt, format="csr")
+        if nt == 0:
+            K = sp.csc_matrix(H_ww)
+        elif nw == 0:
+            K = damped.tocsc()
+        else:
+            C = sp.csr_matrix(H_wt)
+            K = sp.bmat([[sp.csr_matrix(H_ww), C], [C.T, damped]], format="csc")
+        try:
+            dz = spla.splu(K).solve(rhs)
+        except RuntimeError as exc:
+            raise np.linalg.LinAlgError(str(exc)) from exc
+    else:
+        if nt == 0:
+            K = np.atleast_2d(H_ww)
+        elif nw == 0:
+            K = np.atleast_2d(H_tt) + lam * np.eye(nt)
+        else:
+            C = np.atleast_2d(H_wt)
+            K = np.block([[np.atleast_2d(H_ww), C], [C.T, np.atleast_2d(H_tt) + lam * np.eye(nt)]])
+        dz = scipy.linalg.solve(K, rhs, assume_a="sym")
+    if not np.all(np.isfinite(dz)):
+        raise np.linalg.LinAlgError("singular regularized system")
+    return dz[:nw], dz[nw:]
+
+
+def _state_init_protocol(problem, w, tau, cfg):
+    """Gauss-Newton on the state block at frozen deformation (lm.py:129-161)."""
+    _, S, _, H_ww, _, _ = problem.derivatives(w, tau)
+    target = cfg.w0_inner_tol * max(1.0, np.linalg.norm(S))
+    J = None
+    for _ in range(cfg.w0_inner_iters):
+        if np.linalg.norm(S) <= target:
+            break
+        try:
+            dw, _ = _normal_step(H_ww, None, None, S, np.zeros(0), 0.0)
+        except (np.linalg.LinAlgError, RuntimeError):
+            break
+        J = problem.objective(w, tau) if J is None else J
+        sdw = float(S @ dw)
+        alpha, Jt = 1.0, np.inf
+        for _ in range(30):
+            Jt = _trial_objective(problem, w + alpha * dw, tau)
+            if Jt <= J + 1e-4 * alpha * sdw:
+                break
+            alpha *= 0.5
+        else:
+            break
+        w, J = w + alpha * dw, Jt
+        _, S, _, H_ww, _, _ = problem.derivatives(w, tau)
+    return w
+
+
+def lm_solve_protocol(problem, config=None, w0_mode="lsq"):
+    """The reference LM (lm.py:164-271) over the problem protocol, host loop: lambda on the
+    deformation block, Armijo backtracking, gain-ratio + weak-Wolfe damping update, lambda
+    escalation on singular systems / failed searches, best-iterate fallback."""
+    import scipy.sparse as sp
+
+    cfg = as_config(config)
+    if w0_mode not in ("lsq", "keep"):
+        raise ValueError(f"unknown w0_mode {w0_mode!r}")
+    w, tau = (np.asarray(v, dtype=float).copy() for v in problem.initial_guess())
+    if w0_mode == "lsq" and len(w):
+        w = _state_init_protocol(problem, w, tau, cfg)
+    lam, lam_floor = cfg.lambda0, 0.0
+    rows, best, reason, n_done = [], None, "max-iters", 0
+    J, S, T, H_ww, H_wt, H_tt = problem.derivatives(w, tau)
+    for it in range(cfg.max_iters):
+        nS, nT = np.linalg.norm(S), np.linalg.norm(T)
+        if best is None or J < best[0]:
+            best = (J, w.copy(), tau.copy(), nS, nT)
+        if lam is None:  # lambda0 = 1e-4 trace(H_tt) / k_x
+            tr = (H_tt.diagonal().sum() if sp.issparse(H_tt) else np.trace(np.atleast_2d(H_tt))) if len(tau) else 0.0
+            lam = 1e-4 * tr / len(tau) if len(tau) else 0.0
+            lam_floor = 1e-10 * lam if lam > 0 else 0.0
+        if nS <= cfg.eps1 and nT <= cfg.eps2:
+            rows.append((it, J, nS, nT, lam, 0.0))
+            return LmResult(w, tau, True, J, nS, nT, it, np.array(rows), "first-order")
+        rows.append((it, J, nS, nT, lam, np.nan))
+        n_done = it + 1
+        step = None
+        for _ in range(60):  # lambda escalation until a descent step passes the Armijo test
+            grow = 4.0
+            try:
+                dw, dtau = _normal_step(H_ww, H_wt, H_tt, S, T, lam)
+                gdot = float(S @ dw + T @ dtau)
+                if np.isfinite(gdot) and gdot < 0.0:
+                    alpha = 1.0
+                    for _ in range(cfg.max_backtracks):
+                        Jt = _trial_objective(problem, w + alpha * dw, tau + alpha * dtau)
+                        if Jt <= J + cfg.wolfe_c1 * alpha * gdot:
+                            step = (dw, dtau, gdot, alpha, Jt)
+                            break
+                        alpha *= 0.5
+                if step is not None:
+                    break
+                lam = max(grow * lam, 1e-12)
+            except np.linalg.LinAlgError:
+                lam = max(2.0 * lam, 1e-12) * 10.0
+            if lam > cfg.lambda_cap:
+                break
+        if step is None:
+            reason = "line-search-failure"
+            break
+        dw, dtau, gdot, alpha, J_new = step
+        w, tau = w + alpha * dw, tau + alpha * dtau
+        pred = -0.5 * alpha * gdot
+        ratio = (J - J_new) / pred if pred > 0 else 1.0
+        J_prev = J
+        J, S, T, H_ww, H_wt, H_tt = problem.derivatives(w, tau)
+        J = J_new if np.isfinite(J_new) else J
+        curv_ok = float(S @ dw + T @ dtau) >= cfg.wolfe_c2 * gdot
+        if alpha < 0.25 or ratio < cfg.ratio_lo:
+            lam *= cfg.lambda_inc
+        elif alpha == 1.0 and ratio > cfg.ratio_hi and curv_ok:
+            lam *= cfg.lambda_dec
+        lam = min(max(lam, lam_floor), cfg.lambda_cap)
+        rows[-1] = (it, J_prev, rows[-1][2], rows[-1][3], lam, alpha)
+    nS, nT = np.linalg.norm(S), np.linalg.norm(T)
+    if best is not None and best[0] < J:
+        J, w, tau, nS, nT = best
+    return LmResult(w, tau, False, J, nS, nT, n_done, np.array(rows), reason)
+
+
 def lm_solve(problem, config=None, w0_mode="lsq"):
-    """Reference-signature LM solve (lm.py:164); the problem must wrap a GpuReducedOperator."""
+    """Reference-signature LM solve (lm.py:164).  A problem over a ``GpuReducedOperator`` runs
+    as the device-resident batched state machine; any other protocol problem (full-space
+    tracking, alignment: GPU-assembled sparse blocks) runs the host loop above."""
     op = getattr(problem, "op", None)
     if not isinstance(op, GpuReducedOperator):
-        raise NotImplementedError("lm_solve runs on the GPU operator only (no CPU fallback)")
+        if all(hasattr(problem, a) for a in ("initial_guess", "objective", "derivatives")):
+            return lm_solve_protocol(problem, config, w0_mode)
+        raise NotImplementedError("lm_solve needs a GpuReducedOperator problem or a protocol problem")
     w0, tau0 = problem.initial_guess()
     res = lm_solve_batched(op, [problem.mu], w0[None], tau0[None], problem.rho, config, w0_mode,
                            raise_degenerate=True)

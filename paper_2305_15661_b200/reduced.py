@@ -218,7 +218,9 @@ class GpuReducedOperator:
             _lib.CONTRIB: P * ne * K, _lib.CONTRIB_SPLIT: P * ne * 2 * K,
             _lib.RESIDUAL: P * ne * self.dm.nu, _lib.CONTRIB_LPROWS: P * (K + 1) * ne,
             _lib.ELEMJAC: P * ne * EJ_SIZE,
-        }[mode]
+        }.get(mode)
+        if size is None and out is None:
+            raise ValueError("this mode needs a caller-sized output tensor")
         if out is None:
             out = torch.empty(size, dtype=torch.float64, device=self.device)
         stream = torch.cuda.current_stream(self.device).cuda_stream

@@ -29,6 +29,10 @@ def build(name):
     elif name in ("euler_square_q6", "euler_square_default"):
         case = configs.euler_square_case(n=4, ku=16, kx=8, seed=12, quad_order=6 if name.endswith("q6") else None,
                                          per_component=False)
+    elif name.startswith("tracking"):
+        case = configs.euler_square_case(n=4, ku=16, kx=8, seed=61, quad_order=6 if name.endswith("q6") else None)
+        case.law = L.euler(tags={"left": "freestream", "bottom": "freestream", "right": "extrapolate",
+                                 "top": "extrapolate"})
     elif name == "sector":
         case = configs.sector_rom_case(n_radial=4, n_circ=6, ku=6, kx=4, frac_active=0.25, rho_scale=4.0, P=2, seed=13,
                                    wall="extrapolate")

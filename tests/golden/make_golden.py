@@ -263,6 +263,64 @@ def case_lprows():
     save("lprows", out)
 
 
+def case_tracking(quad_order, name, with_problem):
+    """Full-space assembly against the enriched (degree p+1) test space (dg.py:275-326) and the
+    full-space tracking / snapshot-alignment problems on top (tracking.py:41-150), from the
+    reference: residuals, element tangent blocks, products of the CSR Jacobians and of the
+    Gauss-Newton blocks with seeded vectors, and a short reference lm_solve history."""
+    from strom import tracking as strack
+
+    case = configs.euler_square_case(n=4, ku=16, kx=8, seed=61, quad_order=quad_order)
+    case.law = L.euler(tags={"left": "freestream", "bottom": "freestream", "right": "extrapolate", "top": "extrapolate"})
+    op, rm, rmaps, geom = operator(case)
+    rng = np.random.default_rng(161)
+    mu = case.mus[0]
+    U = case.state_offset + case.phi @ (rng.standard_normal(16) * 0.05)
+    x = case.ref_coords.copy()
+    out = inputs_of(case, np.zeros(16), np.zeros(8))
+    out.update(U=U, x=x)
+    Rb, JU, JX = sdg.assemble_enriched(case.law, rm, rmaps, U, x, mu)
+    v_u, v_x, u_r = rng.standard_normal(JU.shape[1]), rng.standard_normal(JX.shape[1]), rng.standard_normal(JU.shape[0])
+    out.update(enr_R=Rb, v_u=v_u, v_x=v_x, u_r=u_r, enr_JU_v=JU @ v_u, enr_JUt_u=JU.T @ u_r, enr_JX_v=JX @ v_x,
+               enr_JXt_u=JX.T @ u_r, enr_nnz=np.array([JU.nnz, JX.nnz]))
+    test = geom.test_space(rmaps.degree_sol + 1)
+    for e in (0, 9, 31):  # element tangent blocks [U_e | U_nbr | x_e] of the enriched rows
+        els = np.array([e])
+        Ue, Un = geom.gather_state(U, els)
+        xe = geom.gather_coords(x, els)
+        o = sdg.element_eval(case.law, geom, els, *sdg.seed_elemental(geom, Ue, Un, xe), mu, test=test)
+        out[f"enr_elem{e}_res"] = o.res.val[0]
+        out[f"enr_elem{e}_tan"] = o.res.tan[0]
+    if with_problem:
+        dist = sdist.DistortionConfig(case.kappa, case.eps)
+        X = rm.nodes.ravel()
+        for tag, enrich in (("fs", True), ("fsplain", False)):
+            prob = strack.TrackingProblem(case.law, rm, rmaps, mu, dist, U0=U, x0=x, enrich=enrich)
+            w0, z0 = prob.initial_guess()
+            J, S, T, Hww, Hwt, Htt = prob.derivatives(w0, z0)
+            a, b = rng.standard_normal(len(w0)), rng.standard_normal(len(z0))
+            out.update({f"{tag}_free": prob.free, f"{tag}_z0": z0, f"{tag}_obj": prob.objective(w0, z0), f"{tag}_J": J,
+                        f"{tag}_S": S, f"{tag}_T": T, f"{tag}_a": a, f"{tag}_b": b, f"{tag}_Hww_a": Hww @ a,
+                        f"{tag}_Hwt_b": Hwt @ b, f"{tag}_Htt_b": Htt @ b, f"{tag}_Htt_diag": Htt.diagonal()})
+        # snapshot alignment: a small state basis holding the state, full-dimensional deformation
+        B = np.linalg.qr(np.column_stack([U, case.phi[:, :3]]))[0]
+        wB = B.T @ U + rng.standard_normal(4) * 1e-3
+        prob = strack.TrackingProblem(case.law, rm, rmaps, mu, dist, state_basis=B, w0=wB, x0=x)
+        w0, z0 = prob.initial_guess()
+        J, S, T, Hww, Hwt, Htt = prob.derivatives(w0, z0)
+        b = rng.standard_normal(len(z0))
+        out.update(al_B=B, al_w0=w0, al_J=J, al_S=S, al_T=T, al_Hww=Hww, al_Hwt_b=Hwt @ b, al_Htt_b=Htt @ b, al_b=b)
+        res = slm.lm_solve(prob, slm.LmConfig(max_iters=4), w0_mode="keep")
+        out.update(al_lm_w=res.w, al_lm_tau=res.tau, al_lm_hist=res.history, al_lm_obj=res.objective,
+                   al_lm_reason=res.reason)
+        # full-space tracking: three LM iterations of the reference solver on the enriched objective
+        prob = strack.TrackingProblem(case.law, rm, rmaps, mu, dist, U0=U, x0=x)
+        res = slm.lm_solve(prob, slm.LmConfig(max_iters=3), w0_mode="keep")
+        out.update(fs_lm_w=res.w, fs_lm_tau=res.tau, fs_lm_hist=res.history, fs_lm_obj=res.objective,
+                   fs_lm_reason=res.reason)
+    save(name, out)
+
+
 if __name__ == "__main__":
     case_strip()
     case_euler_square(6, "euler_square_q6")
@@ -277,3 +335,5 @@ if __name__ == "__main__":
     case_sector_shape("sector_k30", 6, 12, 20, 10, 0.25, 4, 51, 30)
     case_sector_shape("sector_k36", 6, 12, 24, 12, 0.25, 3, 52, 15)
     case_lprows()
+    case_tracking(6, "tracking_q6", True)
+    case_tracking(None, "tracking_default", False)

@@ -1,0 +1,147 @@
+"""GPU enriched assembly (fullspace.assemble_enriched, dg.py:275-326) and the full-space
+tracking / snapshot-alignment problems (tracking.TrackingProblem, tracking.py:41-150) vs
+goldens from the unmodified reference (tests/golden/tracking_*.npz) and vs the pinned oracle."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle.dual  # noqa: F401
+from oracle.element import OracleGeometry, enriched_blocks
+
+from cases import build, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("name", ["tracking_q6", "tracking_default"])
+def test_assemble_enriched_matches_reference(name):
+    from paper_2305_15661_b200.fullspace import assemble_enriched, enriched_records
+
+    case, g = build(name)
+    mu = case.mus[0]
+    Rb, JU, JX = assemble_enriched(case.law, case.mesh, case.maps, g["U"], g["x"], mu, geom=case.geom)
+    ne = case.mesh.num_elements
+    assert Rb.shape == (ne * 40,) and JU.shape == (ne * 40, case.maps.n_global_state)
+    assert JX.shape == (ne * 40, case.maps.n_global_coord)
+    assert rel_err(Rb, g["enr_R"]) < TOL
+    assert rel_err(JU @ g["v_u"], g["enr_JU_v"]) < TOL and rel_err(JU.T @ g["u_r"], g["enr_JUt_u"]) < TOL
+    assert rel_err(JX @ g["v_x"], g["enr_JX_v"]) < TOL and rel_err(JX.T @ g["u_r"], g["enr_JXt_u"]) < TOL
+    assert [JU.nnz, JX.nnz] == g["enr_nnz"].tolist()
+    res, js, jn, jc, _, _ = enriched_records(case.law, case.geom, g["U"], g["x"], mu)
+    for e in (0, 9, 31):
+        tan = g[f"enr_elem{e}_tan"]
+        scale = np.max(np.abs(tan))
+        assert rel_err(res[e], g[f"enr_elem{e}_res"]) < TOL
+        assert rel_err(js[e], tan[:, :24], scale) < TOL
+        ok = np.repeat(case.maps.neighbor_map[e].reshape(3, 24)[:, 0] >= 0, 24)
+        assert rel_err(jn[e][:, ok], tan[:, 24:96][:, ok], scale) < TOL
+        assert rel_err(jc[e], tan[:, 96:], scale) < TOL
+    # value-only path: same residual, no Jacobians copied back
+    R2, a, b = assemble_enriched(case.law, case.mesh, case.maps, g["U"], g["x"], mu, want_jacobians=False,
+                                 geom=case.geom)
+    assert a is None and b is None and np.array_equal(R2, Rb)
+
+
+@pytest.mark.parametrize("flux,wall", [("llf", "slip"), ("roe", "slip"), ("roe", "extrapolate")])
+def test_enriched_blocks_match_oracle_roe_wall(flux, wall):
+    """The GPU-only extensions (Roe flux, slip wall) through the enriched contraction, against
+    the oracle's dual-number blocks on the half-cylinder sector."""
+    from paper_2305_15661_b200 import configs, laws as L
+    from paper_2305_15661_b200.fullspace import enriched_records
+
+    case = configs.sector_rom_case(n_radial=3, n_circ=5, ku=4, kx=2, frac_active=0.5, rho_scale=2.0, P=1, seed=71,
+                                   wall=wall)
+    law = L.euler(tags=configs.sector_bcs(wall), flux=flux)
+    rng = np.random.default_rng(72)
+    ne = case.mesh.num_elements
+    U = np.tile(L.euler_freestream(3.0), ne * 6) * (1.0 + 0.03 * rng.standard_normal(ne * 24))
+    x = case.ref_coords + 2e-3 * rng.standard_normal(case.ref_coords.size)
+    mu = np.array([3.0])
+    res, js, jn, jc, _, _ = enriched_records(law, case.geom, U, x, mu)
+    geom = OracleGeometry(case.mesh, case.maps, case.quad_order)
+    ores, otan = enriched_blocks(law, geom, U, x, mu)
+    scale = np.max(np.abs(otan))
+    assert rel_err(res, ores) < TOL
+    assert rel_err(js, otan[:, :, :24], scale) < TOL and rel_err(jc, otan[:, :, 96:], scale) < TOL
+    ok = np.repeat(case.maps.neighbor_map.reshape(ne, 3, 24)[:, :, 0] >= 0, 24, axis=1)
+    assert rel_err(jn * ok[:, None, :], otan[:, :, 24:96] * ok[:, None, :], scale) < TOL
+
+
+def _problem(case, g, kind):
+    from paper_2305_15661_b200.configs import DistortionConfig
+    from paper_2305_15661_b200.tracking import TrackingProblem
+
+    dist = DistortionConfig(case.kappa, case.eps)
+    kw = dict(geom=case.geom)
+    if kind == "al":
+        return TrackingProblem(case.law, case.mesh, case.maps, case.mus[0], dist, state_basis=g["al_B"],
+                               w0=g["al_w0"], x0=g["x"], **kw)
+    return TrackingProblem(case.law, case.mesh, case.maps, case.mus[0], dist, U0=g["U"], x0=g["x"],
+                           enrich=kind == "fs", **kw)
+
+
+@pytest.mark.parametrize("kind", ["fs", "fsplain"])
+def test_tracking_problem_matches_reference(kind):
+    case, g = build("tracking_q6")
+    prob = _problem(case, g, kind)
+    assert np.array_equal(prob.free, g[f"{kind}_free"])
+    w0, z0 = prob.initial_guess()
+    assert np.array_equal(z0, g[f"{kind}_z0"]) and prob.nw == g["U"].size and prob.ntau == len(prob.free)
+    assert rel_err(prob.objective(w0, z0), g[f"{kind}_obj"]) < TOL
+    J, S, T, Hww, Hwt, Htt = prob.derivatives(w0, z0)
+    a, b = g[f"{kind}_a"], g[f"{kind}_b"]
+    assert rel_err(J, g[f"{kind}_J"]) < TOL and rel_err(S, g[f"{kind}_S"]) < TOL and rel_err(T, g[f"{kind}_T"]) < TOL
+    assert rel_err(Hww @ a, g[f"{kind}_Hww_a"]) < TOL and rel_err(Hwt @ b, g[f"{kind}_Hwt_b"]) < TOL
+    assert rel_err(Htt @ b, g[f"{kind}_Htt_b"]) < TOL and rel_err(Htt.diagonal(), g[f"{kind}_Htt_diag"]) < TOL
+
+
+def test_alignment_problem_matches_reference():
+    case, g = build("tracking_q6")
+    prob = _problem(case, g, "al")
+    w0, z0 = prob.initial_guess()
+    J, S, T, Hww, Hwt, Htt = prob.derivatives(w0, z0)
+    assert rel_err(J, g["al_J"]) < TOL and rel_err(S, g["al_S"]) < TOL and rel_err(T, g["al_T"]) < TOL
+    assert rel_err(Hww, g["al_Hww"]) < TOL
+    assert rel_err(Hwt @ g["al_b"], g["al_Hwt_b"]) < TOL and rel_err(Htt @ g["al_b"], g["al_Htt_b"]) < TOL
+
+
+@pytest.mark.parametrize("kind,iters", [("fs", 3), ("al", 4)])
+def test_tracking_lm_histories_match_reference(kind, iters):
+    """lm.lm_solve (protocol path, GPU-assembled sparse blocks) reproduces the reference
+    lm_solve on the reference TrackingProblem: same step lengths and damping row for row."""
+    from paper_2305_15661_b200.lm import LmConfig, lm_solve
+
+    case, g = build("tracking_q6")
+    res = lm_solve(_problem(case, g, kind), LmConfig(max_iters=iters), w0_mode="keep")
+    hist, ref = res.history, g[f"{kind}_lm_hist"]
+    assert hist.shape == ref.shape and str(res.reason) == str(g[f"{kind}_lm_reason"])
+    assert np.array_equal(hist[:, 0], ref[:, 0]) and np.array_equal(hist[:, 5], ref[:, 5])  # iteration, alpha
+    assert rel_err(hist[:, 4], ref[:, 4]) < 1e-9  # lambda
+    assert rel_err(hist[:, 1], ref[:, 1]) < 1e-8 and rel_err(hist[:, 2:4], ref[:, 2:4]) < 1e-6
+    assert rel_err(res.objective, g[f"{kind}_lm_obj"]) < 1e-8
+    assert rel_err(res.w, g[f"{kind}_lm_w"]) < 1e-8
+    assert rel_err(res.tau, g[f"{kind}_lm_tau"], scale=max(np.max(np.abs(g[f"{kind}_lm_tau"])), 1e-3)) < 1e-6
+
+
+def test_reference_lm_runs_on_gpu_tracking_problem():
+    """Drop-in: the unmodified reference's lm_solve drives the GPU TrackingProblem (its protocol)
+    and lands on the same iterates as the reference problem did."""
+    try:
+        from oracle import strom_ref
+
+        S = strom_ref.load()
+    except ImportError:
+        pytest.skip("reference strom not installed")
+    case, g = build("tracking_q6")
+    res = S["lm"].lm_solve(_problem(case, g, "fs"), S["lm"].LmConfig(max_iters=3), w0_mode="keep")
+    assert np.array_equal(res.history[:, 5], g["fs_lm_hist"][:, 5])
+    assert rel_err(res.objective, g["fs_lm_obj"]) < 1e-8 and rel_err(res.w, g["fs_lm_w"]) < 1e-8

@@ -53,6 +53,30 @@ def test_oracle_matches_reference(name):
                 assert rel_err(mine, ref) < 1e-11, blk
 
 
+@pytest.mark.parametrize("name", ["tracking_q6", "tracking_default"])
+def test_oracle_enriched_matches_reference(name):
+    """The oracle's enriched (degree p+1 test space) element blocks vs the reference's
+    assemble_enriched (dg.py:275-326): residual, element tangents, CSR products."""
+    from oracle.element import enriched_blocks
+
+    case, g = build(name)
+    geom = OracleGeometry(case.mesh, case.maps, case.quad_order)
+    res, tan = enriched_blocks(case.law, geom, g["U"], g["x"], case.mus[0])
+    assert rel_err(res.reshape(-1), g["enr_R"]) < TOL
+    for e in (0, 9, 31):
+        assert rel_err(res[e], g[f"enr_elem{e}_res"]) < TOL
+        assert rel_err(tan[e], g[f"enr_elem{e}_tan"]) < 1e-11
+    # products of the assembled Jacobians with the stored vectors, from the element blocks
+    maps, (ne, nt) = case.maps, res.shape
+    Jv, Jx = np.zeros(ne * nt), np.zeros(ne * nt)
+    for e in range(ne):
+        ok = maps.neighbor_map[e] >= 0
+        rows = slice(e * nt, (e + 1) * nt)
+        Jv[rows] = tan[e][:, :24] @ g["v_u"][maps.state_map[e]] + tan[e][:, 24:96][:, ok] @ g["v_u"][maps.neighbor_map[e][ok]]
+        Jx[rows] = tan[e][:, 96:] @ g["v_x"][maps.coord_map[e]]
+    assert rel_err(Jv, g["enr_JU_v"]) < 1e-11 and rel_err(Jx, g["enr_JX_v"]) < 1e-11
+
+
 def test_oracle_degenerate_elements():
     case, g = build("degenerate")
     op, _ = oracle_op(case)
