@@ -150,15 +150,72 @@ class GreedyState:
         return len(self.selected)
 
 
+# -- full-space callbacks of Algorithm 1 on the GPU-assembled blocks ----------
+def tracking_alignment(law, geom, dist_config, lm_config=None, device=None):
+    """``align(bases, mu) -> x*``: SPEC snapshot_alignment (Eq. align0) — the alignment problem
+    over (w in R^j, sliding deformation) solved by ``lm.lm_solve`` on a
+    ``tracking.TrackingProblem`` with the current state basis; the state coefficients are
+    discarded.  A solve that fails or does not reduce the objective falls back to x = X with a
+    warning (the snapshot is then added unaligned)."""
+    import warnings
+
+    from .lm import LmConfig, lm_solve
+    from .reduced import DegenerateMappingError
+    from .tracking import TrackingProblem
+
+    def align(bases, mu, w0=None):
+        X = np.asarray(geom.mesh.nodes, dtype=float).ravel()
+        if w0 is None:  # the law's initial guess at mu projected on the state basis (w = 0 is no state)
+            from .fullspace import initial_state
+
+            w0 = bases.phi.T @ initial_state(law, geom.mesh, geom.maps, X, mu, geom)
+        try:
+            prob = TrackingProblem(law, geom.mesh, geom.maps, mu, dist_config, state_basis=bases.phi, w0=w0,
+                                   geom=geom, device=device)
+            j0 = prob.objective(*prob.initial_guess())
+            res = lm_solve(prob, lm_config or LmConfig(max_iters=20), w0_mode="lsq")
+        except (DegenerateMappingError, np.linalg.LinAlgError) as exc:
+            warnings.warn(f"snapshot alignment at mu={np.asarray(mu).tolist()} failed ({exc}); x = X")
+            return X
+        if not np.isfinite(res.objective) or res.objective > j0:
+            warnings.warn(f"snapshot alignment at mu={np.asarray(mu).tolist()} did not reduce the objective; x = X")
+            return X
+        return prob.coords_from(res.tau)
+
+    return align
+
+
+def tracking_snapshot(law, geom, dist_config, lm_config=None, track=True, hdm_tol=1e-10, device=None):
+    """``hdm_snapshot(mu, x_aligned) -> (U*, x*)``: the HDM solve on the aligned mesh
+    (``fullspace.solve_hdm``, dg.py:343-400) and, with ``track``, the full-space tracking solve
+    on the enriched residual from there (tracking.py:41-150; SPEC seed: Phi = I, Psi = I,
+    rho = 1), both on GPU-assembled residuals and sparse Jacobians."""
+    from .fullspace import solve_hdm
+    from .lm import LmConfig, lm_solve
+    from .tracking import TrackingProblem
+
+    def hdm_snapshot(mu, x_aligned, U_init=None):
+        mesh, maps = geom.mesh, geom.maps
+        U = solve_hdm(law, mesh, maps, x_aligned, mu, U_init=U_init, tol=hdm_tol, geom=geom, device=device)
+        if not track:
+            return U, np.asarray(x_aligned, dtype=float).copy()
+        prob = TrackingProblem(law, mesh, maps, mu, dist_config, U0=U, x0=x_aligned, geom=geom, device=device)
+        res = lm_solve(prob, lm_config or LmConfig(max_iters=20), w0_mode="keep")
+        return res.w, prob.coords_from(res.tau)
+
+    return hdm_snapshot
+
+
 def greedy_train(law, geom, cand_mus, hdm_snapshot, n_iter, dist_config, train_weights, lm_config=None, align=None,
                  rank=0, world=1, group=None, device=None):
     """Greedy training (Algorithm 1): seed, then per iteration greedy search (GPU, candidates
     sharded over ranks), snapshot alignment, HDM snapshot, basis growth by Gram-Schmidt and
     EQP weight retraining with the previous weights as the guess.
 
-    The full-space solves are callbacks — the HDM / tracking solves are outside this repo's
-    hot path: ``hdm_snapshot(mu, x_aligned) -> (U*, x*)`` and, optionally,
-    ``align(bases, mu) -> x_aligned`` (None: x = X, SPEC's no-alignment fallback).
+    The full-space solves are callbacks: ``hdm_snapshot(mu, x_aligned) -> (U*, x*)`` (None:
+    ``tracking_snapshot``, the GPU-assembled HDM + full-space tracking solve) and
+    ``align(bases, mu) -> x_aligned`` (None: x = X, SPEC's no-alignment fallback; "tracking":
+    ``tracking_alignment``, the alignment problem of Eq. align0).
     ``train_weights(bases, guess, selected_mus) -> WeightVector`` is the EQP LP (e.g. the
     reference's strom.eqp.train_weights with the GPU operator swapped in, dropin.install).
     Seed (SPEC): mu_1 nearest the candidate centroid, Phi_1 = U*(mu_1)/||U*||,
@@ -172,6 +229,12 @@ def greedy_train(law, geom, cand_mus, hdm_snapshot, n_iter, dist_config, train_w
 
     cand_mus = np.atleast_2d(np.asarray(cand_mus, dtype=float))
     X = np.asarray(geom.mesh.nodes, dtype=float).ravel()
+    if hdm_snapshot is None:
+        hdm_snapshot = tracking_snapshot(law, geom, dist_config, device=device)
+    if isinstance(align, str):
+        if align != "tracking":
+            raise ValueError(f"unknown alignment {align!r}")
+        align = tracking_alignment(law, geom, dist_config, device=device)
     i1 = seed_index(cand_mus)
     U1, _ = hdm_snapshot(cand_mus[i1], X)
     phi = gram_schmidt_append(np.zeros((len(U1), 0)), U1)

@@ -64,3 +64,42 @@ def test_greedy_train_bookkeeping():
     assert all(m["psi_grown"] for m in st.metrics[1:])
     with pytest.raises(CandidateSetExhausted):
         greedy_train(law, geom, cands[:2], hdm_snapshot, 3, dist, train, LmConfig(max_iters=3))
+
+
+def test_greedy_train_with_fullspace_callbacks():
+    """Algorithm 1 end to end on the GPU with the built-in full-space callbacks: HDM solves
+    (fullspace.solve_hdm) + full-space tracking for the snapshots, the alignment problem of
+    Eq. align0 (tracking.TrackingProblem with the current state basis) before each of them."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import warnings
+
+    from paper_2305_15661_b200 import configs, laws as L
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.fullspace import assemble_global
+    from paper_2305_15661_b200.greedy import greedy_train, tracking_alignment, tracking_snapshot
+    from paper_2305_15661_b200.lm import LmConfig
+    from paper_2305_15661_b200.mesh import build_box_mesh, get_geometry
+
+    mesh, maps = build_box_mesh(((0.0, 0.0), (1.0, 1.0)), 3, 3, degree_sol=2, n_comp=4)
+    law = L.euler(tags={"left": "freestream", "bottom": "freestream", "right": "extrapolate", "top": "extrapolate"})
+    geom, ne = get_geometry(mesh, maps, 6), mesh.num_elements
+    dist = configs.DistortionConfig(1e-3)
+    cands = np.array([[2.0], [2.5], [3.0], [3.5]])
+    train = lambda bases, guess, mus: WeightVector.ones(ne)  # noqa: E731
+    snap = tracking_snapshot(law, geom, dist, LmConfig(max_iters=3))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")  # uniform flow: the aligned mesh is X, Psi is not grown
+        st = greedy_train(law, geom, cands, snap, 2, dist, train, LmConfig(max_iters=4),
+                          align=tracking_alignment(law, geom, dist, LmConfig(max_iters=3)))
+    assert st.j == 2 and st.bases.phi.shape[1] == 2 and len(set(st.selected)) == 2
+    X = mesh.nodes.ravel()
+    for (U, x), i in zip(st.snapshots, st.selected):
+        # the snapshots solve the DG system on their meshes, and boundary nodes stay on the box
+        R = assemble_global(law, mesh, maps, U, x, cands[i], want_jacobians=False, geom=geom)[0]
+        assert np.linalg.norm(R) < 1e-8
+        assert np.allclose(U.reshape(-1, 4), L.euler_freestream(cands[i][0]), atol=1e-7)  # uniform freestream
+        d = (x - X).reshape(-1, 2)
+        on_v = (np.abs(mesh.nodes[:, 0]) < 1e-12) | (np.abs(mesh.nodes[:, 0] - 1.0) < 1e-12)
+        on_h = (np.abs(mesh.nodes[:, 1]) < 1e-12) | (np.abs(mesh.nodes[:, 1] - 1.0) < 1e-12)
+        assert np.max(np.abs(d[on_v, 0]), initial=0.0) <= 1e-12 and np.max(np.abs(d[on_h, 1]), initial=0.0) <= 1e-12
