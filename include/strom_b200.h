@@ -159,6 +159,11 @@ int strom_lm_solve(strom_handle* h, double* w, double* tau, const double* mu, in
  * batched passes), so these counts are read back once per solve batch. */
 int strom_lm_stats(strom_handle* h, int32_t* out3);
 
+/* Device-time breakdown of the last strom_lm_solve (ms, from %globaltimer stamps taken by
+ * the control kernel): out4 = (control rounds, pass time after rounds that ran only the
+ * derivatives pass, only the objective pass, both). */
+int strom_lm_timing(strom_handle* h, double* out4);
+
 /* Benchmark probe: while enabled, the dominant kernel of every strom_eval is
  * bracketed by CUDA events recorded on the call's stream (capacity 4096
  * launches).  strom_profile_ms synchronizes on the recorded events and

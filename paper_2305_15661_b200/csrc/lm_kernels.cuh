@@ -59,6 +59,10 @@ struct LmCtl {
   int nd, no;         // passes run (statistics)
   int overflow;       // max_rounds reached with unfinished solves
   int ticket;         // control blocks finished this round (the last one ends the round)
+  // device-side timing (globaltimer, ns): when block 0 of a control round starts / the round
+  // ends; the gaps between a round end and the next round's start are the batched passes
+  unsigned long long t_start, t_end;
+  unsigned long long ns_ctl, ns_d, ns_o, ns_do;  // control rounds; gaps after rounds that ran d only / o only / both
 };
 
 struct LmRun {
@@ -436,6 +440,18 @@ static __global__ void __launch_bounds__(LM_THREADS) lm_control_kernel(LmRun R, 
     while ((ii + 1) * (ii + 2) / 2 <= q) ++ii;
     s_tri[q] = (unsigned short)((ii << 8) | (q - ii * (ii + 1) / 2));
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    LmCtl& C = *R.ctl;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (C.round > 0) {
+      const unsigned long long gap = t - C.t_end;
+      if (C.ran_d && C.ran_o) C.ns_do += gap;
+      else if (C.ran_d) C.ns_d += gap;
+      else if (C.ran_o) C.ns_o += gap;
+    }
+    C.t_start = t;
+  }
   const int par = R.ctl->round & 1;
   int* const counters = R.ctl->cnt[par];
   if (blockIdx.x == 0 && threadIdx.x < 4) R.ctl->cnt[par ^ 1][threadIdx.x] = 0;  // next round's set
@@ -610,6 +626,12 @@ static __device__ void lm_round_end(const LmRun& R, cudaGraphConditionalHandle h
   C.ocount = nobj;
   C.round += 1;
   C.ticket = 0;
+  {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    C.ns_ctl += t - C.t_start;
+    C.t_end = t;
+  }
   const bool more = n_active > 0 && C.round < R.max_rounds;
   if (n_active > 0 && !more) C.overflow = 1;
   *R.degen_fill = 0;

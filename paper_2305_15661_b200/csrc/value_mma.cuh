@@ -35,6 +35,7 @@ constexpr int VM_THREADS = 128;
 #define VM_MINB (VM_USMEM ? 3 : 2)
 #endif
 constexpr int kVmUq = VM_UQ, kVmUs = VM_US;
+static_assert(VM_USMEM, "the coordinate reconstruction stages through the face rows of the warp tile");
 constexpr int VM_LDU = 40;  // tile row stride: == 8 mod 16 -> conflict-free double2 C-fragment stores
 constexpr int VM_LDW = 36;  // W row stride: == 4 mod 16 -> conflict-free B-fragment loads
 
@@ -51,10 +52,11 @@ struct VShape {
 // rows r < nrows of the warp tile <- U0 + Phi[row(r)] . W  for the CTA's 32 points,
 // NTB of the four 8-point column tiles per pass (fewer live accumulators; the A
 // fragments are re-read from L1 in later passes)
-template <int MT, int NTB, class RowOf>
-__device__ __forceinline__ void vm_recon(const Run& r, const double* Ws, double* tile, int nrows, RowOf row_of,
-                                         const int* s_prow, int lane) {
-  const int ksn = (r.ku + 3) >> 2;
+template <int MT, int NTB, int LDB = VM_LDW, class RowOf>
+__device__ __forceinline__ void vm_recon_g(const double* __restrict__ basis, int kn, const double* __restrict__ off,
+                                           long long off_stride, const double* Ws, double* tile, int nrows,
+                                           RowOf row_of, const int* s_prow, int lane) {
+  const int ksn = (kn + 3) >> 2;
 #pragma unroll
   for (int n0 = 0; n0 < 4; n0 += NTB) {
     double c[MT][NTB][2];
@@ -65,22 +67,22 @@ __device__ __forceinline__ void vm_recon(const Run& r, const double* Ws, double*
       const int rr = mt * 8 + (lane >> 2);
       ok[mt] = rr < nrows;
       const int row = row_of(ok[mt] ? rr : 0);
-      src[mt] = r.phi + (size_t)row * r.ku;
+      src[mt] = basis + (size_t)row * kn;
 #pragma unroll
       for (int nt = 0; nt < NTB; ++nt)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
-          c[mt][nt][h] = (r.u0 && ok[mt]) ? r.u0[(size_t)s_prow[(n0 + nt) * 8 + 2 * (lane & 3) + h] * r.u0_stride + row] : 0.0;
+          c[mt][nt][h] = (off && ok[mt]) ? off[(size_t)s_prow[(n0 + nt) * 8 + 2 * (lane & 3) + h] * off_stride + row] : 0.0;
     }
 #pragma unroll 2
     for (int ks = 0; ks < ksn; ++ks) {
       const int k = 4 * ks + (lane & 3);
       double a[MT];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) a[mt] = (ok[mt] && k < r.ku) ? __ldg(src[mt] + k) : 0.0;
+      for (int mt = 0; mt < MT; ++mt) a[mt] = (ok[mt] && k < kn) ? __ldg(src[mt] + k) : 0.0;
 #pragma unroll
       for (int nt = 0; nt < NTB; ++nt) {
-        const double b = Ws[k * VM_LDW + (n0 + nt) * 8 + (lane >> 2)];
+        const double b = Ws[k * LDB + (n0 + nt) * 8 + (lane >> 2)];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) dmma(c[mt][nt][0], c[mt][nt][1], a[mt], b);
       }
@@ -94,6 +96,12 @@ __device__ __forceinline__ void vm_recon(const Run& r, const double* Ws, double*
   }
 }
 
+template <int MT, int NTB, class RowOf>
+__device__ __forceinline__ void vm_recon(const Run& r, const double* Ws, double* tile, int nrows, RowOf row_of,
+                                         const int* s_prow, int lane) {
+  vm_recon_g<MT, NTB>(r.phi, r.ku, r.u0, r.u0_stride, Ws, tile, nrows, row_of, s_prow, lane);
+}
+
 template <class LAW, int NB, int NQ, int NS>
 __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __grid_constant__ Params<NB, NQ, NS, Shape<LAW, NB, NQ, NS>::NF> prm) {
   using VS = VShape<LAW, NB>;
@@ -102,7 +110,8 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
   const Run& r = prm.r;
   extern __shared__ __align__(16) double vsm[];
   __shared__ __align__(16) double Ws[32 * VM_LDW];  // W[k][point], k_u <= 32 (zero-padded)
-  __shared__ double Ts[KXMAX][32], red[VM_THREADS / 32][32];
+  __shared__ __align__(16) double Ts[KXMAX * VM_LDW];  // tau[a][point] (zero-padded rows)
+  __shared__ double red[VM_THREADS / 32][32];
   __shared__ int s_prow[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* const tile = vsm + warp * VS::TILE;
@@ -134,7 +143,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
   }
   for (int t = threadIdx.x; t < KXMAX * 32; t += blockDim.x) {
     const int a = t / 32, l = t % 32, pp = row_of_pt(l);
-    Ts[a][l] = (a < r.kx && pp < r.P) ? r.tau[(size_t)pp * r.kx + a] : 0.0;
+    Ts[a * VM_LDW + l] = (a < r.kx && pp < r.P) ? r.tau[(size_t)pp * r.kx + a] : 0.0;
   }
   __syncthreads();
   const int pr = row_of_pt(lane);
@@ -164,22 +173,22 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
     __syncwarp();
 #define VM_U(i) U[i]
 #endif
-    // ---- geometry (value_unit, element_kernels.cuh)
+    // ---- geometry (value_unit, element_kernels.cuh): the six deformed vertex coordinates
+    // x = X_ref + Psi_rows tau of the 32 points as one more DMMA reconstruction through the
+    // face rows of the tile (free until the first face), each lane then reads its column
     double x[6], X[6];
+    int vn[3];
 #pragma unroll
     for (int g = 0; g < 3; ++g) {
-      const int n = r.elem_nodes[3 * e + g];
-      X[2 * g] = r.nodes[2 * n];
-      X[2 * g + 1] = r.nodes[2 * n + 1];
-#pragma unroll
-      for (int ic = 0; ic < 2; ++ic) {
-        const int row = 2 * n + ic;
-        double v = r.xref[(size_t)p * r.x_stride + row];
-        const double* ps = r.psi + (size_t)row * r.kx;
-        for (int a = 0; a < r.kx; ++a) v = fma(__ldg(ps + a), Ts[a][lane], v);
-        x[2 * g + ic] = v;
-      }
+      vn[g] = r.elem_nodes[3 * e + g];
+      X[2 * g] = r.nodes[2 * vn[g]];
+      X[2 * g + 1] = r.nodes[2 * vn[g] + 1];
     }
+    vm_recon_g<1, 4>(r.psi, r.kx, r.xref, r.x_stride, Ts, tile + VS::FROW * VM_LDU, 6,
+                     [&](int rr) { return 2 * (rr < 2 ? vn[0] : (rr < 4 ? vn[1] : vn[2])) + (rr & 1); }, s_prow, lane);
+    __syncwarp();
+#pragma unroll
+    for (int d = 0; d < 6; ++d) x[d] = tile[(VS::FROW + d) * VM_LDU + lane];
     Geo o;
     element_geo(x, X, o);
     const bool deg = o.g <= 0.0;
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
         const double F0 = T.wq[q] * (f[c][0] * adj00 + f[c][1] * adj01);
         const double F1 = T.wq[q] * (f[c][0] * adj10 + f[c][1] * adj11);
 #pragma unroll
-        for (int n = 0; n < NB; ++n) R[n * M + c] -= T.dphi[q][n][0] * F0 + T.dphi[q][n][1] * F1;
+        for (int n = 0; n < NB; ++n) R[n * M + c] = fma(-T.dphi[q][n][1], F1, fma(-T.dphi[q][n][0], F0, R[n * M + c]));
       }
       if (LAW::SRC != SRC_NONE) {
         double pos[2];

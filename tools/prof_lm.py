@@ -26,5 +26,8 @@ from paper_2305_15661_b200 import _lib
 st = (ctypes.c_int32 * 3)()
 _lib.load().strom_lm_stats(op._h, st)
 print("rounds, derivative passes, objective passes:", list(st))
+tm = (ctypes.c_double * 4)()
+_lib.load().strom_lm_timing(op._h, tm)
+print("device ms: control %.2f, after d-only rounds %.2f, o-only %.2f, d+o %.2f" % tuple(tm))
 # per-kernel times of the graph's kernel nodes: run under
 #   ncu --metrics gpu__time_duration.sum --csv python tools/prof_lm.py 3  (tools/launch_summary.py)
