@@ -38,7 +38,9 @@ def build(force=False, verbose=False):
     import tempfile
 
     nvcc = os.environ.get("NVCC", "nvcc")
-    tmp = tempfile.mkdtemp(prefix="strom_build_")
+    tmp = os.environ.get("STROM_OBJ_DIR") or tempfile.mkdtemp(prefix="strom_build_")  # STROM_OBJ_DIR: keep objects
+    os.makedirs(tmp, exist_ok=True)
+    only = os.environ.get("STROM_ONLY_UNITS")  # experiment builds: recompile these units, reuse the other objects
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
     flags += os.environ.get("STROM_NVCC_EXTRA", "").split()  # experiment knobs (-D...)
     if verbose:
@@ -46,6 +48,8 @@ def build(force=False, verbose=False):
 
     def compile_unit(u):
         obj = os.path.join(tmp, u + ".o")
+        if only and u not in only.split(",") and os.path.exists(obj):
+            return u, obj, subprocess.CompletedProcess([], 0, "", "")
         r = subprocess.run([nvcc, *flags, "-c", os.path.join(CSRC, u), "-o", obj], capture_output=True, text=True)
         return u, obj, r
 

@@ -24,6 +24,9 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_HREG_WIDE
 #define STROM_HREG_WIDE 15  // k_u > 16 (240 registers): register Gram for up to 15 upper tiles (K <= 40)
 #endif
+#ifndef STROM_GFRAG
+#define STROM_GFRAG 1  // gradient S / T accumulated from the J accumulator fragments (0: from Jt in shared memory)
+#endif
 #ifndef STROM_MMA_MAXNREG
 #define STROM_MMA_MAXNREG 168  // 3 warps per SMSP (12 per SM with 15 KB of smem per warp)
 #endif
@@ -1001,7 +1004,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     }
     // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
     double* Jt = RA;
-    constexpr bool GFRAG = CT;  // gradient from the J accumulator fragments
+    constexpr bool GFRAG = CT && STROM_GFRAG;  // gradient from the J accumulator fragments
     const bool gfrag = GFRAG && DERIVS;
     double rr[3];  // rho * R at the lane's three projection rows
 #pragma unroll
@@ -1193,7 +1196,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   if (!DERIVS) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) jacc += __shfl_xor_sync(0xffffffffu, jacc, o);
-  if constexpr (CT) {
+  if constexpr (CT && STROM_GFRAG) {
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1)
 #pragma unroll

@@ -145,3 +145,34 @@ def test_reference_lm_runs_on_gpu_tracking_problem():
     res = S["lm"].lm_solve(_problem(case, g, "fs"), S["lm"].LmConfig(max_iters=3), w0_mode="keep")
     assert np.array_equal(res.history[:, 5], g["fs_lm_hist"][:, 5])
     assert rel_err(res.objective, g["fs_lm_obj"]) < 1e-8 and rel_err(res.w, g["fs_lm_w"]) < 1e-8
+
+
+def test_enriched_mode_argument_errors():
+    """C-ABI error behaviour of the enriched mode: no test space bound, more than one
+    parameter point, an active set — all rejected with a negative code (RuntimeError here)."""
+    from paper_2305_15661_b200 import _lib
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.fullspace import _NoDistortion, test_space_tables
+    from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases
+
+    case, g = build("tracking_q6")
+    ne = case.mesh.num_elements
+    op = GpuReducedOperator(case.law, case.geom, ReducedBases(np.zeros((g["U"].size, 0)), np.zeros((g["x"].size, 0)), g["x"]),
+                            _NoDistortion(), state_offset=g["U"])
+    rec = 40 * (1 + 24 + 72 + 6) + 7
+    out = torch.empty(ne * rec, dtype=torch.float64, device=op.device)
+    W = torch.zeros((2, 1), dtype=torch.float64, device=op.device)
+    Mu = torch.full((2, 1), 2.0, dtype=torch.float64, device=op.device)
+    with pytest.raises(RuntimeError, match="test space not set"):
+        op.eval_batched(_lib.ELEMJAC_ENRICHED, W[:1], W[:1], Mu[:1], None, out=out, sync=True)
+    dphi_t, trace_t = test_space_tables(op.dm.tabs, 3)
+    assert dphi_t.shape == (12, 10, 2) and trace_t.shape == (3, 4, 10)
+    _lib.check(op._lib.strom_set_test_space(op._h, 10, dphi_t.ctypes.data, trace_t.ctypes.data), "set_test_space")
+    with pytest.raises(RuntimeError, match="one parameter point"):
+        op.eval_batched(_lib.ELEMJAC_ENRICHED, W, W, Mu, None, out=out, sync=True)
+    with pytest.raises(RuntimeError, match="all elements"):
+        op.eval_batched(_lib.ELEMJAC_ENRICHED, W[:1], W[:1], Mu[:1], WeightVector(np.ones(ne)), out=out, sync=True)
+    with pytest.raises(RuntimeError, match="bad arguments"):
+        _lib.check(op._lib.strom_set_test_space(op._h, 0, dphi_t.ctypes.data, trace_t.ctypes.data), "set_test_space")
+    with pytest.raises(ValueError):
+        op.eval_batched(_lib.ELEMJAC_ENRICHED, W[:1], W[:1], Mu[:1], None)  # needs a caller-sized output
