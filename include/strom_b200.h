@@ -79,10 +79,12 @@ enum {
                                dR/dx_e, N_e, dN_e/dx_e per element at U = U0, x = x_ref (P = 1;
                                4-component laws, p = 2): dg.py:197-225 and distortion.py:64-92, the
                                blocks assemble_global / assemble_distortion scatter */
-  STROM_ELEMJAC_ENRICHED = 8 /* out[ne][NT (1 + 24 + 72 + 6) + 7], NT = 4 n_test: the same blocks with the residual
-                               tested against the nodal space bound by strom_set_test_space (degree p+1):
-                               res, dR/dU_e (NT x 24), dR/dU_nbr (NT x 72), dR/dx_e (NT x 6), N_e, dN_e/dx_e — what
-                               assemble_enriched scatters, dg.py:275-326 */
+  STROM_ELEMJAC_ENRICHED = 8 /* out[ne][NT (1 + 4 n_u + 6) + 7], NT = m n_test, n_u = m n_b: the same blocks with the
+                               residual tested against the nodal space bound by strom_set_test_space:
+                               res, dR/dU_e (NT x n_u), dR/dU_nbr (NT x 3 n_u), dR/dx_e (NT x 6), N_e, dN_e/dx_e.
+                               With the degree p+1 space: what assemble_enriched scatters (dg.py:275-326); with the
+                               trial space itself: the STROM_ELEMJAC blocks for every compiled law and degree
+                               (scalar laws with sources included, dg.py:197-272).  P = 1. */
 };
 
 int strom_create(const strom_mesh_desc* mesh, const strom_law_desc* law, const strom_quad_desc* quad,
@@ -103,12 +105,13 @@ int strom_set_bases(strom_handle* h, const double* phi, int32_t ku, const double
 int strom_set_offsets(strom_handle* h, const double* state_offset, int64_t state_stride,
                       const double* ref_coords, int64_t coord_stride);
 
-/* Bind a residual test space richer than the trial space (Geometry.test_space,
- * strom/geometry.py:162-196; used by assemble_enriched, dg.py:275-326).  HOST pointers:
- * dphi (nq, n_test, 2) reference gradients of the test basis at the volume points, trace
+/* Bind a residual test space (Geometry.test_space, strom/geometry.py:162-196; used by
+ * assemble_enriched, dg.py:275-326).  HOST pointers: phi (nq, n_test) values and dphi
+ * (nq, n_test, 2) reference gradients of the test basis at the volume points, trace
  * (3, ns, n_test) its values at the face points of each local face (zero off the face).
  * The library keeps its own device copy. */
-int strom_set_test_space(strom_handle* h, int32_t n_test, const double* dphi, const double* trace);
+int strom_set_test_space(strom_handle* h, int32_t n_test, const double* phi, const double* dphi,
+                         const double* trace);
 
 /* Size the workspace for up to max_P parameters and max_active elements. */
 int strom_reserve(strom_handle* h, int32_t max_P, int32_t max_active);

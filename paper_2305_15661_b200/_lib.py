@@ -52,7 +52,7 @@ def load(path=SO_PATH):
                                  C.POINTER(DistDesc), C.c_int, C.POINTER(vp)]
     lib.strom_set_bases.argtypes = [vp, vp, i32, vp, i32, vp, vp]
     lib.strom_reserve.argtypes = [vp, i32, i32]
-    lib.strom_set_test_space.argtypes = [vp, i32, vp, vp]
+    lib.strom_set_test_space.argtypes = [vp, i32, vp, vp, vp]
     lib.strom_set_offsets.argtypes = [vp, vp, C.c_int64, vp, C.c_int64]
     lib.strom_eval.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp, i32]
     lib.strom_eval_host.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, i32, vp, C.c_int64, vp, vp]

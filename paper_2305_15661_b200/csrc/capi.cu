@@ -159,16 +159,18 @@ extern "C" int strom_set_offsets(strom_handle* h, const double* state_offset, in
   return 0;
 }
 
-extern "C" int strom_set_test_space(strom_handle* h, int32_t nbt, const double* dphi, const double* trace) {
+extern "C" int strom_set_test_space(strom_handle* h, int32_t nbt, const double* phi, const double* dphi,
+                                    const double* trace) {
   if (!h) return fail(-1, "null handle");
-  if (nbt < 1 || nbt > 64 || !dphi || !trace) return fail(-1, "strom_set_test_space: bad arguments");
+  if (nbt < 1 || nbt > 64 || !phi || !dphi || !trace) return fail(-1, "strom_set_test_space: bad arguments");
   CK(cudaSetDevice(h->device));
   if (h->test_tab) cudaFree(h->test_tab);
   h->test_tab = nullptr;
-  const size_t nd = (size_t)h->nq * nbt * 2, nt = (size_t)3 * h->ns * nbt;
-  CK(cudaMalloc(&h->test_tab, (nd + nt) * sizeof(double)));
+  const size_t nd = (size_t)h->nq * nbt * 2, nt = (size_t)3 * h->ns * nbt, np = (size_t)h->nq * nbt;
+  CK(cudaMalloc(&h->test_tab, (nd + nt + np) * sizeof(double)));  // [dphi | trace | phi]
   CK(cudaMemcpy(h->test_tab, dphi, nd * sizeof(double), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->test_tab + nd, trace, nt * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->test_tab + nd + nt, phi, np * sizeof(double), cudaMemcpyHostToDevice));
   h->test_nb = nbt;
   return 0;
 }
@@ -210,8 +212,9 @@ extern "C" int strom_eval(strom_handle* h, int32_t mode, const double* w, const 
   if (!h) return fail(-1, "null handle");
   if (mode < 0 || mode > MODE_ELEMJAC_ENRICHED) return fail(-1, "bad mode");
   const bool ejmode = mode == MODE_ELEMJAC || mode == MODE_ELEMJAC_ENRICHED;
-  if (ejmode && (h->law.n_comp != 4 || h->p != 2 || P != 1))
-    return fail(-1, "element Jacobians: 4-component laws with p = 2, one parameter point");
+  if (ejmode && P != 1) return fail(-1, "element Jacobians: one parameter point");
+  if (mode == MODE_ELEMJAC && (h->law.n_comp != 4 || h->p != 2))
+    return fail(-1, "STROM_ELEMJAC: 4-component laws with p = 2 (other laws: STROM_ELEMJAC_ENRICHED with the trial space as the test space)");
   if (mode == MODE_ELEMJAC_ENRICHED && !h->test_tab) return fail(-1, "enriched element Jacobians: test space not set");
   if (P < 1) return fail(-1, "P must be >= 1");
   if (!out) return fail(-1, "null output");

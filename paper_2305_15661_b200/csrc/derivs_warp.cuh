@@ -397,6 +397,114 @@ __global__ void __launch_bounds__(WTHREADS) derivs_warp_kernel(
       S[SH::RT + i] = rv + rf;
     }
     __syncwarp();
+    // ---- element Jacobian blocks against a bound test space (STROM_ELEMJAC_ENRICHED: the full-space
+    // assembly of dg.py:197-326 for every law this kernel serves; the test space may be the trial
+    // space itself): the pointwise records of S2 / S3 contracted with the test tabulations,
+    // out[e] = [res (NT) | dR/dU_e (NT x NU) | dR/dU_nbr (NT x 3 NU) | dR/dx_e (NT x 6) | N_e | dN_e/dx_e]
+    if (r.mode == MODE_ELEMJAC_ENRICHED) {
+      const int NBT = r.test_nb, NT = NBT * M;
+      const double* __restrict__ tdphi = r.test_tab;            // [NQ][NBT][2]
+      const double* __restrict__ ttr = tdphi + NQ * NBT * 2;    // [3][NS][NBT]
+      const double* __restrict__ tphi = ttr + 3 * NS * NBT;     // [NQ][NBT]
+      double* const eo = r.out + (size_t)e * ((size_t)NT * (1 + 4 * NU + 6) + 7);
+      const double* adj = S + SH::MADJ;
+      const double* Jm = S + SH::MJ;
+      const double detJ = S[SH::MDET];
+      const double* FX0 = S + SH::FX;
+      if (valid) {
+        for (int i = k; i < NT; i += TPU) {  // residual row (n, c) and its six mesh derivatives
+          const int n = i / M, c = i % M;
+          double t00 = 0.0, t01 = 0.0, t10 = 0.0, t11 = 0.0, sacc = 0.0;
+          for (int q = 0; q < NQ; ++q) {
+            const double d0 = tdphi[(q * NBT + n) * 2], d1 = tdphi[(q * NBT + n) * 2 + 1];
+            const double f0 = RBp[SH::FQ + (c * 2 + 0) * NQP + q], f1 = RBp[SH::FQ + (c * 2 + 1) * NQP + q];
+            t00 = fma(d0, f0, t00); t01 = fma(d0, f1, t01); t10 = fma(d1, f0, t10); t11 = fma(d1, f1, t11);
+            if (LAW::SRC != SRC_NONE) sacc = fma(tphi[q * NBT + n], S[SH::SW + c * NQP + q], sacc);
+          }
+          double rv = -(adj[0] * t00 + adj[1] * t01 + adj[2] * t10 + adj[3] * t11);
+          if (LAW::SRC != SRC_NONE) rv -= detJ * sacc;
+          double rf = 0.0;
+          for (int fs = 0; fs < NFS; ++fs) rf = fma(ttr[fs * NBT + n], RBp[SH::HS + c * NFSP + fs], rf);
+          eo[i] = rv + rf;
+          for (int d = 0; d < 6; ++d) {
+            const int gv = d >> 1, ic = d & 1;
+            const double c0 = (gv == 1) - (gv == 0), c1 = (gv == 2) - (gv == 0);
+            const double dJ00 = ic == 0 ? c0 : 0.0, dJ01 = ic == 0 ? c1 : 0.0, dJ10 = ic == 1 ? c0 : 0.0, dJ11 = ic == 1 ? c1 : 0.0;
+            double v = -(dJ11 * t00 - dJ01 * t01 - dJ10 * t10 + dJ00 * t11);
+            if (LAW::SRC != SRC_NONE) {
+              const double ddet = dJ00 * Jm[3] + Jm[0] * dJ11 - dJ01 * Jm[2] - Jm[1] * dJ10;
+              double sv = 0.0;
+              for (int q = 0; q < NQ; ++q) {
+                double term = ddet * S[SH::SW + c * NQP + q];
+                if (LAW::SRC == SRC_POS) term += S[SH::SP + (c * 2 + ic) * NQP + q] * T.bary[q][gv];
+                sv = fma(tphi[q * NBT + n], term, sv);
+              }
+              v -= sv;
+            }
+            for (int f = 0; f < 3; ++f) {
+              const int a = f, b = (f + 1) % 3;
+              const double del = (gv == b) - (gv == a);
+              if (del == 0.0) continue;
+              const double dnu0 = ic == 0 ? 0.0 : del, dnu1 = ic == 0 ? -del : 0.0;
+              const double* nh = S + SH::MNHAT + 2 * f;
+              const double len = S[SH::MNLEN + f];
+              const double dlen = nh[0] * dnu0 + nh[1] * dnu1;
+              const double dnh0 = (dnu0 - nh[0] * dlen) / len, dnh1 = (dnu1 - nh[1] * dlen) / len;
+              for (int s = 0; s < NS; ++s) {
+                const double* FXp = FX0 + f * NS + s;
+                const double lam = FXp[(3 * M) * NFSP];
+                const double dlam = FXp[(3 * M + 1) * NFSP] * dnh0 + FXp[(3 * M + 2) * NFSP] * dnh1;
+                const double coef = dlam * len + lam * dlen;
+                const double dH = FXp[(2 * c) * NFSP] * dnu0 + FXp[(2 * c + 1) * NFSP] * dnu1 - FXp[(2 * M + c) * NFSP] * coef;
+                v = fma(ttr[(f * NS + s) * NBT + n], dH, v);
+              }
+            }
+            eo[(size_t)NT * (1 + 4 * NU) + i * 6 + d] = v;
+          }
+        }
+        for (int i = k; i < NT * NU; i += TPU) {  // dR/dU_e
+          const int row = i / NU, col = i % NU, n = row / M, c = row % M, np_ = col / M, cp = col % M;
+          double v = 0.0;
+          for (int q = 0; q < NQ; ++q) {
+            double g = fma(tdphi[(q * NBT + n) * 2], RA[SH::BQ + ((c * 2 + 0) * M + cp) * NQ + q],
+                           tdphi[(q * NBT + n) * 2 + 1] * RA[SH::BQ + ((c * 2 + 1) * M + cp) * NQ + q]);
+            if (LAW::SRC == SRC_U) g = fma(tphi[q * NBT + n], RA[SH::BS + (c * M + cp) * NQ + q], g);
+            v = fma(-g, T.phi[q][np_], v);
+          }
+          for (int f = 0; f < 3; ++f)
+            for (int j = 0; j < NF; ++j) {
+              if (fnode_of(PD, f, j) != np_) continue;
+              for (int s = 0; s < NS; ++s)
+                v = fma(ttr[(f * NS + s) * NBT + n] * T.trace[f][s][j], RA[SH::CF + (c * M + cp) * NFS + f * NS + s], v);
+            }
+          eo[NT + i] = v;
+        }
+        for (int i = k; i < NT * 3 * NU; i += TPU) {  // dR/dU_nbr: the neighbor's face-node columns
+          const int row = i / (3 * NU), col = i % (3 * NU), n = row / M, c = row % M;
+          const int f = col / NU, node = (col % NU) / M, cp = col % M;
+          const int fi = r.finfo[3 * e + f];
+          double v = 0.0;
+          if ((fi >> 3) == 0) {
+            const int nf = fi & 3;
+            int jn = -1;
+            for (int j = 0; j < NF; ++j) {
+              const int nodej = j == 0 ? nf : (j == 1 ? (nf + 1) % 3 : 3 + nf * (PD - 1) + (j - 2));
+              if (nodej == node) jn = j;
+            }
+            if (jn >= 0)
+              for (int s = 0; s < NS; ++s) {
+                const int sp = ((fi >> 2) & 1) ? NS - 1 - s : s;
+                v = fma(ttr[(f * NS + s) * NBT + n] * T.trace[0][sp][jn],
+                        RA[SH::CF + M * M * NFS + (c * M + cp) * NFS + f * NS + s], v);
+              }
+          }
+          eo[NT + NT * NU + i] = v;
+        }
+        if (k < 7) eo[(size_t)NT * (1 + 4 * NU + 6) + k] = k == 0 ? S[SH::MN] : S[SH::DNX + k - 1];
+      }
+      __syncwarp();
+      continue;
+    }
     // ---- S4: state tangents (lane k = direction k) ---------------------------------------
     double acc[NU];
 #pragma unroll

@@ -8,8 +8,10 @@ element kernel in its STROM_ELEMJAC mode (the same local Jacobians the reduced p
 written out instead of projected); the scatter into CSR uses the reference's own index
 construction.  ``assemble_enriched`` (dg.py:275-326) tests the same weak form against the
 degree p+1 nodal space: K1's STROM_ELEMJAC_ENRICHED mode contracts its pointwise flux /
-Jacobian records with the test tabulations bound by ``strom_set_test_space``.  4-component
-laws (Euler) with p = 2; other laws raise.  Full-space tracking on top: ``tracking.py``.
+Jacobian records with the test tabulations bound by ``strom_set_test_space``; with the trial
+space bound as the test space the same mode gives the plain blocks for every compiled law and
+degree (the scalar laws with their sources, Euler at p = 1).  Full-space tracking on top:
+``tracking.py``.
 """
 
 import numpy as np
@@ -24,28 +26,30 @@ class _NoDistortion:
 
 
 def test_space_tables(tabs, degree):
-    """Reference gradients (nq, n_test, 2) and face traces (3, ns, n_test) of the degree
-    ``degree`` nodal basis at the element tables' volume / face points (geometry.py:162-196)."""
+    """Values (nq, n_test), reference gradients (nq, n_test, 2) and face traces (3, ns, n_test)
+    of the degree ``degree`` nodal basis at the element tables' volume / face points
+    (geometry.py:162-196)."""
     from .tables import LOCAL_EDGES, lagrange_basis, triangle_rule
 
     verts = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]])
-    _, dphi_t = lagrange_basis(degree, triangle_rule(tabs.quad_order).points)
+    phi_t, dphi_t = lagrange_basis(degree, triangle_rule(tabs.quad_order).points)
     s = np.asarray(tabs.s)
     trace_t = np.stack([lagrange_basis(degree, (1.0 - s)[:, None] * verts[a] + s[:, None] * verts[b])[0]
                         for a, b in LOCAL_EDGES])
-    return np.ascontiguousarray(dphi_t), np.ascontiguousarray(trace_t)
+    return np.ascontiguousarray(phi_t), np.ascontiguousarray(dphi_t), np.ascontiguousarray(trace_t)
 
 
 def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenerate=True, test_degree=None,
                      columns=None):
-    """(ne, EJ_SIZE) STROM_ELEMJAC records at the global state U and coordinates x; with
-    ``test_degree`` the STROM_ELEMJAC_ENRICHED records (ne, NT (1 + 24 + 72 + 6) + 7).
-    ``columns`` (slice) limits what is copied back to the host."""
+    """Element records at the global state U and coordinates x: (ne, EJ_SIZE) STROM_ELEMJAC
+    records (4-component laws, p = 2), or with ``test_degree`` the STROM_ELEMJAC_ENRICHED records
+    (ne, NT (1 + 4 n_u + 6) + 7) for any compiled law and degree.  ``columns`` limits what is
+    copied back to the host."""
     import torch
 
     mesh, maps = geom.mesh, geom.maps
-    if maps.n_comp != 4 or maps.degree_sol != 2:
-        raise NotImplementedError("GPU element Jacobians: 4-component laws with p = 2")
+    if test_degree is None and (maps.n_comp != 4 or maps.degree_sol != 2):
+        raise NotImplementedError("STROM_ELEMJAC records: 4-component laws with p = 2 (pass test_degree)")
     U = np.asarray(U, dtype=float).reshape(-1)
     x = np.asarray(x, dtype=float).reshape(-1)
     bases = ReducedBases(np.zeros((U.size, 0)), np.zeros((x.size, 0)), x)
@@ -55,11 +59,12 @@ def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenera
     Mu = torch.as_tensor(op._mu(mu)[None]).to(op.device)
     mode, rec = _lib.ELEMJAC, EJ_SIZE
     if test_degree is not None:
-        dphi_t, trace_t = test_space_tables(op.dm.tabs, test_degree)
+        phi_t, dphi_t, trace_t = test_space_tables(op.dm.tabs, test_degree)
         nbt = dphi_t.shape[1]
-        _lib.check(op._lib.strom_set_test_space(op._h, nbt, dphi_t.ctypes.data, trace_t.ctypes.data),
-                   "strom_set_test_space")
-        mode, rec = _lib.ELEMJAC_ENRICHED, 4 * nbt * (1 + 24 + 72 + 6) + 7
+        _lib.check(op._lib.strom_set_test_space(op._h, nbt, phi_t.ctypes.data, dphi_t.ctypes.data,
+                                                trace_t.ctypes.data), "strom_set_test_space")
+        nu = op.dm.nu
+        mode, rec = _lib.ELEMJAC_ENRICHED, maps.n_comp * nbt * (1 + 4 * nu + 6) + 7
     out = torch.empty(mesh.num_elements * rec, dtype=torch.float64, device=op.device)
     out, rc = op.eval_batched(mode, W, Tau, Mu, None, out=out, sync=True)
     if rc == 1 and raise_degenerate:  # g <= 0 somewhere: raised after the whole batch, as dg.py:177-178
@@ -73,31 +78,80 @@ def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenera
     return (out if columns is None else out[:, columns].contiguous()).cpu().numpy()
 
 
+def element_blocks(law, geom, U, x, mu, test_degree=None, dist=None, want_jacobians=True, device=None,
+                   raise_degenerate=True):
+    """Element blocks of the DG residual in one K1 pass over the mesh:
+    (res (ne, NT), dR/dU_e (ne, NT, n_u), dR/dU_nbr (ne, NT, 3 n_u), dR/dx_e (ne, NT, 6), N (ne,),
+    dN/dx_e (ne, 6)) — what ``elemental_residual(..., want_jacobians=True)`` returns per element
+    (dg.py:197-225) plus the distortion residual and its gradient (distortion.py:53-68).
+    ``test_degree`` None: the trial space tests the residual (NT = n_u); otherwise the nodal
+    space of that degree (``assemble_enriched``: p + 1).  The Jacobian blocks are None (and never
+    copied back) when ``want_jacobians`` is false."""
+    from .tables import lagrange_nodes
+
+    maps = geom.maps
+    m, p = maps.n_comp, maps.degree_sol
+    nu = lagrange_nodes(p).shape[0] * m
+    if test_degree is None and m == 4 and p == 2:  # the DMMA local-Jacobian path (STROM_ELEMJAC)
+        cols = None if want_jacobians else np.r_[0:24, 2472:2479]
+        o = _element_records(law, geom, U, x, mu, dist=dist, device=device, raise_degenerate=raise_degenerate,
+                             columns=cols)
+        if not want_jacobians:
+            return o[:, :24], None, None, None, o[:, 24], o[:, 25:]
+        return (o[:, :24], o[:, 24:600].reshape(-1, 24, 24), o[:, 600:2328].reshape(-1, 24, 72),
+                o[:, 2328:2472].reshape(-1, 24, 6), o[:, 2472], o[:, 2473:2479])
+    deg = p if test_degree is None else test_degree
+    NT = lagrange_nodes(deg).shape[0] * m
+    rec = NT * (1 + 4 * nu + 6)
+    if not want_jacobians:  # residual rows and the distortion scalar only
+        cols = np.r_[0:NT, rec:rec + 7]
+        o = _element_records(law, geom, U, x, mu, dist=dist, device=device, raise_degenerate=raise_degenerate,
+                             test_degree=deg, columns=cols)
+        return o[:, :NT], None, None, None, o[:, NT], o[:, NT + 1:]
+    o = _element_records(law, geom, U, x, mu, dist=dist, device=device, raise_degenerate=raise_degenerate,
+                         test_degree=deg)
+    a, b, c = NT, NT + NT * nu, NT + NT * 4 * nu
+    return (o[:, :a], o[:, a:b].reshape(-1, NT, nu), o[:, b:c].reshape(-1, NT, 3 * nu), o[:, c:rec].reshape(-1, NT, 6),
+            o[:, rec], o[:, rec + 1:rec + 7])
+
+
 def element_jacobians(law, geom, U, x, mu, device=None):
-    """(res (ne, 24), jac_self (ne, 24, 24), jac_neigh (ne, 24, 72), jac_coord (ne, 24, 6)) at
+    """(res (ne, n_u), jac_self (ne, n_u, n_u), jac_neigh (ne, n_u, 3 n_u), jac_coord (ne, n_u, 6)) at
     the global state U and coordinates x (dg.py:197-225, batched over all elements)."""
-    o = _element_records(law, geom, U, x, mu, device=device)
-    return (o[:, :24], o[:, 24:600].reshape(-1, 24, 24), o[:, 600:2328].reshape(-1, 24, 72),
-            o[:, 2328:2472].reshape(-1, 24, 6))
+    return element_blocks(law, geom, U, x, mu, device=device)[:4]
+
+
+def _any_law(mesh, maps):
+    """A compiled law with the mesh's component count whose boundaries all extrapolate (the
+    distortion residual does not depend on the law or the state) and an admissible state."""
+    import dataclasses
+
+    from . import laws as L
+
+    tags = {t: L.BoundaryCondition("extrapolate") for t in mesh.boundary_tags}
+    if maps.n_comp == 4:
+        return L.euler(tags={t: "extrapolate" for t in mesh.boundary_tags}), L.euler_freestream(2.0)
+    if maps.n_comp == 1:
+        return dataclasses.replace(L.linear_advection(), boundary_data=tags), np.ones(1)
+    raise NotImplementedError(f"no compiled law with {maps.n_comp} components")
 
 
 def assemble_distortion(mesh, maps, x, config, want_jacobian=True, geom=None, device=None):
     """Elemental distortion residuals N (ne,) and the CSR gradient dN/dx (ne, N_x):
     strom/distortion.py:71-92 (never raises: eps floors the Jacobian determinant)."""
-    from . import laws as L
     from .mesh import get_geometry
 
     geom = geom or get_geometry(mesh, maps)
-    if maps.n_comp != 4 or maps.degree_sol != 2:
-        raise NotImplementedError("GPU distortion assembly runs on the p = 2, 4-component element kernel")
-    U = np.tile(L.euler_freestream(2.0), mesh.num_elements * 6)  # the state does not enter N
-    law = L.euler(tags={t: "extrapolate" for t in mesh.boundary_tags})
-    o = _element_records(law, geom, U, x, np.array([2.0]), dist=config, device=device, raise_degenerate=False)
-    N = o[:, 2472].copy()
+    law, u1 = _any_law(mesh, maps)
+    nb = maps.state_map.shape[1] // maps.n_comp
+    U = np.tile(u1, mesh.num_elements * nb)  # the state does not enter N
+    _, _, _, _, N, dN = element_blocks(law, geom, U, x, np.array([2.0]), dist=config, want_jacobians=False,
+                                       device=device, raise_degenerate=False)
+    N = N.copy()
     if not want_jacobian:
         return N, None
     rows = np.repeat(np.arange(mesh.num_elements), 6)
-    jac = sp.coo_matrix((o[:, 2473:2479].ravel(), (rows, maps.coord_map.ravel())),
+    jac = sp.coo_matrix((dN.ravel(), (rows, maps.coord_map.ravel())),
                         shape=(mesh.num_elements, maps.n_global_coord)).tocsr()
     return N, jac
 
@@ -138,27 +192,9 @@ def _scatter_csr(maps, rows, jac_self, jac_neigh, jac_coord, n_rows):
 
 def enriched_records(law, geom, U, x, mu, test_degree=None, dist=None, want_jacobians=True, device=None,
                      raise_degenerate=True):
-    """Element blocks of the enriched residual in one K1 pass: (res (ne, NT), jac_self
-    (ne, NT, 24), jac_neigh (ne, NT, 72), jac_coord (ne, NT, 6), N (ne,), dN (ne, 6)); the
-    Jacobian blocks are None (and never copied back) when ``want_jacobians`` is false."""
-    from .tables import lagrange_nodes
-
-    maps = geom.maps
-    deg = maps.degree_sol + 1 if test_degree is None else test_degree
-    NT = lagrange_nodes(deg).shape[0] * maps.n_comp
-    rec = NT * (1 + 24 + 72 + 6)
-    if not want_jacobians:  # residual rows and the distortion scalar only
-        import torch  # noqa: F401
-
-        cols = np.r_[0:NT, rec:rec + 7]
-        o = _element_records(law, geom, U, x, mu, dist=dist, device=device, raise_degenerate=raise_degenerate,
-                             test_degree=deg, columns=cols)
-        return o[:, :NT], None, None, None, o[:, NT], o[:, NT + 1:]
-    o = _element_records(law, geom, U, x, mu, dist=dist, device=device, raise_degenerate=raise_degenerate,
-                         test_degree=deg)
-    a, b, c = NT, NT + NT * 24, NT + NT * 96
-    return (o[:, :a], o[:, a:b].reshape(-1, NT, 24), o[:, b:c].reshape(-1, NT, 72), o[:, c:rec].reshape(-1, NT, 6),
-            o[:, rec], o[:, rec + 1:rec + 7])
+    """``element_blocks`` against the degree p+1 (or ``test_degree``) test space (dg.py:275-326)."""
+    deg = geom.maps.degree_sol + 1 if test_degree is None else test_degree
+    return element_blocks(law, geom, U, x, mu, deg, dist, want_jacobians, device, raise_degenerate)
 
 
 def assemble_enriched(law, mesh, maps, U, x, mu, test_degree=None, want_jacobians=True, geom=None, device=None):

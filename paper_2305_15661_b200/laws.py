@@ -185,8 +185,16 @@ def burgers_spacetime():
         "right": BoundaryCondition("extrapolate"),
         "top": BoundaryCondition("extrapolate"),
     }
+    def initial_state(pos, mu):
+        """Inflow characteristic behind the straight shock line x = (a + 1) t / 2, the slab value 1
+        ahead of it (conslaw.py:136-144)."""
+        a, b = mu
+        x, t = pos[..., 0], pos[..., 1]
+        behind = np.sqrt(a * a + (0.04 / b) * (np.exp(b * x) - 1.0))
+        return np.where(x <= 0.5 * (a + 1.0) * t, behind, 1.0)[..., None]
+
     return LawSpec("burgers-spacetime", 1, 2, flux, source, None, wavespeed, bcs,
-                   np.array([[3.0, 9.0], [0.02, 0.075]]), law_id=LAW_BURGERS_SPACETIME)
+                   np.array([[3.0, 9.0], [0.02, 0.075]]), initial_state, law_id=LAW_BURGERS_SPACETIME)
 
 
 def burgers_strip(u_left=1.0, u_right=-0.5):

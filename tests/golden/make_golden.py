@@ -321,6 +321,47 @@ def case_tracking(quad_order, name, with_problem):
     save(name, out)
 
 
+def case_tracking_scalar(name, law, p, box, nx, ny, mu, seed):
+    """The reference's own scalar laws through the full-space path: assemble_global Jacobian
+    products, assemble_enriched (dg.py:275-326) and the full-space TrackingProblem with a
+    short lm_solve history (tracking.py:41-150)."""
+    from strom import tracking as strack
+
+    from paper_2305_15661_b200.mesh import build_box_mesh
+
+    mesh, maps = build_box_mesh(box, nx, ny, degree_sol=p, n_comp=1)
+    rm, rmaps = ref_mesh(mesh, maps)
+    rng = np.random.default_rng(seed)
+    mu = np.asarray(mu, dtype=float)
+    X = rm.nodes.ravel()
+    z = 0.02 * min((box[1][0] - box[0][0]) / nx, (box[1][1] - box[0][1]) / ny) * rng.standard_normal(X.size)
+    free = strack.boundary_slide_dofs(rm)
+    x = X.copy()
+    x[free] += z[free]
+    U = sdg.initial_state(law, rm, rmaps, x, mu) * (1.0 + 0.02 * rng.standard_normal(rmaps.n_global_state))
+    out = dict(p=p, box=np.asarray(box, dtype=float), nxny=np.array([nx, ny]), mu=mu, U=U, x=x)
+    R, JU, JX = sdg.assemble_global(law, rm, rmaps, U, x, mu)
+    Rb, EU, EX = sdg.assemble_enriched(law, rm, rmaps, U, x, mu)
+    v_u, v_x = rng.standard_normal(JU.shape[1]), rng.standard_normal(JX.shape[1])
+    u_r, u_e = rng.standard_normal(JU.shape[0]), rng.standard_normal(EU.shape[0])
+    out.update(v_u=v_u, v_x=v_x, u_r=u_r, u_e=u_e, glob_R=R, glob_JU_v=JU @ v_u, glob_JUt_u=JU.T @ u_r,
+               glob_JX_v=JX @ v_x, glob_JXt_u=JX.T @ u_r, enr_R=Rb, enr_JU_v=EU @ v_u, enr_JUt_u=EU.T @ u_e,
+               enr_JX_v=EX @ v_x, enr_JXt_u=EX.T @ u_e)
+    dist = sdist.DistortionConfig(1e-3)
+    N, JN = sdist.assemble_distortion(rm, rmaps, x, dist)
+    out.update(dist_N=N, dist_JN_v=JN @ v_x)
+    prob = strack.TrackingProblem(law, rm, rmaps, mu, dist, U0=U, x0=x)
+    w0, z0 = prob.initial_guess()
+    J, S, T, Hww, Hwt, Htt = prob.derivatives(w0, z0)
+    a, b = rng.standard_normal(len(w0)), rng.standard_normal(len(z0))
+    out.update(fs_obj=prob.objective(w0, z0), fs_J=J, fs_S=S, fs_T=T, fs_a=a, fs_b=b, fs_Hww_a=Hww @ a,
+               fs_Hwt_b=Hwt @ b, fs_Htt_b=Htt @ b)
+    res = slm.lm_solve(prob, slm.LmConfig(max_iters=3), w0_mode="keep")
+    out.update(fs_lm_w=res.w, fs_lm_tau=res.tau, fs_lm_hist=res.history, fs_lm_obj=res.objective,
+               fs_lm_reason=res.reason)
+    save(name, out)
+
+
 if __name__ == "__main__":
     case_strip()
     case_euler_square(6, "euler_square_q6")
@@ -337,3 +378,6 @@ if __name__ == "__main__":
     case_lprows()
     case_tracking(6, "tracking_q6", True)
     case_tracking(None, "tracking_default", False)
+    case_tracking_scalar("tracking_burgers_p2", slaw.burgers_spacetime(), 2, ((0.0, 0.0), (2.0, 1.0)), 4, 3, (5.0, 0.05), 171)
+    case_tracking_scalar("tracking_burgers_p1", slaw.burgers_spacetime(), 1, ((0.0, 0.0), (2.0, 1.0)), 5, 3, (4.0, 0.03), 172)
+    case_tracking_scalar("tracking_linadv_p1", slaw.linear_advection((1.0, 0.5)), 1, ((0.0, 0.0), (1.0, 1.0)), 3, 3, (0.5,), 173)

@@ -165,14 +165,98 @@ def test_enriched_mode_argument_errors():
     Mu = torch.full((2, 1), 2.0, dtype=torch.float64, device=op.device)
     with pytest.raises(RuntimeError, match="test space not set"):
         op.eval_batched(_lib.ELEMJAC_ENRICHED, W[:1], W[:1], Mu[:1], None, out=out, sync=True)
-    dphi_t, trace_t = test_space_tables(op.dm.tabs, 3)
-    assert dphi_t.shape == (12, 10, 2) and trace_t.shape == (3, 4, 10)
-    _lib.check(op._lib.strom_set_test_space(op._h, 10, dphi_t.ctypes.data, trace_t.ctypes.data), "set_test_space")
+    phi_t, dphi_t, trace_t = test_space_tables(op.dm.tabs, 3)
+    assert phi_t.shape == (12, 10) and dphi_t.shape == (12, 10, 2) and trace_t.shape == (3, 4, 10)
+    _lib.check(op._lib.strom_set_test_space(op._h, 10, phi_t.ctypes.data, dphi_t.ctypes.data, trace_t.ctypes.data),
+               "set_test_space")
     with pytest.raises(RuntimeError, match="one parameter point"):
         op.eval_batched(_lib.ELEMJAC_ENRICHED, W, W, Mu, None, out=out, sync=True)
     with pytest.raises(RuntimeError, match="all elements"):
         op.eval_batched(_lib.ELEMJAC_ENRICHED, W[:1], W[:1], Mu[:1], WeightVector(np.ones(ne)), out=out, sync=True)
     with pytest.raises(RuntimeError, match="bad arguments"):
-        _lib.check(op._lib.strom_set_test_space(op._h, 0, dphi_t.ctypes.data, trace_t.ctypes.data), "set_test_space")
+        _lib.check(op._lib.strom_set_test_space(op._h, 0, phi_t.ctypes.data, dphi_t.ctypes.data, trace_t.ctypes.data),
+                   "set_test_space")
     with pytest.raises(ValueError):
         op.eval_batched(_lib.ELEMJAC_ENRICHED, W[:1], W[:1], Mu[:1], None)  # needs a caller-sized output
+
+
+# -- the reference's own scalar laws (with sources), p = 1 and 2: the warp kernel's contraction ----
+def _scalar_case(name):
+    from cases import load
+    from paper_2305_15661_b200 import laws as L
+    from paper_2305_15661_b200.mesh import build_box_mesh, get_geometry
+
+    g = load(name)
+    nx, ny = (int(v) for v in g["nxny"])
+    mesh, maps = build_box_mesh(g["box"], nx, ny, degree_sol=int(g["p"]), n_comp=1)
+    law = L.burgers_spacetime() if "burgers" in name else L.linear_advection((1.0, 0.5))
+    return g, law, mesh, maps, get_geometry(mesh, maps)
+
+
+SCALAR = ["tracking_burgers_p2", "tracking_burgers_p1", "tracking_linadv_p1"]
+
+
+@pytest.mark.parametrize("name", SCALAR)
+def test_scalar_law_assembly_matches_reference(name):
+    """assemble_global / assemble_enriched / assemble_distortion for the reference's scalar laws
+    (position-dependent source included) vs the reference's CSR products."""
+    from paper_2305_15661_b200.configs import DistortionConfig
+    from paper_2305_15661_b200.fullspace import assemble_distortion, assemble_enriched, assemble_global
+
+    g, law, mesh, maps, geom = _scalar_case(name)
+    U, x, mu = g["U"], g["x"], g["mu"]
+    R, JU, JX = assemble_global(law, mesh, maps, U, x, mu, geom=geom)
+    assert rel_err(R, g["glob_R"]) < TOL
+    assert rel_err(JU @ g["v_u"], g["glob_JU_v"]) < TOL and rel_err(JU.T @ g["u_r"], g["glob_JUt_u"]) < TOL
+    assert rel_err(JX @ g["v_x"], g["glob_JX_v"]) < TOL and rel_err(JX.T @ g["u_r"], g["glob_JXt_u"]) < TOL
+    Rb, EU, EX = assemble_enriched(law, mesh, maps, U, x, mu, geom=geom)
+    assert rel_err(Rb, g["enr_R"]) < TOL
+    assert rel_err(EU @ g["v_u"], g["enr_JU_v"]) < TOL and rel_err(EU.T @ g["u_e"], g["enr_JUt_u"]) < TOL
+    assert rel_err(EX @ g["v_x"], g["enr_JX_v"]) < TOL and rel_err(EX.T @ g["u_e"], g["enr_JXt_u"]) < TOL
+    N, JN = assemble_distortion(mesh, maps, x, DistortionConfig(1e-3), geom=geom)
+    assert rel_err(N, g["dist_N"], max(np.max(np.abs(g["dist_N"])), 1e-12)) < 1e-8  # N = kappa (eta - eta_ref): a difference
+    assert rel_err(JN @ g["v_x"], g["dist_JN_v"]) < TOL
+
+
+@pytest.mark.parametrize("name", ["burgers_st_p1", "burgers_st_p2", "linadv_p1", "linadv_p2", "strip"])
+def test_scalar_element_jacobians_match_reference_goldens(name):
+    """fullspace.element_jacobians for the scalar laws vs the reference's elemental_residual
+    blocks stored in the round-1 goldens (dg.py:197-225)."""
+    from paper_2305_15661_b200.fullspace import element_jacobians
+
+    case, g = build(name)
+    U = case.phi @ g["w"] + (case.state_offset if case.state_offset is not None else 0.0)
+    x = case.ref_coords + case.psi @ g["tau"]
+    res, js, jn, jx = element_jacobians(case.law, case.geom, U, x, case.mus[0])
+    elems = sorted({int(k[4:].split("_")[0]) for k in g if k.startswith("elem") and k.endswith("_res")})
+    assert elems
+    for e in elems:
+        scale = np.max(np.abs(g[f"elem{e}_jself"]))
+        assert rel_err(res[e], g[f"elem{e}_res"], max(np.max(np.abs(g[f"elem{e}_res"])), 1e-8 * scale)) < 1e-9
+        assert rel_err(js[e], g[f"elem{e}_jself"]) < TOL
+        assert rel_err(jn[e], g[f"elem{e}_jneigh"], scale) < TOL
+        assert rel_err(jx[e], g[f"elem{e}_jcoord"], max(np.max(np.abs(g[f"elem{e}_jcoord"])), 1e-8 * scale)) < 1e-9
+
+
+@pytest.mark.parametrize("name", SCALAR)
+def test_scalar_tracking_lm_matches_reference(name):
+    """Full-space tracking of the reference's Burgers / advection problems: Gauss-Newton blocks
+    and the lm_solve history row for row against the reference."""
+    from paper_2305_15661_b200.configs import DistortionConfig
+    from paper_2305_15661_b200.lm import LmConfig, lm_solve
+    from paper_2305_15661_b200.tracking import TrackingProblem
+
+    g, law, mesh, maps, geom = _scalar_case(name)
+    prob = TrackingProblem(law, mesh, maps, g["mu"], DistortionConfig(1e-3), U0=g["U"], x0=g["x"], geom=geom)
+    w0, z0 = prob.initial_guess()
+    assert rel_err(prob.objective(w0, z0), g["fs_obj"]) < TOL
+    J, S, T, Hww, Hwt, Htt = prob.derivatives(w0, z0)
+    assert rel_err(J, g["fs_J"]) < TOL and rel_err(S, g["fs_S"]) < TOL and rel_err(T, g["fs_T"]) < TOL
+    assert rel_err(Hww @ g["fs_a"], g["fs_Hww_a"]) < TOL and rel_err(Hwt @ g["fs_b"], g["fs_Hwt_b"]) < TOL
+    assert rel_err(Htt @ g["fs_b"], g["fs_Htt_b"]) < TOL
+    res = lm_solve(prob, LmConfig(max_iters=3), w0_mode="keep")
+    hist, ref = res.history, g["fs_lm_hist"]
+    assert hist.shape == ref.shape and str(res.reason) == str(g["fs_lm_reason"])
+    assert np.array_equal(hist[:, 5], ref[:, 5]) and rel_err(hist[:, 4], ref[:, 4]) < 1e-8
+    assert rel_err(hist[:, 1], ref[:, 1], np.max(np.abs(ref[:, 1]))) < 1e-8
+    assert rel_err(res.w, g["fs_lm_w"]) < 1e-7
