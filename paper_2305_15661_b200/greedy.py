@@ -186,22 +186,32 @@ def tracking_alignment(law, geom, dist_config, lm_config=None, device=None):
 
 
 def tracking_snapshot(law, geom, dist_config, lm_config=None, track=True, hdm_tol=1e-10, device=None):
-    """``hdm_snapshot(mu, x_aligned) -> (U*, x*)``: the HDM solve on the aligned mesh
-    (``fullspace.solve_hdm``, dg.py:343-400) and, with ``track``, the full-space tracking solve
-    on the enriched residual from there (tracking.py:41-150; SPEC seed: Phi = I, Psi = I,
-    rho = 1), both on GPU-assembled residuals and sparse Jacobians."""
-    from .fullspace import solve_hdm
+    """``hdm_snapshot(mu, x_aligned) -> (U*, x*)``: with ``track``, the full-space tracking solve
+    on the enriched residual from the law's initial guess on the aligned mesh (tracking.py:41-150;
+    SPEC seed: Phi = I, Psi = I, rho = 1), then the HDM solve on the tracked mesh
+    (``fullspace.solve_hdm``, dg.py:343-400: plain Newton suffices on a feature-aligned mesh) —
+    both on GPU-assembled residuals and sparse Jacobians.  An HDM solve that does not converge
+    keeps the tracked state with a warning."""
+    import warnings
+
+    from .fullspace import HdmSolveError, initial_state, solve_hdm
     from .lm import LmConfig, lm_solve
     from .tracking import TrackingProblem
 
     def hdm_snapshot(mu, x_aligned, U_init=None):
         mesh, maps = geom.mesh, geom.maps
-        U = solve_hdm(law, mesh, maps, x_aligned, mu, U_init=U_init, tol=hdm_tol, geom=geom, device=device)
-        if not track:
-            return U, np.asarray(x_aligned, dtype=float).copy()
-        prob = TrackingProblem(law, mesh, maps, mu, dist_config, U0=U, x0=x_aligned, geom=geom, device=device)
-        res = lm_solve(prob, lm_config or LmConfig(max_iters=20), w0_mode="keep")
-        return res.w, prob.coords_from(res.tau)
+        x = np.asarray(x_aligned, dtype=float).copy()
+        U = initial_state(law, mesh, maps, x, mu, geom) if U_init is None else np.asarray(U_init, dtype=float)
+        if track:
+            prob = TrackingProblem(law, mesh, maps, mu, dist_config, U0=U, x0=x, geom=geom, device=device)
+            res = lm_solve(prob, lm_config or LmConfig(max_iters=50), w0_mode="keep")
+            U, x = res.w, prob.coords_from(res.tau)
+        try:
+            U = solve_hdm(law, mesh, maps, x, mu, U_init=U, tol=hdm_tol, geom=geom, device=device)
+        except HdmSolveError as exc:
+            warnings.warn(f"HDM solve at mu={np.asarray(mu).tolist()} stopped at |R| = {exc.residual_norm:.2e}; "
+                          "the tracked state is kept")
+        return U, x
 
     return hdm_snapshot
 
