@@ -525,6 +525,109 @@ def run_cfg5(args, dev, world, rank, local, group=None):
             "clocks": clocks}
 
 
+def _fullspace_case(n_radial, n_circ, seed=6):
+    from paper_2305_15661_b200 import configs, laws as L
+
+    case = configs.sector_rom_case(n_radial, n_circ, 2, 1, 0.5, 2.0, 1, seed=seed, name="fullspace", wall="extrapolate")
+    rng = np.random.default_rng(seed)
+    ne = case.mesh.num_elements
+    U = np.tile(L.euler_freestream(3.0), ne * 6) * (1.0 + 0.03 * rng.standard_normal(ne * 24))
+    return case, U, case.ref_coords.copy(), np.array([3.0])
+
+
+def _fullspace_cpu(_):
+    """Stock reference assemble_enriched (dg.py:275-326) on a 400-triangle sector: elements/s."""
+    from oracle import strom_ref
+
+    strom_ref.load()
+    import strom.dg as sdg
+
+    case, U, x, mu = _fullspace_case(10, 20)
+    rop = strom_ref.operator(case)
+    t0 = time.perf_counter()
+    sdg.assemble_enriched(case.law, rop.geom.mesh, rop.geom.maps, U, x, mu)
+    return case.mesh.num_elements / (time.perf_counter() - t0)
+
+
+def run_fullspace(args, dev, local):
+    """SURVEY §8f-3 measurement: one enriched full-space assembly (dg.py:275-326: residual against
+    the degree-3 test space with dR/dU, dR/dx blocks, N_e and dN_e/dx) of a 4,000-triangle
+    sector. Device time of the K1 pass (CUDA events), e2e of the public assemble_enriched (host
+    state in, scipy CSR out: H2D of U and x, D2H of the records, host scatter)."""
+    import torch
+
+    from paper_2305_15661_b200 import _lib, fullspace
+    from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases
+
+    case, U, x, mu = _fullspace_case(25, 80)
+    ne = case.mesh.num_elements
+    geom = case.geom
+    op = GpuReducedOperator(case.law, geom, ReducedBases(np.zeros((U.size, 0)), np.zeros((x.size, 0)), x),
+                            fullspace._NoDistortion(), device=dev, state_offset=U)
+    phi_t, dphi_t, trace_t = fullspace.test_space_tables(op.dm.tabs, 3)
+    _lib.check(op._lib.strom_set_test_space(op._h, 10, phi_t.ctypes.data, dphi_t.ctypes.data, trace_t.ctypes.data),
+               "strom_set_test_space")
+    rec = 40 * (1 + 4 * 24 + 6) + 7
+    out = torch.empty(ne * rec, dtype=torch.float64, device=dev)
+    W = torch.zeros((1, 1), dtype=torch.float64, device=dev)
+    Mu = torch.as_tensor(mu[None]).to(dev)
+    for _ in range(3):
+        op.eval_batched(_lib.ELEMJAC_ENRICHED, W, W, Mu, None, out=out)
+    torch.cuda.synchronize()
+    steps = 10
+    clk = Clocks(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.current_stream()
+    e0.record(st)
+    for _ in range(steps):
+        op.eval_batched(_lib.ELEMJAC_ENRICHED, W, W, Mu, None, out=out)
+    e1.record(st)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / steps
+    fullspace.assemble_enriched(case.law, case.mesh, case.maps, U, x, mu, geom=geom, device=dev)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        Rb, JU, JX = fullspace.assemble_enriched(case.law, case.mesh, case.maps, U, x, mu, geom=geom, device=dev)
+    e2e_s = (time.perf_counter() - t0) / 3
+    wbytes = ne * rec * 8.0
+    rbytes = ne * (24 * 8.0 * 4 + 64)  # own + neighbor state rows, indices, coordinates (approx.)
+    peak = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak = float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        peak = 6500.0
+    res = {"metric": "full-space enriched element Jacobian evals/sec (fp64)", "value": ne / (ms / 1e3),
+           "unit": "elements/s", "higher_is_better": True, "ms_per_step": ms, "steps": steps,
+           "config": {"workload": "4,000-triangle half-cylinder sector, Euler p=2, degree-3 test space (40 rows/element), "
+                                  "one STROM_ELEMJAC_ENRICHED pass: 4,127 doubles written per element"},
+           "roofline": {"bound": "hbm", "achieved": (wbytes + rbytes) / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": (wbytes + rbytes) / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                        "bytes_per_launch": wbytes + rbytes,
+                        "note": "one warp per element, plain per-lane contraction loops: an offline path, far from the HBM bound"},
+           "e2e": {"value": ne / e2e_s, "unit": "elements/s", "h2d_bytes_per_step": 8 * (U.size + x.size),
+                   "d2h_bytes_per_step": 8 * (int(JU.nnz) + int(JX.nnz) + ne * 47), "csr_nnz": [int(JU.nnz), int(JX.nnz)],
+                   "note": "assemble_enriched on a warm operator: H2D of U and x, K1 pass, device gather of the CSR values "
+                           "on the cached pattern, D2H of the nnz values, residual rows and distortion columns"},
+           "clocks": clocks}
+    if not args.no_cpu_baseline:
+        try:
+            import concurrent.futures as cf
+
+            n = min(16, os.cpu_count() or 1)
+            with cf.ProcessPoolExecutor(max_workers=n) as ex:
+                t0 = time.perf_counter()
+                rates = list(ex.map(_fullspace_cpu, range(n)))
+                wall = time.perf_counter() - t0
+            res["cpu_baseline"] = {"value": n * 400 / wall, "unit": "elements/s", "cores": n, "kind": "reference",
+                                   "sample": f"stock strom.dg.assemble_enriched on a 400-triangle sector per process x {n} "
+                                             f"processes (wall incl. geometry set-up); per-process rate {np.mean(rates):.0f} el/s"}
+        except Exception as exc:  # the reference is test infrastructure: absent -> no baseline
+            res["cpu_baseline"] = {"unavailable": str(exc)[:200]}
+    return res
+
+
 def _lm_stats(op):
     """(control rounds, derivative passes, objective passes) of the op's last batched solve."""
     import ctypes
@@ -669,6 +772,9 @@ def run_mine(args):
         n_out = 1 + ku + kx + ku * ku + ku * kx + kx * kx
         e2e_io = (8 * (ku + kx + op.n_mu) + 8 * n_out, 2 * 8 * n_out + 4)
     gn = None if args.no_gn else run_gn(args, dev, world, rank, local)
+    fs = None
+    if rank == 0 and world == 1 and not args.no_fullspace:
+        fs = run_fullspace(args, dev, local)
     cfg4 = cfg5 = None
     if not args.no_sharded:
         cfg4 = run_cfg4(args, dev, world, rank, local)
@@ -709,6 +815,8 @@ def run_mine(args):
         line["gn"] = gn
     if cfg4 is not None:
         line["cfg4"], line["cfg5"] = cfg4, cfg5
+    if fs is not None:
+        line["fullspace"] = fs
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(n=args.cpu_n)
         if gn is not None:
@@ -730,6 +838,7 @@ def main():
     ap.add_argument("--no-gn", action="store_true", help="skip the config-3 Gauss-Newton solves/s measurement")
     ap.add_argument("--gn-steps", type=int, default=20, help="timed 64-mu LM batches of the GN measurement")
     ap.add_argument("--no-sharded", action="store_true", help="skip the config-4 / config-5 sharded measurements")
+    ap.add_argument("--no-fullspace", action="store_true", help="skip the full-space enriched assembly measurement")
     ap.add_argument("--no-graph", action="store_true", help="time the config-2 step with eager launches")
     ap.add_argument("--cfg-steps", type=int, default=3, help="timed steps of the config-4 / config-5 measurements")
     args = ap.parse_args()

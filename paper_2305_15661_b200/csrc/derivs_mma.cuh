@@ -786,22 +786,23 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         }
         eo[NT + i] = v;
       }
-      for (int i = lane; i < NT * 3 * NU; i += 32) {  // dR/dU_nbr: the neighbor's face-node columns
-        const int row = i / (3 * NU), col = i % (3 * NU), n = row / M, c = row % M;
-        const int f = col / NU, node = (col % NU) / M, cp = col % M;
+      // dR/dU_nbr: zero, then the 12 face-node columns of each interior face's neighbor
+      for (int i = lane; i < NT * 3 * NU; i += 32) eo[NT + NT * NU + i] = 0.0;
+      __syncwarp();
+      for (int i = lane; i < NT * 3 * NF * M; i += 32) {
+        const int row = i / (3 * NF * M), rem = i % (3 * NF * M), n = row / M, c = row % M;
+        const int f = rem / (NF * M), jn = (rem / M) % NF, cp = rem % M;
         const int fi = EI[7 + f];
+        if ((fi >> 3) != 0) continue;
+        const int nf = fi & 3;
+        const int node = jn == 0 ? nf : (jn == 1 ? (nf + 1) % 3 : 3 + nf);
         double v = 0.0;
-        if ((fi >> 3) == 0) {
-          const int nf = fi & 3;
-          const int jn = node == nf ? 0 : (node == (nf + 1) % 3 ? 1 : (node == 3 + nf ? 2 : -1));
-          if (jn >= 0)
-            for (int s = 0; s < NS; ++s) {
-              const int sp = ((fi >> 2) & 1) ? NS - 1 - s : s;
-              v = fma(ttr[(f * NS + s) * NBT + n] * T.trace[0][sp][jn],
-                      RA[SH::CF + SH::CFS + (c * M + cp) * NFSP + f * NS + s], v);
-            }
+        for (int s = 0; s < NS; ++s) {
+          const int sp = ((fi >> 2) & 1) ? NS - 1 - s : s;
+          v = fma(ttr[(f * NS + s) * NBT + n] * T.trace[0][sp][jn],
+                  RA[SH::CF + SH::CFS + (c * M + cp) * NFSP + f * NS + s], v);
         }
-        eo[NT + NT * NU + i] = v;
+        eo[NT + NT * NU + (size_t)row * 3 * NU + f * NU + node * M + cp] = v;
       }
       if (lane < 7) eo[(size_t)NT * (1 + 4 * NU + 6) + lane] = lane == 0 ? S[SH::MN] : S[SH::DNX + lane - 1];
       __syncwarp();

@@ -40,7 +40,7 @@ def test_space_tables(tabs, degree):
 
 
 def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenerate=True, test_degree=None,
-                     columns=None):
+                     columns=None, on_device=False):
     """Element records at the global state U and coordinates x: (ne, EJ_SIZE) STROM_ELEMJAC
     records (4-component laws, p = 2), or with ``test_degree`` the STROM_ELEMJAC_ENRICHED records
     (ne, NT (1 + 4 n_u + 6) + 7) for any compiled law and degree.  ``columns`` limits what is
@@ -52,17 +52,32 @@ def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenera
         raise NotImplementedError("STROM_ELEMJAC records: 4-component laws with p = 2 (pass test_degree)")
     U = np.asarray(U, dtype=float).reshape(-1)
     x = np.asarray(x, dtype=float).reshape(-1)
-    bases = ReducedBases(np.zeros((U.size, 0)), np.zeros((x.size, 0)), x)
-    op = GpuReducedOperator(law, geom, bases, dist or _NoDistortion(), device=device, state_offset=U)
+    # one operator per (geometry, law, distortion constants, device): later calls only refresh the
+    # state and coordinate vectors in place (an LM tracking solve evaluates dozens of times)
+    d = dist or _NoDistortion()
+    cache = geom.__dict__.setdefault("_b200_fullspace_ops", {})
+    key = (id(law), float(d.kappa), float(d.eps), str(device))
+    op = cache.get(key)
+    if op is None or op.law is not law:
+        bases = ReducedBases(np.zeros((U.size, 0)), np.zeros((x.size, 0)), x)
+        op = cache[key] = GpuReducedOperator(law, geom, bases, d, device=device, state_offset=U)
+        op._test_degree = None
+    else:
+        op.u0.copy_(torch.as_tensor(U))
+        op.ref_coords.copy_(torch.as_tensor(x))
     W = torch.zeros((1, op.k_u), dtype=torch.float64, device=op.device)
     Tau = torch.zeros((1, 1), dtype=torch.float64, device=op.device)
     Mu = torch.as_tensor(op._mu(mu)[None]).to(op.device)
     mode, rec = _lib.ELEMJAC, EJ_SIZE
     if test_degree is not None:
-        phi_t, dphi_t, trace_t = test_space_tables(op.dm.tabs, test_degree)
-        nbt = dphi_t.shape[1]
-        _lib.check(op._lib.strom_set_test_space(op._h, nbt, phi_t.ctypes.data, dphi_t.ctypes.data,
-                                                trace_t.ctypes.data), "strom_set_test_space")
+        from .tables import lagrange_nodes
+
+        nbt = lagrange_nodes(test_degree).shape[0]
+        if op._test_degree != test_degree:
+            phi_t, dphi_t, trace_t = test_space_tables(op.dm.tabs, test_degree)
+            _lib.check(op._lib.strom_set_test_space(op._h, nbt, phi_t.ctypes.data, dphi_t.ctypes.data,
+                                                    trace_t.ctypes.data), "strom_set_test_space")
+            op._test_degree = test_degree
         nu = op.dm.nu
         mode, rec = _lib.ELEMJAC_ENRICHED, maps.n_comp * nbt * (1 + 4 * nu + 6) + 7
     out = torch.empty(mesh.num_elements * rec, dtype=torch.float64, device=op.device)
@@ -75,6 +90,8 @@ def _element_records(law, geom, U, x, mu, dist=None, device=None, raise_degenera
         op._lib.strom_degenerate_elements(op._h, 0, ids.ctypes.data, n)
         raise degenerate_error(ids[:n].astype(np.int64))
     out = out.view(mesh.num_elements, rec)
+    if on_device:
+        return out
     return (out if columns is None else out[:, columns].contiguous()).cpu().numpy()
 
 
@@ -161,33 +178,123 @@ def assemble_global(law, mesh, maps, U, x, mu, want_jacobians=True, geom=None, d
     from .mesh import get_geometry
 
     geom = geom or get_geometry(mesh, maps)
-    if not want_jacobians:
-        bases = ReducedBases(np.zeros((np.size(U), 0)), np.zeros((np.size(x), 0)), np.asarray(x, float).ravel())
-        op = GpuReducedOperator(law, geom, bases, _NoDistortion(), device=device, state_offset=np.asarray(U, float))
-        from .reduced import ReducedCoords
+    if not want_jacobians:  # residual rows only (the same cached operator, nothing but the rows copied back)
+        return element_blocks(law, geom, U, x, mu, want_jacobians=False, device=device)[0].reshape(-1).copy(), None, None
+    res, dRdU, dRdx, _, _ = assemble_blocks_csr(law, geom, U, x, mu, None, device=device, rows=maps.state_map)
+    return res.reshape(-1).copy(), dRdU, dRdx
 
-        return op.global_residual(ReducedCoords(np.zeros(0), np.zeros(0)), mu), None, None
-    res, jac_self, jac_neigh, jac_coord = element_jacobians(law, geom, U, x, mu, device)
-    R = res.reshape(-1)
-    dRdU, dRdx = _scatter_csr(maps, maps.state_map[:, :, None], jac_self, jac_neigh, jac_coord, maps.n_global_state)
-    return R, dRdU, dRdx
+
+def _csr_pattern(r, c, shape):
+    """Sorted, duplicate-free CSR structure of the COO coordinates (r, c): (order, starts,
+    indptr, indices) with data_csr = add.reduceat(data_coo[order], starts) — what
+    ``coo_matrix(...).tocsr()`` computes, with the sort done once per mesh."""
+    key = r.astype(np.int64) * shape[1] + c
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    first = np.flatnonzero(np.r_[True, ks[1:] != ks[:-1]])
+    rows = (ks[first] // shape[1]).astype(np.int64)
+    indices = (ks[first] % shape[1]).astype(np.int32)
+    indptr = np.zeros(shape[0] + 1, dtype=np.int32)
+    np.cumsum(np.bincount(rows, minlength=shape[0]), out=indptr[1:])
+    return order, first, indptr, indices
 
 
 def _scatter_csr(maps, rows, jac_self, jac_neigh, jac_coord, n_rows):
-    """CSR dR/dU and dR/dx from element blocks (the index construction of dg.py:246-271)."""
-    r1 = np.broadcast_to(rows, jac_self.shape).ravel()
-    c1 = np.broadcast_to(maps.state_map[:, None, :], jac_self.shape).ravel()
+    """CSR dR/dU and dR/dx from element blocks: the index construction of dg.py:246-271 (self and
+    neighbor blocks concatenated, entries of missing neighbors masked to zero at column 0,
+    duplicates summed); the sorted structure is cached on ``maps`` per block shape."""
+    cache = maps.__dict__.setdefault("_b200_csr_patterns", {})
+    ck = (jac_self.shape, n_rows, int(rows[0, 0, 0]), int(rows[-1, -1, 0]))
     nmap = maps.neighbor_map
     valid = nmap >= 0
-    r2 = np.broadcast_to(rows, jac_neigh.shape).ravel()
-    c2 = np.broadcast_to(np.clip(nmap, 0, None)[:, None, :], jac_neigh.shape).ravel()
-    d2 = (jac_neigh * valid[:, None, :]).ravel()
-    dRdU = sp.coo_matrix((np.concatenate([jac_self.ravel(), d2]), (np.concatenate([r1, r2]), np.concatenate([c1, c2]))),
-                         shape=(n_rows, maps.n_global_state)).tocsr()
-    r3 = np.broadcast_to(rows, jac_coord.shape).ravel()
-    c3 = np.broadcast_to(maps.coord_map[:, None, :], jac_coord.shape).ravel()
-    dRdx = sp.coo_matrix((jac_coord.ravel(), (r3, c3)), shape=(n_rows, maps.n_global_coord)).tocsr()
+    if ck not in cache:
+        r1 = np.broadcast_to(rows, jac_self.shape).ravel()
+        c1 = np.broadcast_to(maps.state_map[:, None, :], jac_self.shape).ravel()
+        r2 = np.broadcast_to(rows, jac_neigh.shape).ravel()
+        c2 = np.broadcast_to(np.clip(nmap, 0, None)[:, None, :], jac_neigh.shape).ravel()
+        r3 = np.broadcast_to(rows, jac_coord.shape).ravel()
+        c3 = np.broadcast_to(maps.coord_map[:, None, :], jac_coord.shape).ravel()
+        cache[ck] = (_csr_pattern(np.concatenate([r1, r2]), np.concatenate([c1, c2]), (n_rows, maps.n_global_state)),
+                     _csr_pattern(r3, c3, (n_rows, maps.n_global_coord)))
+    (ou, su, pu, iu), (ox, sx, px, ix) = cache[ck]
+    vals = np.concatenate([jac_self.ravel(), (jac_neigh * valid[:, None, :]).ravel()])
+    dRdU = sp.csr_matrix((np.add.reduceat(vals[ou], su), iu, pu), shape=(n_rows, maps.n_global_state))
+    dRdx = sp.csr_matrix((np.add.reduceat(jac_coord.ravel()[ox], sx), ix, px), shape=(n_rows, maps.n_global_coord))
     return dRdU, dRdx
+
+
+def assemble_blocks_csr(law, geom, U, x, mu, test_degree=None, dist=None, device=None, rows=None):
+    """One K1 pass and the CSR Jacobians straight from the device records:
+    (res (ne, NT), dR/dU csr, dR/dx csr, N (ne,), dN/dx_e (ne, 6)).
+
+    The sorted CSR structure of dg.py:246-271 is fixed per (mesh, test space), so it is built once
+    (``_csr_pattern``) together with, for every stored entry, the record position that holds its
+    value: duplicates of the reference's COO list are only the masked entries of missing
+    neighbors (exact zeros in the records), so a device gather of one position per entry equals
+    the reference's duplicate sum.  Per call the GPU gathers the nnz values and only they, the
+    residual rows and the distortion columns cross to the host.  ``rows`` (ne, NT) global row ids
+    (default: element-major test rows, ``assemble_enriched``; ``maps.state_map`` for
+    ``assemble_global``)."""
+    import torch
+
+    from .tables import lagrange_nodes
+
+    maps = geom.maps
+    m, p, ne = maps.n_comp, maps.degree_sol, geom.mesh.num_elements
+    nu = lagrange_nodes(p).shape[0] * m
+    plain_mma = test_degree is None and m == 4 and p == 2
+    deg = p if test_degree is None else test_degree
+    NT = lagrange_nodes(deg).shape[0] * m
+    out = _element_records(law, geom, U, x, mu, dist=dist, device=device, test_degree=None if plain_mma else deg,
+                           on_device=True)
+    rec = out.shape[1]
+    a, b, c, d = NT, NT + NT * nu, NT + 4 * NT * nu, NT * (1 + 4 * nu + 6)
+    if rows is None:
+        rows = (np.arange(ne)[:, None] * NT + np.arange(NT)[None, :]).astype(np.int64)
+        n_rows = ne * NT
+    else:
+        n_rows = maps.n_global_state
+    cache = maps.__dict__.setdefault("_b200_csr_device", {})
+    ck = (NT, nu, n_rows, int(rows[0, 0]), int(rows[-1, -1]), str(out.device))
+    if ck not in cache:
+        base = (np.arange(ne, dtype=np.int64) * rec)[:, None, None]
+        rr = rows[:, :, None]
+        pos_s = base + a + (np.arange(NT)[None, :, None] * nu + np.arange(nu)[None, None, :])
+        pos_n = base + b + (np.arange(NT)[None, :, None] * 3 * nu + np.arange(3 * nu)[None, None, :])
+        pos_x = base + c + (np.arange(NT)[None, :, None] * 6 + np.arange(6)[None, None, :])
+        nmap = maps.neighbor_map
+        r_u = np.concatenate([np.broadcast_to(rr, pos_s.shape).ravel(), np.broadcast_to(rr, pos_n.shape).ravel()])
+        c_u = np.concatenate([np.broadcast_to(maps.state_map[:, None, :], pos_s.shape).ravel(),
+                              np.broadcast_to(np.clip(nmap, 0, None)[:, None, :], pos_n.shape).ravel()])
+        real = np.concatenate([np.ones(pos_s.size, bool), np.broadcast_to((nmap >= 0)[:, None, :], pos_n.shape).ravel()])
+        src = np.concatenate([pos_s.ravel(), pos_n.ravel()])
+        # real entries first within a duplicate group (stable sort on (key, not real))
+        key = r_u.astype(np.int64) * maps.n_global_state + c_u
+        order = np.lexsort((~real, key))
+        ks = key[order]
+        first = np.flatnonzero(np.r_[True, ks[1:] != ks[:-1]])
+        n_real = np.add.reduceat(real[order].astype(np.int64), first)
+        if np.any(n_real > 1):
+            raise NotImplementedError("two element blocks share a Jacobian entry (not a conforming mesh)")
+        indptr = np.zeros(n_rows + 1, dtype=np.int32)
+        np.cumsum(np.bincount(ks[first] // maps.n_global_state, minlength=n_rows), out=indptr[1:])
+        pu = (torch.as_tensor(src[order][first]).to(out.device), indptr, (ks[first] % maps.n_global_state).astype(np.int32))
+        ox, fx, px, ix = _csr_pattern(np.broadcast_to(rr, pos_x.shape).ravel(),
+                                      np.broadcast_to(maps.coord_map[:, None, :], pos_x.shape).ravel(),
+                                      (n_rows, maps.n_global_coord))
+        if len(fx) != pos_x.size:
+            raise NotImplementedError("duplicate coordinate columns within an element")
+        cache[ck] = (pu, (torch.as_tensor(pos_x.ravel()[ox]).to(out.device), px, ix))
+    (gu, pu_, iu), (gx, px, ix) = cache[ck]
+    flat = out.view(-1)
+    small = torch.cat([out[:, :NT].reshape(-1), out[:, d:d + 7].reshape(-1)])
+    host = torch.cat([flat[gu], flat[gx], small]).cpu().numpy()
+    nu_, nx_ = gu.numel(), gx.numel()
+    dRdU = sp.csr_matrix((host[:nu_], iu, pu_), shape=(n_rows, maps.n_global_state))
+    dRdx = sp.csr_matrix((host[nu_:nu_ + nx_], ix, px), shape=(n_rows, maps.n_global_coord))
+    res = host[nu_ + nx_:nu_ + nx_ + ne * NT].reshape(ne, NT)
+    nd = host[nu_ + nx_ + ne * NT:].reshape(ne, 7)
+    return res, dRdU, dRdx, nd[:, 0], nd[:, 1:]
 
 
 def enriched_records(law, geom, U, x, mu, test_degree=None, dist=None, want_jacobians=True, device=None,
@@ -203,15 +310,12 @@ def assemble_enriched(law, mesh, maps, U, x, mu, test_degree=None, want_jacobian
     from .mesh import get_geometry
 
     geom = geom or get_geometry(mesh, maps)
-    res, js, jn, jc, _, _ = enriched_records(law, geom, U, x, mu, test_degree, want_jacobians=want_jacobians,
-                                             device=device)
-    Rbar = res.reshape(-1).copy()
+    deg = maps.degree_sol + 1 if test_degree is None else test_degree
     if not want_jacobians:
-        return Rbar, None, None
-    ne, n_t = res.shape
-    rows = (np.arange(ne)[:, None] * n_t + np.arange(n_t)[None, :]).astype(np.int64)[:, :, None]
-    dRdU, dRdx = _scatter_csr(maps, rows, js, jn, jc, ne * n_t)
-    return Rbar, dRdU, dRdx
+        res = element_blocks(law, geom, U, x, mu, deg, want_jacobians=False, device=device)[0]
+        return res.reshape(-1).copy(), None, None
+    res, dRdU, dRdx, _, _ = assemble_blocks_csr(law, geom, U, x, mu, deg, device=device)
+    return res.reshape(-1).copy(), dRdU, dRdx
 
 
 class HdmSolveError(RuntimeError):

@@ -1,9 +1,9 @@
 # round-end GPU session (part 2): launch list + ncu --set full of K1 (kept) and K2 (raw csv only:
 # gpurun copies back at most 64 MiB)
 mkdir -p gpurun_out
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-gn --no-sharded > gpurun_out/bench_small.log 2>&1 && \
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-gn --no-sharded --no-fullspace > gpurun_out/bench_small.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-gn --no-sharded > gpurun_out/ncu_launch.log 2>&1
+    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-gn --no-sharded --no-fullspace > gpurun_out/ncu_launch.log 2>&1
 bash tools/prof_k1.sh > gpurun_out/prof_k1.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:^value_mma -s 3 -c 1 -o /tmp/prof_k2 -f \
     python tools/prof_value.py > gpurun_out/ncu_k2.log 2>&1 && \
