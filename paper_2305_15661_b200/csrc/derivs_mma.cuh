@@ -27,6 +27,9 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_GFRAG
 #define STROM_GFRAG 1  // gradient S / T accumulated from the J accumulator fragments (0: from Jt in shared memory)
 #endif
+#ifndef STROM_HDIRECT
+#define STROM_HDIRECT 0  // Gram DMMAs accumulate straight into the register Gram on sqrt(rho)-scaled fragments
+#endif
 #ifndef STROM_MMA_MAXNREG
 #define STROM_MMA_MAXNREG 168  // 3 warps per SMSP (12 per SM with 15 KB of smem per warp)
 #endif
@@ -1089,7 +1092,25 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
 #pragma unroll
           for (int rs = 0; rs < NU / 4; ++rs) fr[cc][rs] = Jt[(rs * 4 + (lane & 3)) * LDJ + cc * 8 + (lane >> 2)];
         constexpr int NTRI = NT8C * (NT8C + 1) / 2;
-        double gc[NTRI][2];  // all upper tiles in flight: k-step outer, independent chains inner
+        constexpr bool HDIRECT = HREG && STROM_HDIRECT;
+        if constexpr (HDIRECT) {
+          const double sr = sqrt(rho);
+#pragma unroll
+          for (int cc = 0; cc < NT8C; ++cc)
+#pragma unroll
+            for (int rs = 0; rs < NU / 4; ++rs) fr[cc][rs] *= sr;
+#pragma unroll
+          for (int rs = 0; rs < NU / 4; ++rs)
+#pragma unroll
+            for (int ti = 0; ti < NT8C; ++ti)
+#pragma unroll
+              for (int tj = ti; tj < NT8C; ++tj) {
+                const int t = SH::tri_tile(ti, tj, NT8C);
+                dmma(hacc[t][0], hacc[t][1], fr[ti][rs], fr[tj][rs]);
+              }
+        }
+        double gc[HDIRECT ? 1 : NTRI][2];  // all upper tiles in flight: k-step outer, independent chains inner
+        if constexpr (!HDIRECT) {
 #pragma unroll
         for (int t = 0; t < NTRI; ++t) gc[t][0] = gc[t][1] = 0.0;
 #pragma unroll
@@ -1101,6 +1122,8 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
               const int t = SH::tri_tile(ti, tj, NT8C);
               dmma(gc[t][0], gc[t][1], fr[ti][rs], fr[tj][rs]);
             }
+        }
+        if constexpr (!HDIRECT)
 #pragma unroll
         for (int ti = 0; ti < NT8C; ++ti)
 #pragma unroll
