@@ -185,6 +185,17 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     for (int ti = 0; ti < KP / 8; ++ti)
       for (int tj = ti; tj < KP / 8; ++tj) s_tile[t++] = (ti << 4) | tj;
   }
+  // enriched mode: the test tabulations ([NQ][NBT][2] gradients, [3][NS][NBT] traces) staged in
+  // shared memory (generic instantiation only; up to the degree-3 space, else read from global)
+  constexpr int TT_MAX = DM < 0 ? (NQ * 2 + 3 * NS) * 10 : 1;
+  __shared__ double s_tt[TT_MAX];
+  const double* tt_base = r.test_tab;
+  if constexpr (DM < 0) {
+    if (EJT && (NQ * 2 + 3 * NS) * r.test_nb <= TT_MAX) {
+      for (int i = threadIdx.x; i < (NQ * 2 + 3 * NS) * r.test_nb; i += blockDim.x) s_tt[i] = r.test_tab[i];
+      tt_base = s_tt;
+    }
+  }
   LawArgs la;
 #pragma unroll
   for (int i = 0; i < 8; ++i) la.p[i] = r.lawp[i];
@@ -734,8 +745,8 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     if (EJT) {
       __syncwarp();  // FD slots written above
       const int NBT = r.test_nb, NT = NBT * M;
-      const double* __restrict__ tdphi = r.test_tab;              // [NQ][NBT][2]
-      const double* __restrict__ ttr = r.test_tab + NQ * NBT * 2;  // [3][NS][NBT]
+      const double* tdphi = tt_base;               // [NQ][NBT][2]
+      const double* ttr = tt_base + NQ * NBT * 2;  // [3][NS][NBT]
       double* const eo = r.out + (size_t)e * (NT * (1 + 4 * NU + 6) + 7);
       const double* adj = S + SH::MADJ;
       for (int i = lane; i < NT; i += 32) {  // residual row (n, c) and its six mesh derivatives
