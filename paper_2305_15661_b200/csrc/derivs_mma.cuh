@@ -24,18 +24,13 @@ constexpr int MTHREADS = 256;
 #ifndef STROM_HREG_WIDE
 #define STROM_HREG_WIDE 15  // k_u > 16 (240 registers): register Gram for up to 15 upper tiles (K <= 40)
 #endif
-#ifndef STROM_GFRAG
-#define STROM_GFRAG 1  // gradient S / T accumulated from the J accumulator fragments (0: from Jt in shared memory)
-#endif
-#ifndef STROM_HDIRECT
-#define STROM_HDIRECT 0  // Gram DMMAs accumulate straight into the register Gram on sqrt(rho)-scaled fragments
-#endif
 #ifndef STROM_MMA_MAXNREG
 #define STROM_MMA_MAXNREG 168  // 3 warps per SMSP (12 per SM with 15 KB of smem per warp)
 #endif
 // Measured and removed in round 2 (DESIGN.md §3 table): buffered three-face out-blocks,
 // register prefetch of the projection B fragments, cp.async staging of the next basis block,
-// the dR/dx stage in the L-GEMM shadow, L1 / L2 neighbor-row prefetch, flipped J stores.
+// the dR/dx stage in the L-GEMM shadow, L1 / L2 neighbor-row prefetch, flipped J stores, the gradient from Jt
+// in shared memory instead of the J fragments, Gram DMMAs accumulating straight into the register Gram.
 
 template <int NQ>
 struct MShape {
@@ -1019,7 +1014,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
     }
     // ---- write J_U, then J_x = (dR/dx) Psi_e on DMMA, into Jt (region A, phase 3) --------
     double* Jt = RA;
-    constexpr bool GFRAG = CT && STROM_GFRAG;  // gradient from the J accumulator fragments
+    constexpr bool GFRAG = CT;  // gradient from the J accumulator fragments
     const bool gfrag = GFRAG && DERIVS;
     double rr[3];  // rho * R at the lane's three projection rows
 #pragma unroll
@@ -1103,25 +1098,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
 #pragma unroll
           for (int rs = 0; rs < NU / 4; ++rs) fr[cc][rs] = Jt[(rs * 4 + (lane & 3)) * LDJ + cc * 8 + (lane >> 2)];
         constexpr int NTRI = NT8C * (NT8C + 1) / 2;
-        constexpr bool HDIRECT = HREG && STROM_HDIRECT;
-        if constexpr (HDIRECT) {
-          const double sr = sqrt(rho);
-#pragma unroll
-          for (int cc = 0; cc < NT8C; ++cc)
-#pragma unroll
-            for (int rs = 0; rs < NU / 4; ++rs) fr[cc][rs] *= sr;
-#pragma unroll
-          for (int rs = 0; rs < NU / 4; ++rs)
-#pragma unroll
-            for (int ti = 0; ti < NT8C; ++ti)
-#pragma unroll
-              for (int tj = ti; tj < NT8C; ++tj) {
-                const int t = SH::tri_tile(ti, tj, NT8C);
-                dmma(hacc[t][0], hacc[t][1], fr[ti][rs], fr[tj][rs]);
-              }
-        }
-        double gc[HDIRECT ? 1 : NTRI][2];  // all upper tiles in flight: k-step outer, independent chains inner
-        if constexpr (!HDIRECT) {
+        double gc[NTRI][2];  // all upper tiles in flight: k-step outer, independent chains inner
 #pragma unroll
         for (int t = 0; t < NTRI; ++t) gc[t][0] = gc[t][1] = 0.0;
 #pragma unroll
@@ -1133,8 +1110,6 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
               const int t = SH::tri_tile(ti, tj, NT8C);
               dmma(gc[t][0], gc[t][1], fr[ti][rs], fr[tj][rs]);
             }
-        }
-        if constexpr (!HDIRECT)
 #pragma unroll
         for (int ti = 0; ti < NT8C; ++ti)
 #pragma unroll
@@ -1231,7 +1206,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
   if (!DERIVS) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) jacc += __shfl_xor_sync(0xffffffffu, jacc, o);
-  if constexpr (CT && STROM_GFRAG) {
+  if constexpr (CT) {
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1)
 #pragma unroll

@@ -16,26 +16,8 @@
 namespace strom {
 
 constexpr int VM_THREADS = 128;
-#ifndef VM_NTB_OWN
-#define VM_NTB_OWN 4
-#endif
-#ifndef VM_NTB_F
-#define VM_NTB_F 4
-#endif
-#ifndef VM_USMEM
-#define VM_USMEM 1  // U and the neighbor face values read from the warp tile (no register copies)
-#endif
-#ifndef VM_UQ
-#define VM_UQ 1  // volume-point loop unroll
-#endif
-#ifndef VM_US
-#define VM_US 1  // face-point loop unroll
-#endif
-#ifndef VM_MINB
-#define VM_MINB (VM_USMEM ? 3 : 2)
-#endif
-constexpr int kVmUq = VM_UQ, kVmUs = VM_US;
-static_assert(VM_USMEM, "the coordinate reconstruction stages through the face rows of the warp tile");
+constexpr int VM_NTB_OWN = 4, VM_NTB_F = 4;  // column tiles per reconstruction pass (own rows / face rows)
+constexpr int VM_MINB = 3;                    // 3 CTAs of 4 warps per SM at 168 registers (4 CTAs = 128 registers spill: +50%)
 constexpr int VM_LDU = 40;  // tile row stride: == 8 mod 16 -> conflict-free double2 C-fragment stores
 constexpr int VM_LDW = 36;  // W row stride: == 4 mod 16 -> conflict-free B-fragment loads
 
@@ -44,9 +26,8 @@ struct VShape {
   static constexpr int M = LAW::M, NU = NB * M, P = NB == 3 ? 1 : (NB == 6 ? 2 : 3), NF = P + 1;
   static constexpr int NFR = NF * M;                      // one face's neighbor rows
   static constexpr int MT_OWN = (NU + 7) / 8, MT_F = (NFR + 7) / 8;
-  static constexpr int MTB = MT_OWN > MT_F ? MT_OWN : MT_F;
-  static constexpr int FROW = VM_USMEM ? MT_OWN * 8 : 0;   // first face row of the tile
-  static constexpr int TILE = (VM_USMEM ? MT_OWN * 8 + MT_F * 8 : MTB * 8) * VM_LDU;  // doubles per warp
+  static constexpr int FROW = MT_OWN * 8;                   // first face row of the tile
+  static constexpr int TILE = (MT_OWN * 8 + MT_F * 8) * VM_LDU;  // doubles per warp
 };
 
 // rows r < nrows of the warp tile <- U0 + Phi[row(r)] . W  for the CTA's 32 points,
@@ -163,16 +144,8 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
     // ---- own rows
     vm_recon<VS::MT_OWN, VM_NTB_OWN>(r, Ws, tile, NU, [&](int rr) { return e * NU + rr; }, s_prow, lane);
     __syncwarp();
-#if VM_USMEM
-    const double* U = tile + lane;  // U[i * VM_LDU]
+    const double* U = tile + lane;  // the lane's column of the warp tile: U[i * VM_LDU]
 #define VM_U(i) U[(i) * VM_LDU]
-#else
-    double U[NU];
-#pragma unroll
-    for (int i = 0; i < NU; ++i) U[i] = tile[i * VM_LDU + lane];
-    __syncwarp();
-#define VM_U(i) U[i]
-#endif
     // ---- geometry (value_unit, element_kernels.cuh): the six deformed vertex coordinates
     // x = X_ref + Psi_rows tau of the 32 points as one more DMMA reconstruction through the
     // face rows of the tile (free until the first face), each lane then reads its column
@@ -197,8 +170,8 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
     double R[NU];
 #pragma unroll
     for (int i = 0; i < NU; ++i) R[i] = 0.0;
-    // ---- volume (dg.py:105-125)
-#pragma unroll kVmUq
+    // ---- volume (dg.py:105-125); the point loops stay rolled (unrolling spills: neutral to -5%)
+#pragma unroll 1
     for (int q = 0; q < NQ; ++q) {
       double uq[M];
 #pragma unroll
@@ -239,29 +212,21 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
       const int nb = r.nbr[3 * e + f];
       const int fi = r.finfo[3 * e + f];
       const int bc = fi >> 3;
-      double Un[NF][M];
       int flip = 0;
       if (bc == 0) {  // warp-uniform (one element per warp)
         const int nf = fi & 3;
         flip = (fi >> 2) & 1;
-        if (VM_USMEM) __syncwarp();  // the previous face's reads of the face rows are done
+        __syncwarp();  // the previous face's reads of the face rows are done
         vm_recon<VS::MT_F, VM_NTB_F>(r, Ws, tile + VS::FROW * VM_LDU, NFR, [&](int rr) {
           const int j = rr / M, c = rr % M;
           const int node = j == 0 ? nf : (j == 1 ? (nf + 1) % 3 : 3 + nf * (PD - 1) + (j - 2));
           return nb * NU + node * M + c;
         }, s_prow, lane);
         __syncwarp();
-        if (!VM_USMEM) {
-#pragma unroll
-          for (int j = 0; j < NF; ++j)
-#pragma unroll
-            for (int c = 0; c < M; ++c) Un[j][c] = tile[(VS::FROW + j * M + c) * VM_LDU + lane];
-          __syncwarp();
-        }
       }
       double ghost[M];
       if (bc >= 2 && bc != BC_REFLECT) LAW::ghost(bc - 2, la, ghost);
-#pragma unroll kVmUs
+#pragma unroll 1
       for (int s = 0; s < NS; ++s) {
         double ui[M], uo[M];
 #pragma unroll
@@ -278,7 +243,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
             double v = 0.0;
 #pragma unroll
             for (int j = 0; j < NF; ++j)
-              v = fma(T.trace[0][sp][j], VM_USMEM ? tile[(VS::FROW + j * M + c) * VM_LDU + lane] : Un[j][c], v);
+              v = fma(T.trace[0][sp][j], tile[(VS::FROW + j * M + c) * VM_LDU + lane], v);
             uo[c] = v;
           }
         } else if (bc == 1) {

@@ -1,4 +1,4 @@
 # quick GPU session: parity tests + short bench (no CPU baselines, no sharded configs)
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -q -rs > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-python bench.py --steps 50 --no-cpu-baseline --no-sharded > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+python bench.py --steps 50 --no-cpu-baseline --no-sharded --no-fullspace > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
