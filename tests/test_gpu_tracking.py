@@ -260,3 +260,49 @@ def test_scalar_tracking_lm_matches_reference(name):
     assert np.array_equal(hist[:, 5], ref[:, 5]) and rel_err(hist[:, 4], ref[:, 4]) < 1e-8
     assert rel_err(hist[:, 1], ref[:, 1], np.max(np.abs(ref[:, 1]))) < 1e-8
     assert rel_err(res.w, g["fs_lm_w"]) < 1e-7
+
+
+@pytest.mark.parametrize("kind", ["euler_p1", "strip_p2", "burgers_p1_default"])
+def test_warp_kernel_blocks_match_oracle(kind):
+    """The warp kernel's element-block contraction on the cases the goldens do not reach: Euler at
+    p = 1 (4 components, 3 nodes), the strip law (state-dependent source) and the space-time
+    Burgers law (position-dependent source) on the default 2q+2p+1 rule — plain (trial = test)
+    and enriched (p + 1) blocks against the oracle's dual-number tangents."""
+    from oracle.element import element_eval
+    import oracle.dual as D
+    from paper_2305_15661_b200 import laws as L
+    from paper_2305_15661_b200.fullspace import element_blocks
+    from paper_2305_15661_b200.mesh import build_box_mesh, get_geometry
+
+    rng = np.random.default_rng(33)
+    if kind == "euler_p1":
+        mesh, maps = build_box_mesh(((0.0, 0.0), (1.0, 1.0)), 3, 2, degree_sol=1, n_comp=4)
+        law = L.euler(tags={"left": "freestream", "bottom": "freestream", "right": "extrapolate", "top": "extrapolate"})
+        U = np.tile(L.euler_freestream(2.5), mesh.num_elements * 3) * (1.0 + 0.03 * rng.standard_normal(mesh.num_elements * 12))
+        mu, qo = np.array([2.5]), None
+    elif kind == "strip_p2":
+        mesh, maps = build_box_mesh(((0.0, 0.0), (1.0, 0.125)), 8, 1, degree_sol=2, n_comp=1)
+        law, mu, qo = L.burgers_strip(), np.array([2.0]), None
+        U = 0.5 + 0.3 * rng.standard_normal(maps.n_global_state)
+    else:
+        mesh, maps = build_box_mesh(((0.0, 0.0), (2.0, 1.0)), 3, 2, degree_sol=1, n_comp=1)
+        law, mu, qo = L.burgers_spacetime(), np.array([5.0, 0.05]), None
+        U = 3.0 + 0.5 * rng.standard_normal(maps.n_global_state)
+    geom = get_geometry(mesh, maps, qo)
+    x = mesh.nodes.ravel() + 0.01 * rng.standard_normal(mesh.nodes.size) * np.min(np.ptp(mesh.nodes, axis=0)) / 8
+    og = OracleGeometry(mesh, maps, qo)
+    els = np.arange(mesh.num_elements)
+    Ue, Un = og.gather_state(U, els)
+    xe = og.gather_coords(x, els)
+    nu = og.n_basis * og.n_comp
+    T = 4 * nu + 6
+    seeds = (D.seed_identity(Ue, 0, T), D.seed_identity(Un, nu, T), D.seed_identity(xe, 4 * nu, T))
+    ok = np.repeat(maps.neighbor_map.reshape(len(els), 3, nu)[:, :, 0] >= 0, nu, axis=1)
+    for deg in (None, maps.degree_sol + 1):
+        out = element_eval(law, og, els, *seeds, mu, test=None if deg is None else og.test_space(deg))
+        res, js, jn, jc, _, _ = element_blocks(law, geom, U, x, mu, deg)
+        tan = out.res.tan
+        scale = np.max(np.abs(tan))
+        assert rel_err(res, out.res.val, max(np.max(np.abs(out.res.val)), 1e-6 * scale)) < 1e-9
+        assert rel_err(js, tan[:, :, :nu], scale) < TOL and rel_err(jc, tan[:, :, 4 * nu:], scale) < TOL
+        assert rel_err(jn * ok[:, None, :], tan[:, :, nu:4 * nu] * ok[:, None, :], scale) < TOL
