@@ -315,7 +315,9 @@ def lm_solve(problem, config=None, w0_mode="lsq"):
     as the device-resident batched state machine; any other protocol problem (full-space
     tracking, alignment: GPU-assembled sparse blocks) runs the host loop above."""
     op = getattr(problem, "op", None)
-    if not isinstance(op, GpuReducedOperator):
+    if not isinstance(op, GpuReducedOperator) or getattr(op, "_pad", 0):
+        # protocol problems, and the tau-only reduced problem (k_u = 0, reduced.py:197-199: the
+        # batched device LM needs a state block): host loop over the GPU evaluations
         if all(hasattr(problem, a) for a in ("initial_guess", "objective", "derivatives")):
             return lm_solve_protocol(problem, config, w0_mode)
         raise NotImplementedError("lm_solve needs a GpuReducedOperator problem or a protocol problem")

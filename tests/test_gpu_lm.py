@@ -132,3 +132,28 @@ def test_gpu_lm_graph_reuse_is_deterministic():
     st = (ctypes.c_int32 * 3)()
     _lib.check(_lib.load().strom_lm_stats(op._h, st), "strom_lm_stats")
     assert st[0] > 0 and st[1] > 0 and st[2] > 0
+
+
+def test_tau_only_lm_matches_oracle():
+    """k_u = 0 (no state basis): lm.lm_solve runs its protocol loop over the GPU operator and
+    follows the oracle's LM (pinned to the reference) step for step."""
+    import oracle.dual  # noqa: F401
+    from oracle.element import OracleGeometry, OracleReducedOperator
+    from oracle import lm as olm
+    from paper_2305_15661_b200 import configs
+    from paper_2305_15661_b200.lm import LmConfig, ReducedTrackingProblem, lm_solve
+    from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases
+
+    case = configs.euler_square_case(n=4, ku=16, kx=8, seed=12)
+    phi0 = np.zeros((case.phi.shape[0], 0))
+    op = GpuReducedOperator(case.law, case.geom, ReducedBases(phi0, case.psi, case.ref_coords), case.dist,
+                            state_offset=case.state_offset)
+    ref = OracleReducedOperator(case.law, OracleGeometry(case.mesh, case.maps, case.quad_order), phi0, case.psi,
+                                case.ref_coords, case.kappa, case.eps, state_offset=case.state_offset)
+    tau0 = 2e-3 * np.random.default_rng(4).standard_normal(8)
+    got = lm_solve(ReducedTrackingProblem(op, case.mus[0], tau0=tau0), LmConfig(max_iters=6))
+    want = olm.lm_solve(olm.OracleProblem(ref, case.mus[0], tau0=tau0), olm.LmConfig(max_iters=6))
+    assert got.n_iters == want.n_iters and got.reason == want.reason and got.w.shape == (0,)
+    assert np.array_equal(got.history[:, 5], want.history[:, 5], equal_nan=True)
+    assert np.allclose(got.history[:, 1:5], want.history[:, 1:5], rtol=1e-8, atol=1e-14)
+    assert np.allclose(got.tau, want.tau, rtol=1e-8, atol=1e-12)
