@@ -130,7 +130,7 @@ def lm_solve_batched(op, mus, W0=None, Tau0=None, rho=None, config=None, w0_mode
     if not isinstance(op, GpuReducedOperator):
         raise TypeError("lm_solve_batched needs a GpuReducedOperator")
     if getattr(op, "_pad", 0):
-        raise NotImplementedError("the batched GPU LM needs k_u >= 1 (the reference's tau-only LM is not ported)")
+        raise NotImplementedError("the batched device LM needs k_u >= 1; the tau-only problem runs through lm_solve (protocol loop)")
     if w0_mode not in ("lsq", "keep"):
         raise ValueError(f"unknown w0_mode {w0_mode!r}")
     cfg = as_config(config)
