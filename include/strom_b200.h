@@ -167,6 +167,10 @@ int strom_lm_stats(strom_handle* h, int32_t* out3);
  * derivatives pass, only the objective pass, both). */
 int strom_lm_timing(strom_handle* h, double* out4);
 
+/* Rows evaluated by the last strom_lm_solve: out2 = (parameter rows summed over the derivatives
+ * passes, trial rows summed over the objective passes). */
+int strom_lm_rows(strom_handle* h, double* out2);
+
 /* Benchmark probe: while enabled, the dominant kernel of every strom_eval is
  * bracketed by CUDA events recorded on the call's stream (capacity 4096
  * launches).  strom_profile_ms synchronizes on the recorded events and

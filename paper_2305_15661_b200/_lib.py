@@ -30,7 +30,7 @@ class DistDesc(C.Structure):
 
 EXPORTS = ("strom_create", "strom_set_bases", "strom_set_offsets", "strom_set_test_space", "strom_reserve", "strom_eval", "strom_eval_host",
            "strom_degenerate_elements",
-           "strom_lm_solve", "strom_lm_stats", "strom_lm_timing", "strom_profile", "strom_profile_ms", "strom_last_error", "strom_destroy")
+           "strom_lm_solve", "strom_lm_stats", "strom_lm_timing", "strom_lm_rows", "strom_profile", "strom_profile_ms", "strom_last_error", "strom_destroy")
 
 _lib = None
 
@@ -60,6 +60,7 @@ def load(path=SO_PATH):
     lib.strom_lm_solve.argtypes = [vp, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp, vp]
     lib.strom_lm_stats.argtypes = [vp, vp]
     lib.strom_lm_timing.argtypes = [vp, vp]
+    lib.strom_lm_rows.argtypes = [vp, vp]
     lib.strom_profile.argtypes = [vp, i32]
     lib.strom_profile_ms.argtypes = [vp, C.POINTER(i32)]
     lib.strom_profile_ms.restype = C.c_double

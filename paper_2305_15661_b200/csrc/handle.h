@@ -92,6 +92,7 @@ struct strom_handle {
   unsigned long long epoch = 0;      // bumped whenever bases / offsets change (graph key)
   // statistics of the last strom_lm_solve: control rounds, derivative / objective passes
   int lm_rounds = 0, lm_dpasses = 0, lm_opasses = 0;
+  double lm_rows[2] = {0, 0};      // rows evaluated by the derivatives / objective passes of the last solve
   double lm_ms[4] = {0, 0, 0, 0};  // device time of the last solve: control rounds, d-only / o-only / d+o pass gaps
   bool prof = false;
   std::vector<cudaEvent_t> ev;

@@ -63,6 +63,7 @@ struct LmCtl {
   // ends; the gaps between a round end and the next round's start are the batched passes
   unsigned long long t_start, t_end;
   unsigned long long ns_ctl, ns_d, ns_o, ns_do;  // control rounds; gaps after rounds that ran d only / o only / both
+  unsigned long long rows_d, rows_o;             // rows evaluated by the derivatives / objective passes (statistics)
 };
 
 struct LmRun {
@@ -622,6 +623,8 @@ static __device__ void lm_round_end(const LmRun& R, cudaGraphConditionalHandle h
   C.ran_o = run_o;
   C.nd += run_d;
   C.no += run_o;
+  if (run_d) C.rows_d += nder;
+  if (run_o) C.rows_o += nobj;
   C.dcount = nder;
   C.ocount = nobj;
   C.round += 1;

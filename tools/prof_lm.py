@@ -29,5 +29,8 @@ print("rounds, derivative passes, objective passes:", list(st))
 tm = (ctypes.c_double * 4)()
 _lib.load().strom_lm_timing(op._h, tm)
 print("device ms: control %.2f, after d-only rounds %.2f, o-only %.2f, d+o %.2f" % tuple(tm))
+rw = (ctypes.c_double * 2)()
+_lib.load().strom_lm_rows(op._h, rw)
+print("rows evaluated: derivatives %d (%.1f per mu), objective trials %d (%.1f per mu)" % (rw[0], rw[0] / len(res), rw[1], rw[1] / len(res)))
 # per-kernel times of the graph's kernel nodes: run under
 #   ncu --metrics gpu__time_duration.sum --csv python tools/prof_lm.py 3  (tools/launch_summary.py)
