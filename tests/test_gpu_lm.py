@@ -157,3 +157,27 @@ def test_tau_only_lm_matches_oracle():
     assert np.array_equal(got.history[:, 5], want.history[:, 5], equal_nan=True)
     assert np.allclose(got.history[:, 1:5], want.history[:, 1:5], rtol=1e-8, atol=1e-14)
     assert np.allclose(got.tau, want.tau, rtol=1e-8, atol=1e-12)
+
+
+def test_lm_statistics_entry_points():
+    """strom_lm_stats / strom_lm_timing / strom_lm_rows after a batched solve: consistent counts
+    (every mu needs at least one derivatives row per iteration) and non-negative device times."""
+    import ctypes
+
+    from paper_2305_15661_b200 import _lib, configs
+    from paper_2305_15661_b200.eqp import WeightVector
+    from paper_2305_15661_b200.lm import LmConfig, lm_solve_batched
+    from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases
+
+    case = configs.sector_rom_case(n_radial=4, n_circ=6, ku=6, kx=4, frac_active=0.25, rho_scale=4.0, P=5, seed=13)
+    op = GpuReducedOperator(case.law, case.geom, ReducedBases(case.phi, case.psi, case.ref_coords), case.dist)
+    res = lm_solve_batched(op, case.mus, case.W[0], None, WeightVector(case.rho), LmConfig(max_iters=6))
+    lib = _lib.load()
+    st, tm, rw = (ctypes.c_int32 * 3)(), (ctypes.c_double * 4)(), (ctypes.c_double * 2)()
+    assert lib.strom_lm_stats(op._h, st) == 0 and lib.strom_lm_timing(op._h, tm) == 0 and lib.strom_lm_rows(op._h, rw) == 0
+    rounds, nd, no = list(st)
+    assert rounds >= nd >= 1 and rounds >= no >= 1
+    assert all(t >= 0.0 for t in tm) and sum(tm) > 0.0
+    assert rw[0] >= sum(r.n_iters for r in res) and rw[1] >= sum(r.n_iters for r in res)
+    assert rw[0] <= nd * len(res) and rw[1] <= no * len(res) * 4
+    assert lib.strom_lm_rows(op._h, None) < 0  # null output: argument error
