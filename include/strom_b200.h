@@ -44,7 +44,9 @@ typedef struct {
 /* Compiled conservation law (replaces the Python callables of
  * ConservationLawSpec, strom/conslaw.py:32-57). */
 typedef struct {
-  int32_t law_id;     /* 0 linear-advection, 1 burgers-spacetime, 2 burgers-strip, 3 euler */
+  int32_t law_id;     /* 0 linear-advection, 1 burgers-spacetime, 2 burgers-strip, 3 euler, 4 euler + Roe flux,
+                         5 euler on a mesh with slip walls, 6 linear advection with the manufactured solution
+                         u = a0 + a1 exp(k1 x + k2 y) (position-dependent source and inflow ghosts) */
   int32_t n_comp;     /* m */
   int32_t n_mu;       /* parameters per mu vector */
   double params[8];   /* law constants (velocity, gamma, boundary states) */

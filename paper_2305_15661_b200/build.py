@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.environ.get("STROM_SO_OUT") or os.path.join(HERE, "_strom_b200.so")  # variant builds for A/B runs
 CSRC = os.path.join(HERE, "csrc")
-UNITS = ["capi.cu", "law_euler.cu", "law_euler_roe.cu", "law_strip.cu", "law_burgers_st.cu", "law_linadv.cu"]
+UNITS = ["capi.cu", "law_euler.cu", "law_euler_roe.cu", "law_strip.cu", "law_burgers_st.cu", "law_linadv.cu", "law_linadv_ms.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

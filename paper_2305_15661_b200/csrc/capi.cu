@@ -41,6 +41,7 @@ static int dispatch(strom_handle* h, const EvalArgs& a) {
     case 3: return eval_euler(h, a);
     case 4: return eval_euler_roe(h, a);
     case 5: return eval_euler_wall(h, a);
+    case 6: return eval_linadv_ms(h, a);
     default: return fail(-1, "unknown law id");
   }
 }

@@ -394,7 +394,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
       const bool wall = LAW::WALLS && bc == BC_REFLECT;  // slip wall: exterior = R(nh) u_in
       if (side && bc >= 2) {
         if (wall) reflect_state(us, nh, us);
-        else LAW::ghost(bc - 2, la, us);
+        else LAW::ghost(bc - 2, la, nullptr, us);  // 4-component laws: constant ghosts
       }
       // A(n) is linear in n: evaluated along sc * nu it comes out already scaled by the face
       // weight and the LLF 1/2 (weight 1 on an extrapolated exterior, whose C_out folds into
@@ -558,7 +558,7 @@ __global__ void __maxnreg__(MShape<NQ>::wide(KUT) ? STROM_MMA_MAXNREG_WIDE : STR
         } else if (wall) {
           reflect_state(ui, nh, uo);
         } else {
-          LAW::ghost(bc - 2, la, uo);
+          LAW::ghost(bc - 2, la, nullptr, uo);
         }
         if (!dz) {
           // dD/du_side in two passes of two seeded components each (Dn<2>: fewer live values)

@@ -270,7 +270,14 @@ __global__ void __launch_bounds__(WTHREADS) derivs_warp_kernel(
 #pragma unroll
         for (int c = 0; c < M; ++c) uo[c] = ui[c];
       } else {
-        LAW::ghost(bc - 2, la, uo);
+        // deformed position of the face point: the vertex part of the trace (the edge-node
+        // function splits evenly between the two vertices on a straight face)
+        const int va = f, vb = (f + 1) % 3;
+        const double half = NF > 2 ? 0.5 * T.trace[f][s][NF - 1] : 0.0;
+        const double la_ = T.trace[f][s][0] + half, lb_ = T.trace[f][s][1] + half;
+        const double pos[2] = {la_ * S[SH::MX + 2 * va] + lb_ * S[SH::MX + 2 * vb],
+                               la_ * S[SH::MX + 2 * va + 1] + lb_ * S[SH::MX + 2 * vb + 1]};
+        LAW::ghost(bc - 2, la, pos, uo);
       }
       double fni[M], fno[M], Ai[M][M], Ao[M][M];
       PointOps<LAW>::flux_dir(ui, nu, fni, Ai, la);

@@ -324,7 +324,7 @@ __device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB,
       }
     }
     double ghost[M];
-    if (bc >= 2 && bc != BC_REFLECT) LAW::ghost(bc - 2, la, ghost);
+    if (bc >= 2 && bc != BC_REFLECT && !LAW::GHOST_POS) LAW::ghost(bc - 2, la, nullptr, ghost);
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       double ui[M], uo[M];
@@ -348,6 +348,13 @@ __device__ __forceinline__ void value_unit(const Tabs<NB, NQ, NS, Shape<LAW, NB,
 #pragma unroll
         for (int c = 0; c < M; ++c) uo[c] = ui[c];
       } else {
+      if constexpr (LAW::GHOST_POS) {  // ghost at the deformed face point (vertex part of the trace)
+        const int va = f, vb = (f + 1) % 3;
+        const double half = NF > 2 ? 0.5 * T.trace[f][s][NF - 1] : 0.0;
+        const double la_ = T.trace[f][s][0] + half, lb_ = T.trace[f][s][1] + half;
+        const double pos[2] = {la_ * x[2 * va] + lb_ * x[2 * vb], la_ * x[2 * va + 1] + lb_ * x[2 * vb + 1]};
+        LAW::ghost(bc - 2, la, pos, ghost);
+      }
 #pragma unroll
         for (int c = 0; c < M; ++c) uo[c] = ghost[c];
       }

@@ -103,6 +103,7 @@ namespace strom_host {
 int ensure_part(strom_handle* h, size_t n);
 void prof_mark(strom_handle* h, cudaStream_t st, int which);
 int eval_linadv(strom_handle* h, const EvalArgs& a);
+int eval_linadv_ms(strom_handle* h, const EvalArgs& a);
 int eval_burgers_st(strom_handle* h, const EvalArgs& a);
 int eval_strip(strom_handle* h, const EvalArgs& a);
 int eval_euler(strom_handle* h, const EvalArgs& a);

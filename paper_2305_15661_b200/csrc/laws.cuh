@@ -120,6 +120,7 @@ struct LinAdv {
   static constexpr bool WALLS = false;
   static constexpr int M = 1;
   static constexpr int SRC = SRC_NONE;
+  static constexpr bool GHOST_POS = false;  // prescribed ghosts depend on the face-point position
   template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
     f[0][0] = a.p[0] * u[0];
     f[0][1] = a.p[1] * u[0];
@@ -130,7 +131,35 @@ struct LinAdv {
   template <class T> __device__ static T wavespeed(const T* u, const T* n, const LawArgs& a) {
     return dabs(a.p[0] * n[0] + a.p[1] * n[1]) + 0.0 * u[0];
   }
-  __device__ static void ghost(int id, const LawArgs& a, double* out) { out[0] = 1.0; }
+  __device__ static void ghost(int id, const LawArgs& a, const double* pos, double* out) { out[0] = 1.0; }
+};
+
+// linear advection with the manufactured solution u(x, y) = a0 + a1 exp(k1 x + k2 y)
+// (conslaw.py:174-253 with manufactured = (u_exact, grad_exact)): source c . grad u_exact at the
+// deformed position (it enters the x-Jacobian, dg.py:113,121), inflow ghosts u_exact at the
+// deformed face points (value only, no x-derivative, dg.py:151-161).
+// params: c0, c1, a0, a1, k1, k2
+struct LinAdvMS {
+  static constexpr bool ANALYTIC = false;
+  static constexpr bool ROE = false;
+  static constexpr bool WALLS = false;
+  static constexpr int M = 1;
+  static constexpr int SRC = SRC_POS;
+  static constexpr bool GHOST_POS = true;
+  template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
+    f[0][0] = a.p[0] * u[0];
+    f[0][1] = a.p[1] * u[0];
+  }
+  template <class T> __device__ static void source(const T* pos, const T* u, T* s, const LawArgs& a) {
+    const T e = a.p[3] * dexp(a.p[4] * pos[0] + a.p[5] * pos[1]);
+    s[0] = a.p[0] * (a.p[4] * e) + a.p[1] * (a.p[5] * e) + 0.0 * u[0];
+  }
+  template <class T> __device__ static T wavespeed(const T* u, const T* n, const LawArgs& a) {
+    return dabs(a.p[0] * n[0] + a.p[1] * n[1]) + 0.0 * u[0];
+  }
+  __device__ static void ghost(int id, const LawArgs& a, const double* pos, double* out) {
+    out[0] = a.p[2] + a.p[3] * exp(a.p[4] * pos[0] + a.p[5] * pos[1]);
+  }
 };
 
 // space-time Burgers, conslaw.py:94-163
@@ -140,6 +169,7 @@ struct BurgersST {
   static constexpr bool WALLS = false;
   static constexpr int M = 1;
   static constexpr int SRC = SRC_POS;
+  static constexpr bool GHOST_POS = false;
   template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
     f[0][0] = 0.5 * u[0] * u[0];
     f[0][1] = u[0];
@@ -151,7 +181,7 @@ struct BurgersST {
     T v = u[0] * n[0] + n[1];
     return dsqrt(v * v + 1e-6);
   }
-  __device__ static void ghost(int id, const LawArgs& a, double* out) { out[0] = id == 0 ? a.mu[0] : 1.0; }
+  __device__ static void ghost(int id, const LawArgs& a, const double* pos, double* out) { out[0] = id == 0 ? a.mu[0] : 1.0; }
 };
 
 // steady Burgers strip (config 1): (u^2/2)_x = mu u
@@ -161,6 +191,7 @@ struct BurgersStrip {
   static constexpr bool WALLS = false;
   static constexpr int M = 1;
   static constexpr int SRC = SRC_U;
+  static constexpr bool GHOST_POS = false;
   template <class T> __device__ static void flux(const T* u, T (*f)[2], const LawArgs& a) {
     f[0][0] = 0.5 * u[0] * u[0];
     f[0][1] = 0.0 * u[0];
@@ -172,7 +203,7 @@ struct BurgersStrip {
     T v = u[0] * n[0];
     return dsqrt(v * v + 1e-6);
   }
-  __device__ static void ghost(int id, const LawArgs& a, double* out) { out[0] = id == 0 ? a.p[0] : a.p[1]; }
+  __device__ static void ghost(int id, const LawArgs& a, const double* pos, double* out) { out[0] = id == 0 ? a.p[0] : a.p[1]; }
 };
 
 // compressible Euler, conservative (rho, rho u, rho v, E); LLF speed |v.n| + c
@@ -182,6 +213,7 @@ struct Euler {
   static constexpr bool WALLS = false;  // slip-wall faces compiled in (EulerWall / EulerRoe)
   static constexpr int M = 4;
   static constexpr int SRC = SRC_NONE;
+  static constexpr bool GHOST_POS = false;
   // fn = f(u).n and A = d(f.n)/du for a (not necessarily unit) direction n
   __device__ static void flux_dir(const double* u, const double* n, double* fn, double (*A)[4], const LawArgs& a) {
     const double g = a.p[0], gm = g - 1.0;
@@ -344,7 +376,7 @@ struct Euler {
     T vn = vx * n[0] + vy * n[1];
     return dabs(vn) + dsqrt(g * p / u[0]);
   }
-  __device__ static void ghost(int id, const LawArgs& a, double* out) {
+  __device__ static void ghost(int id, const LawArgs& a, const double* pos, double* out) {
     const double g = a.p[0], mach = a.mu[0], p = 1.0 / g;
     out[0] = 1.0; out[1] = mach; out[2] = 0.0; out[3] = p / (g - 1.0) + 0.5 * mach * mach;
   }

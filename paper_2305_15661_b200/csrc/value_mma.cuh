@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
         __syncwarp();
       }
       double ghost[M];
-      if (bc >= 2 && bc != BC_REFLECT) LAW::ghost(bc - 2, la, ghost);
+      if (bc >= 2 && bc != BC_REFLECT && !LAW::GHOST_POS) LAW::ghost(bc - 2, la, nullptr, ghost);
 #pragma unroll 1
       for (int s = 0; s < NS; ++s) {
         double ui[M], uo[M];
@@ -250,6 +250,13 @@ __global__ void __launch_bounds__(VM_THREADS, VM_MINB) value_mma_kernel(const __
 #pragma unroll
           for (int c = 0; c < M; ++c) uo[c] = ui[c];
         } else {
+          if constexpr (LAW::GHOST_POS) {  // ghost at the deformed face point (vertex part of the trace)
+            const int va = f, vb = (f + 1) % 3;
+            const double half = NF > 2 ? 0.5 * T.trace[f][s][NF - 1] : 0.0;
+            const double la_ = T.trace[f][s][0] + half, lb_ = T.trace[f][s][1] + half;
+            const double pos[2] = {la_ * x[2 * va] + lb_ * x[2 * vb], la_ * x[2 * va + 1] + lb_ * x[2 * vb + 1]};
+            LAW::ghost(bc - 2, la, pos, ghost);
+          }
 #pragma unroll
           for (int c = 0; c < M; ++c) uo[c] = ghost[c];
         }

@@ -30,6 +30,7 @@ LAW_BURGERS_STRIP = 2
 LAW_EULER = 3
 LAW_EULER_ROE = 4
 LAW_EULER_WALL = 5  # Euler (LLF) instantiated with slip-wall support (chosen when the mesh has walls)
+LAW_LINADV_MS = 6   # linear advection with the manufactured solution ExpManufactured
 
 BC_INTERIOR = 0
 BC_EXTRAPOLATE = 1
@@ -140,15 +141,70 @@ def _zero_like(x):
     return 0.0 * x
 
 
-def linear_advection(velocity=(1.0, 1.0)):
+class ExpManufactured:
+    """Manufactured solution u(x, y) = a0 + a1 exp(k1 x + k2 y) with a compiled device counterpart.
+
+    ``u`` and ``grad`` are the (dual-safe) callables the reference takes as
+    ``linear_advection(..., manufactured=(m.u, m.grad))`` (conslaw.py:174-225); a law built from
+    them — here or by the reference's own factory — maps to the device functor ``LinAdvMS``."""
+
+    def __init__(self, a0=1.0, a1=0.5, k1=0.7, k2=-0.4):
+        self.params = (float(a0), float(a1), float(k1), float(k2))
+
+    def _e(self, pos):
+        a0, a1, k1, k2 = self.params
+        return a1 * exp(k1 * pos[..., 0] + k2 * pos[..., 1])
+
+    def u(self, pos):
+        return self.params[0] + self._e(pos)
+
+    def grad(self, pos):
+        e = self._e(pos)
+        return (self.params[2] * e, self.params[3] * e)
+
+
+def _manufactured_of(obj):
+    """The ExpManufactured behind ``obj`` (the object, its (u, grad) pair, or a callable closing
+    over its bound methods — the reference's source / bc_value closures), or None."""
+    if isinstance(obj, ExpManufactured):
+        return obj
+    if isinstance(obj, (tuple, list)):
+        for o in obj:
+            m = _manufactured_of(o)
+            if m is not None:
+                return m
+        return None
+    owner = getattr(obj, "__self__", None)
+    if isinstance(owner, ExpManufactured):
+        return owner
+    for cell in getattr(obj, "__closure__", None) or ():
+        try:
+            m = _manufactured_of(cell.cell_contents)
+        except ValueError:  # empty cell
+            m = None
+        if m is not None:
+            return m
+    return None
+
+
+def linear_advection(velocity=(1.0, 1.0), manufactured=None):
+    """Constant-velocity advection (conslaw.py:174-253).  ``manufactured``: an ``ExpManufactured``
+    (or its ``(u, grad)`` pair): the source becomes c . grad u_exact and the inflow boundaries
+    prescribe u_exact at the deformed face points (conslaw.py:214-225)."""
     c = np.asarray(velocity, dtype=float)
+    ms = _manufactured_of(manufactured) if manufactured is not None else None
+    if manufactured is not None and ms is None:
+        raise NotImplementedError("manufactured solutions other than laws.ExpManufactured have no device functor")
 
     def flux(u, grad_u, mu):
         uc = u[..., 0]
         return _flux_from_rows([(c[0] * uc, c[1] * uc)])
 
     def source(pos, u, grad_u, mu):
-        return _comp_last(_zero_like(pos[..., 0]))
+        if ms is None:
+            return _comp_last(_zero_like(pos[..., 0]))
+        gx = ms.grad(pos)
+        return _comp_last(c[0] * gx[0] + c[1] * gx[1])
 
     def wavespeed(u, nhat, mu):
         ws = absolute(c[0] * nhat[..., 0] + c[1] * nhat[..., 1])
@@ -156,15 +212,24 @@ def linear_advection(velocity=(1.0, 1.0)):
             ws = ws + _zero_like(u[..., 0])
         return ws
 
+    def bc_value(pos, mu):
+        if ms is None:
+            return _const_state(pos, [1.0])
+        return np.asarray(ms.u(np.asarray(pos, dtype=float)))[..., None]
+
     bcs = {}
     for name, normal in (("left", (-1, 0)), ("right", (1, 0)), ("bottom", (0, -1)), ("top", (0, 1))):
         if c @ np.asarray(normal, dtype=float) < 0:
-            bcs[name] = BoundaryCondition("prescribed", lambda pos, mu: _const_state(pos, [1.0]), 0)
+            bcs[name] = BoundaryCondition("prescribed", bc_value, 0)
         else:
             bcs[name] = BoundaryCondition("extrapolate")
+    if ms is None:
+        return LawSpec("linear-advection", 1, 2, flux, source, None, wavespeed, bcs,
+                       np.array([[0.0, 1.0]]), lambda pos, mu: _const_state(pos, [1.0]),
+                       law_id=LAW_LINEAR_ADVECTION, params=(float(c[0]), float(c[1])))
     return LawSpec("linear-advection", 1, 2, flux, source, None, wavespeed, bcs,
                    np.array([[0.0, 1.0]]), lambda pos, mu: _const_state(pos, [1.0]),
-                   law_id=LAW_LINEAR_ADVECTION, params=(float(c[0]), float(c[1])))
+                   law_id=LAW_LINADV_MS, params=(float(c[0]), float(c[1]), *ms.params))
 
 
 def burgers_spacetime():
@@ -360,9 +425,13 @@ def _reference_law_id(law):
             raise NotImplementedError("gradient-dependent laws have no device functor")
         probe = np.asarray(law.flux(np.ones((1, 1)), None, np.zeros(1)), dtype=float).reshape(-1)
         src = np.asarray(law.source(np.full((1, 2), 0.37), np.ones((1, 1)), None, np.zeros(1)), dtype=float)
-        if np.any(src != 0.0):
-            raise NotImplementedError("manufactured linear-advection sources have no device functor")
         ghosts = {t: 0 for t, bc in law.boundary_data.items() if bc.kind == "prescribed"}
+        if np.any(src != 0.0):  # manufactured = (u_exact, grad_exact), conslaw.py:214-225
+            ms = _manufactured_of(law.source)
+            if ms is None:
+                raise NotImplementedError("manufactured linear-advection sources other than laws.ExpManufactured "
+                                          "have no device functor")
+            return LAW_LINADV_MS, (float(probe[0]), float(probe[1]), *ms.params), ghosts
         return LAW_LINEAR_ADVECTION, (float(probe[0]), float(probe[1])), ghosts
     raise NotImplementedError(f"no compiled device law for {name!r}")
 

@@ -46,7 +46,8 @@ def build(name):
         if name.startswith("burgers_st"):
             law = L.burgers_spacetime()
         else:
-            law = L.linear_advection((1.0, 0.5) if name == "linadv_p2" else (-0.7, 1.0))
+            law = L.linear_advection((1.0, 0.5) if name.endswith("p2") else (-0.7, 1.0),
+                                     manufactured=L.ExpManufactured() if name.startswith("linadv_ms") else None)
         case = configs.Case(name, law, mesh, maps, None, None, None, None, None, None, None)
     else:
         raise KeyError(name)
@@ -60,7 +61,7 @@ def build(name):
 
 
 EVAL_CASES = ["strip", "euler_square_q6", "euler_square_default", "sector", "burgers_st_p1", "burgers_st_p2",
-              "linadv_p1", "linadv_p2"]
+              "linadv_p1", "linadv_p2", "linadv_ms_p1", "linadv_ms_p2"]
 
 
 def rel_err(a, b, scale=None):

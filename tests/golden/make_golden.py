@@ -371,6 +371,12 @@ if __name__ == "__main__":
     case_reference_law(slaw.burgers_spacetime(), "burgers_st_p2", 2, ((0.0, 0.0), (2.0, 1.0)), 4, 3, (4.0, 0.03), 6, 3, 16)
     case_reference_law(slaw.linear_advection((1.0, 0.5)), "linadv_p2", 2, ((0.0, 0.0), (1.0, 1.0)), 3, 3, (0.5,), 5, 3, 17)
     case_reference_law(slaw.linear_advection((-0.7, 1.0)), "linadv_p1", 1, ((0.0, 0.0), (1.0, 1.0)), 4, 2, (0.5,), 4, 2, 18)
+    # the verification law with a manufactured solution (position-dependent source and inflow ghosts)
+    ms = L.ExpManufactured()
+    case_reference_law(slaw.linear_advection((1.0, 0.5), manufactured=(ms.u, ms.grad)), "linadv_ms_p2", 2,
+                       ((0.0, 0.0), (1.0, 1.0)), 3, 3, (0.5,), 5, 3, 19)
+    case_reference_law(slaw.linear_advection((-0.7, 1.0), manufactured=(ms.u, ms.grad)), "linadv_ms_p1", 1,
+                       ((0.0, 0.0), (1.0, 1.0)), 4, 2, (0.5,), 4, 2, 20)
     case_degenerate()
     case_cfg1()
     case_sector_shape("sector_k30", 6, 12, 20, 10, 0.25, 4, 51, 30)

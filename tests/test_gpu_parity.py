@@ -125,3 +125,28 @@ def test_graft_smoke_entry():
     import __graft_entry__
 
     __graft_entry__.smoke()
+
+
+def test_reference_manufactured_law_object_maps_to_device():
+    """A law built by the reference's own factory with manufactured = (m.u, m.grad)
+    (conslaw.py:174-225) runs on the GPU: the ExpManufactured behind its closures selects the
+    LinAdvMS functor (position-dependent source and inflow ghosts); other callables raise."""
+    try:
+        from oracle import strom_ref
+
+        S = strom_ref.load()
+    except ImportError:
+        pytest.skip("reference strom not installed")
+    from paper_2305_15661_b200 import laws as L
+    from paper_2305_15661_b200.reduced import GpuReducedOperator, ReducedBases, ReducedCoords
+
+    case, g = build("linadv_ms_p2")
+    ms = L.ExpManufactured()
+    rlaw = S["conslaw"].linear_advection((1.0, 0.5), manufactured=(ms.u, ms.grad))
+    op = GpuReducedOperator(rlaw, case.geom, ReducedBases(case.phi, case.psi, case.ref_coords), case.dist)
+    got = op.derivatives(ReducedCoords(g["w"], g["tau"]), case.mus[0])
+    for k, name in enumerate(("J", "S", "T", "Hww", "Hwt", "Htt")):
+        assert rel_err(got[k], g[f"der_all_{name}"]) < TOL, name
+    other = S["conslaw"].linear_advection((1.0, 0.5), manufactured=(lambda p: p[..., 0], lambda p: (1.0 + 0 * p[..., 0], 0 * p[..., 0])))
+    with pytest.raises(NotImplementedError):
+        GpuReducedOperator(other, case.geom, ReducedBases(case.phi, case.psi, case.ref_coords), case.dist)

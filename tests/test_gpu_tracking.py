@@ -218,7 +218,7 @@ def test_scalar_law_assembly_matches_reference(name):
     assert rel_err(JN @ g["v_x"], g["dist_JN_v"]) < TOL
 
 
-@pytest.mark.parametrize("name", ["burgers_st_p1", "burgers_st_p2", "linadv_p1", "linadv_p2", "strip"])
+@pytest.mark.parametrize("name", ["burgers_st_p1", "burgers_st_p2", "linadv_p1", "linadv_p2", "linadv_ms_p1", "linadv_ms_p2", "strip"])
 def test_scalar_element_jacobians_match_reference_goldens(name):
     """fullspace.element_jacobians for the scalar laws vs the reference's elemental_residual
     blocks stored in the round-1 goldens (dg.py:197-225)."""
