@@ -165,7 +165,10 @@ extern "C" int strom_set_test_space(strom_handle* h, int32_t nbt, const double* 
   if (!h) return fail(-1, "null handle");
   if (nbt < 1 || nbt > 64 || !phi || !dphi || !trace) return fail(-1, "strom_set_test_space: bad arguments");
   CK(cudaSetDevice(h->device));
-  if (h->test_tab) cudaFree(h->test_tab);
+  if (h->test_tab) {
+    CK(cudaDeviceSynchronize());  // an asynchronous evaluation may still read the previous table
+    cudaFree(h->test_tab);
+  }
   h->test_tab = nullptr;
   const size_t nd = (size_t)h->nq * nbt * 2, nt = (size_t)3 * h->ns * nbt, np = (size_t)h->nq * nbt;
   CK(cudaMalloc(&h->test_tab, (nd + nt + np) * sizeof(double)));  // [dphi | trace | phi]
